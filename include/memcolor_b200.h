@@ -1,0 +1,139 @@
+/*
+ * memcolor_b200.h -- C ABI of the B200-native batched local-search engine.
+ *
+ * Drop-in boundary for the data-parallel hot path of the reference package
+ * `memcolor` (arxiv 2109.05948; paths below are relative to
+ * /root/reference/pkg/src/memcolor/).  Each entry point replaces one numba
+ * kernel and takes exactly that kernel's arrays, as pointer + sizes, with
+ * the same in/out roles:
+ *
+ *   mcb_tabucol_batch  <- _tabucol_batch   localsearch.py:266-286 (body :287-410)
+ *   mcb_wvcp_batch     <- _wvcp_batch      localsearch.py:89-119  (body :120-263)
+ *   mcb_gpx_batch      <- _gpx_batch       crossover.py:60-66     (+ _gpx_into :14-57)
+ *   mcb_pairwise       <- _pairwise_kernel distance.py:90-119     (+ _greedy_match_total :40-72)
+ *   mcb_stream_values  <- stream_value     rng.py:56-59 (known-answer tests)
+ *
+ * Conventions
+ *  - Plain `mcb_*` functions take DEVICE pointers and enqueue on `stream`
+ *    (a cudaStream_t, NULL = legacy default stream); they do not synchronise
+ *    unless stated.  `mcb_*_host` variants take HOST pointers, perform the
+ *    host<->device copies themselves and return after the results are back
+ *    (the ctypes binding a reference maintainer adds).
+ *  - Array layouts are row-major and exactly the reference's dtypes:
+ *    assigns int32[p,n], adj_indptr int64[n+1], adj_indices int32[2m],
+ *    edges_u/edges_v int32[m], keys uint64[p], scalar outputs int64[p].
+ *  - Ownership follows `_run_tabucol_batch` (localsearch.py:556-598):
+ *    `assigns` is overwritten with the end state; every output is
+ *    preallocated by the caller.
+ *  - Errors: nonzero status; `mcb_last_error()` gives the message.  The
+ *    Python shim maps MCB_ERR_VALUE/UNSUPPORTED/RANGE to ValueError and
+ *    MCB_ERR_CUDA to RuntimeError; a nonzero `diag[i]` (incremental state
+ *    diverged from scratch recomputation, localsearch.py:398-405) is mapped to
+ *    AssertionError exactly like localsearch.py:589-590.
+ */
+#ifndef MEMCOLOR_B200_H
+#define MEMCOLOR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCB_OK 0
+#define MCB_ERR_VALUE 1
+#define MCB_ERR_CUDA 2
+#define MCB_ERR_UNSUPPORTED 3
+#define MCB_ERR_RANGE 4
+
+/* flags */
+#define MCB_FLAG_DIAG 0x1u         /* scratch re-evaluation every 1024 iterations (reference behaviour) */
+#define MCB_FLAG_PRODUCTION 0x2u   /* Philox4x32 tie-break + tenure draws instead of SplitMix64 streams */
+#define MCB_FLAG_FORCE_WIDE 0x4u   /* int16 gamma / 32-bit tabu stamps from the start (tests) */
+#define MCB_FLAG_FORCE_GLOBAL 0x8u /* gamma/tabu tables in global memory (L2-resident path, tests) */
+
+const char *mcb_version(void);
+const char *mcb_last_error(void);
+int mcb_device_count(void);
+
+/* out[i] = stream_value(keys[i], ctrs[i]) (rng.py:56-59); device pointers. */
+int mcb_stream_values(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out, int64_t count,
+                      void *stream);
+
+/*
+ * Batched TabuCol (localsearch.py:266-410).  One individual per CTA.
+ * log_* may be NULL when log_cap == 0.  counters (nullable) receives int64[p,2]:
+ * sum over iterations of the conflicting-vertex count and of deg(v*) (the
+ * algorithmic-bytes counters of SURVEY.md 8(d)).
+ */
+int mcb_tabucol_batch(int32_t *assigns, int64_t p, int64_t n, int64_t k,
+                      const int64_t *adj_indptr, const int32_t *adj_indices,
+                      const int32_t *edges_u, const int32_t *edges_v, int64_t m,
+                      int64_t depth, const uint64_t *keys,
+                      int32_t *best_assigns, int64_t *best_conflicts, int64_t *end_conflicts,
+                      int64_t *iters_used, int64_t *diag,
+                      int64_t log_cap, int32_t *log_v, int64_t *log_iter, int64_t *log_tt,
+                      int64_t *log_cnt, int64_t *counters, uint32_t flags, void *stream);
+int mcb_tabucol_batch_host(int32_t *assigns, int64_t p, int64_t n, int64_t k,
+                           const int64_t *adj_indptr, const int32_t *adj_indices,
+                           const int32_t *edges_u, const int32_t *edges_v, int64_t m,
+                           int64_t depth, const uint64_t *keys,
+                           int32_t *best_assigns, int64_t *best_conflicts, int64_t *end_conflicts,
+                           int64_t *iters_used, int64_t *diag,
+                           int64_t log_cap, int32_t *log_v, int64_t *log_iter, int64_t *log_tt,
+                           int64_t *log_cnt, int64_t *counters, uint32_t flags, void *stream);
+
+/*
+ * Batched weighted-colouring tabu search (localsearch.py:89-263).
+ * phi_used is double[p, rounds+1]; log_asp int8[p, log_cap].
+ */
+int mcb_wvcp_batch(int32_t *assigns, int64_t p, int64_t n, int64_t k,
+                   const int64_t *adj_indptr, const int32_t *adj_indices,
+                   const int32_t *edges_u, const int32_t *edges_v, int64_t m,
+                   const int32_t *wranks, const int64_t *wvals, int64_t nranks,
+                   const int64_t *weights, int64_t depth, int64_t rounds, int32_t schedule_on,
+                   const double *phi0s, double forced_phi, int64_t tt_base, const uint64_t *keys,
+                   int32_t *best_assigns, int64_t *best_scores, int64_t *end_scores,
+                   int64_t *end_conflicts, double *phi_used, int64_t *diag,
+                   int64_t log_cap, int32_t *log_v, int64_t *log_iter, int64_t *log_tt,
+                   int8_t *log_asp, int64_t *log_cnt, uint32_t flags, void *stream);
+int mcb_wvcp_batch_host(int32_t *assigns, int64_t p, int64_t n, int64_t k,
+                        const int64_t *adj_indptr, const int32_t *adj_indices,
+                        const int32_t *edges_u, const int32_t *edges_v, int64_t m,
+                        const int32_t *wranks, const int64_t *wvals, int64_t nranks,
+                        const int64_t *weights, int64_t depth, int64_t rounds, int32_t schedule_on,
+                        const double *phi0s, double forced_phi, int64_t tt_base,
+                        const uint64_t *keys, int32_t *best_assigns, int64_t *best_scores,
+                        int64_t *end_scores, int64_t *end_conflicts, double *phi_used,
+                        int64_t *diag, int64_t log_cap, int32_t *log_v, int64_t *log_iter,
+                        int64_t *log_tt, int8_t *log_asp, int64_t *log_cnt, uint32_t flags,
+                        void *stream);
+
+/*
+ * Batched GPX crossover (crossover.py:14-66): out[i,j,:] = GPX(pop[i],
+ * pop[matches[i,j]]) with stream keys[i*K+j].  out is int32[p,K,n].
+ */
+int mcb_gpx_batch(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches, int64_t K,
+                  int64_t k, const uint64_t *keys, int32_t *out, uint32_t flags, void *stream);
+int mcb_gpx_batch_host(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches,
+                       int64_t K, int64_t k, const uint64_t *keys, int32_t *out, uint32_t flags,
+                       void *stream);
+
+/*
+ * Approximate partition distances over the reference's linear job space
+ * (distance.py:90-119): jobs [0, p*q) -> cross[i,j] = d(pop_i, off_j);
+ * jobs [p*q, p*q + q(q-1)/2) -> within[i,j] = within[j,i] = d(off_i, off_j).
+ * Only jobs in [job_begin, job_end) are computed (job_end < 0: all), which is
+ * how ranks shard the pass.  cross int32[p,q], within int32[q,q].
+ */
+int mcb_pairwise(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n,
+                 int64_t k, int32_t *cross, int32_t *within, int64_t job_begin, int64_t job_end,
+                 uint32_t flags, void *stream);
+int mcb_pairwise_host(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n,
+                      int64_t k, int32_t *cross, int32_t *within, int64_t job_begin,
+                      int64_t job_end, uint32_t flags, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEMCOLOR_B200_H */

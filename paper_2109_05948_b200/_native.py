@@ -1,0 +1,97 @@
+"""ctypes binding of the C ABI (include/memcolor_b200.h).
+
+There is no fallback: if the shared library is missing or no CUDA device is
+visible, every operator raises.  Status codes map onto the exception types the
+reference raises for the same conditions (`localsearch.py:589-590,682`,
+`crossover.py:73-74`, `distance.py:23-24`).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from ._build import LIB
+
+MCB_OK, MCB_ERR_VALUE, MCB_ERR_CUDA, MCB_ERR_UNSUPPORTED, MCB_ERR_RANGE = 0, 1, 2, 3, 4
+FLAG_DIAG = 0x1
+FLAG_PRODUCTION = 0x2
+FLAG_FORCE_WIDE = 0x4
+FLAG_FORCE_GLOBAL = 0x8
+
+EXPORTS = [
+    "mcb_version", "mcb_last_error", "mcb_device_count", "mcb_stream_values",
+    "mcb_tabucol_batch", "mcb_tabucol_batch_host", "mcb_wvcp_batch", "mcb_wvcp_batch_host",
+    "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_pairwise", "mcb_pairwise_host",
+]
+
+_lib = None
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+def _declare(L):
+    P, I64, U32, I32 = C.c_void_p, C.c_int64, C.c_uint32, C.c_int32
+    L.mcb_version.restype = C.c_char_p
+    L.mcb_last_error.restype = C.c_char_p
+    L.mcb_device_count.restype = C.c_int
+    L.mcb_stream_values.argtypes = [P, P, P, I64, P]
+    tab = [P, I64, I64, I64, P, P, P, P, I64, I64, P, P, P, P, P, P, I64, P, P, P, P, P, U32, P]
+    L.mcb_tabucol_batch.argtypes = tab
+    L.mcb_tabucol_batch_host.argtypes = tab
+    wv = [P, I64, I64, I64, P, P, P, P, I64, P, P, I64, P, I64, I64, I32, P, C.c_double, I64, P,
+          P, P, P, P, P, P, I64, P, P, P, P, P, U32, P]
+    L.mcb_wvcp_batch.argtypes = wv
+    L.mcb_wvcp_batch_host.argtypes = wv
+    gp = [P, I64, I64, P, I64, I64, P, P, U32, P]
+    L.mcb_gpx_batch.argtypes = gp
+    L.mcb_gpx_batch_host.argtypes = gp
+    pw = [P, I64, P, I64, I64, I64, P, P, I64, I64, U32, P]
+    L.mcb_pairwise.argtypes = pw
+    L.mcb_pairwise_host.argtypes = pw
+    for name in EXPORTS[3:]:
+        getattr(L, name).restype = C.c_int
+
+
+def load(path=None):
+    """Load the library (no device needed).  Raises if it is not built."""
+    global _lib
+    if _lib is None:
+        path = path or LIB
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: build it with `python -m paper_2109_05948_b200._build`")
+        L = C.CDLL(path)
+        _declare(L)
+        _lib = L
+    return _lib
+
+
+def lib():
+    """The library, with a CUDA device required (no CPU fallback)."""
+    L = load()
+    if L.mcb_device_count() < 1:
+        raise NativeUnavailable("memcolor-b200 needs a CUDA device; none is visible")
+    return L
+
+
+def check(rc):
+    if rc == MCB_OK:
+        return
+    msg = (load().mcb_last_error() or b"").decode(errors="replace")
+    if rc in (MCB_ERR_VALUE, MCB_ERR_UNSUPPORTED, MCB_ERR_RANGE):
+        raise ValueError(msg)
+    raise RuntimeError(f"CUDA error: {msg}")
+
+
+def ptr(a):
+    """Address of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()

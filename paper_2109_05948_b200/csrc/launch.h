@@ -1,0 +1,72 @@
+// launch.h -- internal host-side interface between the C ABI (capi.cu) and
+// the kernel launchers.  Not part of the public ABI (include/memcolor_b200.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mcb {
+
+int set_error(int code, const char *fmt, ...);
+int num_sms();
+int max_smem_optin();
+// Grow-only per-device scratch buffer (stream-ordered users must be done with
+// the previous contents; every entry point synchronises before returning).
+void *workspace(size_t bytes);
+
+struct TabucolArgs {
+    int32_t *assigns;
+    int64_t p, n, k;
+    const int64_t *indptr;
+    const int32_t *indices;
+    const int32_t *eu, *ev;
+    int64_t m, depth;
+    const uint64_t *keys;
+    int32_t *best_assigns;
+    int64_t *best_conflicts, *end_conflicts, *iters_used, *diag;
+    int64_t log_cap;
+    int32_t *log_v;
+    int64_t *log_iter, *log_tt, *log_cnt, *counters;
+    uint32_t flags;
+};
+int tabucol_run(const TabucolArgs &a, cudaStream_t st);
+
+struct WvcpArgs {
+    int32_t *assigns;
+    int64_t p, n, k;
+    const int64_t *indptr;
+    const int32_t *indices;
+    const int32_t *eu, *ev;
+    int64_t m;
+    const int32_t *wranks;
+    const int64_t *wvals;
+    int64_t nranks;
+    const int64_t *weights;
+    int64_t depth, rounds;
+    int32_t schedule_on;
+    const double *phi0s;
+    double forced_phi;
+    int64_t tt_base;
+    const uint64_t *keys;
+    int32_t *best_assigns;
+    int64_t *best_scores, *end_scores, *end_conflicts;
+    double *phi_used;
+    int64_t *diag;
+    int64_t log_cap;
+    int32_t *log_v;
+    int64_t *log_iter, *log_tt;
+    int8_t *log_asp;
+    int64_t *log_cnt;
+    uint32_t flags;
+};
+int wvcp_run(const WvcpArgs &a, cudaStream_t st);
+
+int gpx_run(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches, int64_t K, int64_t k,
+            const uint64_t *keys, int32_t *out, uint32_t flags, cudaStream_t st);
+int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n, int64_t k,
+                 int32_t *cross, int32_t *within, int64_t job_begin, int64_t job_end,
+                 uint32_t flags, cudaStream_t st);
+int stream_values_run(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out, int64_t count,
+                      cudaStream_t st);
+
+}  // namespace mcb

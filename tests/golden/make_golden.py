@@ -1,0 +1,265 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (where /root/reference exists and numba is
+installed):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+It imports the reference package (`/root/reference/pkg/src/memcolor`) and its
+test oracles (`/root/reference/pkg/tests/oracles.py`) and records, for seeded
+inputs, the outputs of the reference's own hot-path kernels:
+
+* rng.npz       stream_key / stream_value / u64_below (`rng.py:56-82`)
+* graphs.npz    rand_graph digests (`tests/oracles.py:15-22`)
+* tabucol.npz   _run_tabucol_batch outputs + move logs (`localsearch.py:556`)
+* wvcp.npz      _run_wvcp_batch outputs + move logs (`localsearch.py:427`)
+* gpx.npz       build_offspring_batch / gpx (`crossover.py:69-93`)
+* distance.npz  pairwise_distances / approx_partition_distance (`distance.py:75-155`)
+
+Inputs are regenerated in the tests from the recorded parameters with the
+package's own generators (which are themselves pinned by graphs.npz and the
+initial-colouring digests), so the fixtures stay small.  Nothing at test time
+reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+REF = "/root/reference/pkg"
+sys.path.insert(0, os.path.join(REF, "src"))
+sys.path.insert(0, os.path.join(REF, "tests"))
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+
+import numpy as np  # noqa: E402
+
+from memcolor import crossover as RCX  # noqa: E402
+from memcolor import distance as RDI  # noqa: E402
+from memcolor import localsearch as RLS  # noqa: E402
+from memcolor import rng as RRNG  # noqa: E402
+from memcolor.coloring import Coloring as RColoring  # noqa: E402
+from oracles import rand_graph as ref_rand_graph  # noqa: E402
+
+from paper_2109_05948_b200.graph import rand_graph  # noqa: E402
+from paper_2109_05948_b200.init import random_col_assigns  # noqa: E402
+from paper_2109_05948_b200.rng import TAG_CROSS, TAG_LS, stream_keys  # noqa: E402
+
+
+def digest(x):
+    return hashlib.sha256(np.ascontiguousarray(x, dtype=np.int32).tobytes()).hexdigest()[:16]
+
+
+# --------------------------------------------------------------------------
+# TabuCol cases: (name, seed, n, p_edge, k, pop, depth, log_cap, full_arrays)
+# --------------------------------------------------------------------------
+TABUCOL_CASES = [
+    ("c1", 1, 125, 0.5, 18, 64, 10000, 10000, True),      # BASELINE config 0
+    ("c2s", 1, 500, 0.5, 48, 4, 50000, 4000, True),       # config 1 shape, 4 individuals
+    ("c2w", 1, 500, 0.5, 48, 32, 3000, 3000, True),       # config 1 shape, 32 x 3k
+    ("c3s", 1, 1000, 0.5, 83, 2, 4000, 4000, True),       # config 2 shape
+    ("k2dense", 5, 300, 0.9, 2, 4, 400, 400, True),       # gamma > 127: wide-table path
+    ("k3", 7, 60, 0.3, 3, 16, 2000, 2000, True),
+    ("k5sparse", 8, 200, 0.05, 5, 16, 5000, 5000, True),
+    ("k8", 9, 90, 0.4, 8, 16, 3000, 3000, True),
+    ("k40", 10, 200, 0.9, 40, 8, 4000, 4000, True),
+    ("k64", 11, 400, 0.85, 64, 4, 3000, 3000, True),
+    ("k70", 12, 400, 0.9, 70, 4, 3000, 3000, True),       # k > 64
+    ("k150", 13, 700, 0.95, 150, 2, 1500, 1500, True),    # config 5 palette
+    ("easy", 14, 80, 0.1, 6, 16, 5000, 5000, True),       # early exits
+    ("k1", 15, 30, 0.3, 1, 4, 100, 100, True),            # k < 2: no iterations
+    ("edgeless", 16, 40, 0.0, 4, 4, 100, 100, True),      # m = 0
+    ("n1", 17, 1, 0.5, 3, 2, 10, 10, True),               # single vertex
+    ("tenure", 18, 500, 0.9, 8, 2, 2500, 2500, True),     # long tenures (conflicts ~ 1e4)
+    ("long", 19, 100, 0.5, 14, 4, 40000, 0, True),        # > 2x16384 iterations (stamp wrap)
+    ("tenure32", 20, 800, 0.9, 4, 2, 300, 300, True),     # tenure > 16383 and gamma > 127
+]
+
+WVCP_CASES = [
+    # name, seed, n, p_edge, wmax, k, pop, depth, rounds, schedule, phi0 (None=default), log
+    ("c4s", 1, 500, 0.5, 100, 60, 2, 5000, 10, True, None, 4000),
+    ("c4w", 1, 500, 0.5, 100, 60, 16, 300, 4, True, None, 1200),
+    ("small", 21, 60, 0.4, 9, 10, 16, 400, 5, True, None, 2000),
+    ("fixed", 22, 80, 0.3, 20, 12, 8, 600, 1, False, 3.0, 600),
+    ("unit", 23, 100, 0.5, 1, 20, 8, 500, 3, True, None, 1500),
+    ("k70", 24, 150, 0.5, 50, 70, 4, 300, 3, True, None, 900),
+    ("legal", 25, 50, 0.1, 30, 12, 8, 400, 3, True, None, 1200),
+]
+
+
+def gen_tabucol(out):
+    meta = []
+    for name, seed, n, pe, k, pop, depth, cap, _ in TABUCOL_CASES:
+        g = ref_rand_graph(seed, n, pe, wmax=1) if n <= 600 else None
+        mine = rand_graph(seed, n, pe, wmax=1)
+        if g is not None:
+            assert np.array_equal(g.edges, mine.edges), name
+        else:
+            g = mine  # n > 600: ref rand_graph is a pure-Python n^2 loop
+        if k >= 1:
+            A = random_col_assigns(n, k, pop, seed)
+        keys = stream_keys(seed, TAG_LS, 0, pop)
+        r = RLS._run_tabucol_batch(g, A.copy(), k, keys, depth, log_moves=cap > 0)
+        pre = f"{name}__"
+        out[pre + "params"] = np.array([seed, n, int(pe * 1000), k, pop, depth, cap], np.int64)
+        out[pre + "init_digest"] = np.array([digest(A)])
+        out[pre + "best_conflicts"] = r["best_conflicts"]
+        out[pre + "end_conflicts"] = r["end_conflicts"]
+        out[pre + "iters_used"] = r["iters_used"]
+        out[pre + "end_assigns"] = r["end_assigns"].astype(np.uint8)
+        out[pre + "best_assigns"] = r["best_assigns"].astype(np.uint8)
+        if cap > 0:
+            lv, li, lt, lc = r["log"]
+            out[pre + "log_cnt"] = lc
+            nkeep = min(pop, 8)
+            out[pre + "log_v"] = lv[:nkeep, :cap].astype(np.int16)
+            out[pre + "log_iter"] = li[:nkeep, :cap].astype(np.int32)
+            out[pre + "log_tt"] = lt[:nkeep, :cap].astype(np.int32)
+        meta.append(name)
+        print("tabucol", name, r["best_conflicts"][:4], r["iters_used"][:4])
+    out["cases"] = np.array(meta)
+
+
+def gen_wvcp(out):
+    meta = []
+    for name, seed, n, pe, wmax, k, pop, depth, rounds, sched, phi0, cap in WVCP_CASES:
+        g = ref_rand_graph(seed, n, pe, wmax=wmax)
+        mine = rand_graph(seed, n, pe, wmax=wmax)
+        assert np.array_equal(g.edges, mine.edges) and np.array_equal(g.weights, mine.weights)
+        A = random_col_assigns(n, k, pop, seed)
+        keys = stream_keys(seed, TAG_LS, 0, pop)
+        phi = RLS.default_wvcp_phi0(g, k) if phi0 is None else phi0
+        r = RLS._run_wvcp_batch(g, A.copy(), k, keys, depth, rounds, sched, phi, log_moves=True)
+        pre = f"{name}__"
+        out[pre + "params"] = np.array([seed, n, int(pe * 1000), wmax, k, pop, depth, rounds,
+                                        int(sched)], np.int64)
+        out[pre + "phi0"] = np.array([phi], np.float64)
+        for key in ["best_scores", "end_scores", "end_conflicts", "phi_used"]:
+            out[pre + key] = r[key]
+        out[pre + "end_assigns"] = r["end_assigns"].astype(np.uint8)
+        out[pre + "best_assigns"] = r["best_assigns"].astype(np.uint8)
+        lv, li, lt, la, lc = r["log"]
+        nkeep = min(pop, 4)
+        c = min(cap, lv.shape[1])
+        out[pre + "log_cnt"] = lc
+        out[pre + "log_v"] = lv[:nkeep, :c].astype(np.int16)
+        out[pre + "log_iter"] = li[:nkeep, :c].astype(np.int32)
+        out[pre + "log_tt"] = lt[:nkeep, :c].astype(np.int32)
+        out[pre + "log_asp"] = la[:nkeep, :c]
+        meta.append(name)
+        print("wvcp", name, r["best_scores"][:4], r["end_scores"][:4])
+    out["cases"] = np.array(meta)
+
+
+def gen_gpx(out):
+    meta = []
+    cases = [("appA", 1, 1000, 83, 8, 4, "ring")]
+    for s in range(12):
+        st = RRNG.Stream(900 + s)
+        n = 1 + st.below(300)
+        k = 1 + st.below(40)
+        p = 2 + st.below(6)
+        K = 1 + st.below(p - 1) if p > 1 else 1
+        cases.append((f"r{s}", 900 + s, n, k, p, K, "rand"))
+    cases.append(("k150", 77, 2000, 150, 4, 3, "rand"))
+    for name, seed, n, k, p, K, how in cases:
+        P = random_col_assigns(n, k, p, seed)
+        if how == "ring":
+            matches = np.array([[(i + 1 + j) % p for j in range(K)] for i in range(p)], np.int64)
+        else:
+            st = RRNG.Stream(seed * 31 + 7)
+            matches = np.array([[st.below(p) for _ in range(K)] for _ in range(p)], np.int64)
+        o = RCX.build_offspring_batch(P, matches, k, seed, 0)
+        keys = stream_keys(seed, TAG_CROSS, 0, p * K)
+        # single-pair API on job 0 (`crossover.py:69-78`)
+        single = RCX.gpx(RColoring(P[0], k), RColoring(P[matches[0, 0]], k), k,
+                         RRNG.Stream(int(keys[0])))
+        assert np.array_equal(single.assign, o[0, 0])
+        pre = f"{name}__"
+        out[pre + "params"] = np.array([seed, n, k, p, K], np.int64)
+        out[pre + "matches"] = matches
+        out[pre + "out"] = o.astype(np.uint8)
+        meta.append(name)
+    out["cases"] = np.array(meta)
+    print("gpx", len(meta))
+
+
+def gen_distance(out):
+    meta = []
+    cases = [("appA", 1, 1000, 83, 8, 8)]
+    for s in range(16):
+        st = RRNG.Stream(500 + s)
+        cases.append((f"r{s}", 500 + s, 1 + st.below(200), 1 + st.below(40), st.below(6), 1 + st.below(7)))
+    cases.append(("k150", 3, 2000, 150, 5, 6))
+    cases.append(("near", 4, 300, 10, 6, 6))  # near-identical partitions
+    for name, seed, n, k, p, q in cases:
+        if name == "appA":
+            P = random_col_assigns(n, k, p, seed)
+            matches = np.array([[(i + 1 + j) % 8 for j in range(4)] for i in range(8)], np.int64)
+            Q = RCX.build_offspring_batch(P, matches, k, seed, 0)[:, 0]
+        elif name == "near":
+            P = random_col_assigns(n, k, p, seed)
+            Q = P.copy()
+            st = RRNG.Stream(4444)
+            for i in range(q):
+                for _ in range(5):
+                    Q[i, st.below(n)] = st.below(k)
+        else:
+            P = random_col_assigns(n, k, p, seed)
+            Q = random_col_assigns(n, k, q, seed + 10_000)
+        cross, within = RDI.pairwise_distances(P, Q, k=k)
+        pre = f"{name}__"
+        out[pre + "params"] = np.array([seed, n, k, p, q], np.int64)
+        out[pre + "P"] = P.astype(np.uint8)
+        out[pre + "Q"] = Q.astype(np.uint8)
+        out[pre + "cross"] = cross
+        out[pre + "within"] = within
+        meta.append(name)
+    # hand cases incl. the reference's known-bad expectation
+    hand = [([0, 0, 1, 1], [0, 1, 0, 1], 2), ([0, 1, 2, 0], [0, 1, 2, 0], 3),
+            ([0, 0, 1, 1, 2], [2, 2, 0, 0, 1], 3), ([0, 0, 1, 1, 2, 2], [0, 0, 1, 1, 2, 1], 3)]
+    out["hand_values"] = np.array(
+        [RDI.approx_partition_distance(RColoring(a, k), RColoring(b, k)) for a, b, k in hand])
+    out["cases"] = np.array(meta)
+    print("distance", len(meta), out["hand_values"])
+
+
+def gen_rng(out):
+    rows = []
+    for seed, tag, idx in [(1, 2, (0, 0)), (1, 1, (0,)), (2024, 2, (5, 11)), (7, 1, ()),
+                           (0, 0, ()), (2**64 - 1, 7, (3, 2**40, 9)), (42, 3, (1, 2, 3, 4))]:
+        key = RRNG.stream_key(seed, tag, *idx)
+        vals = [int(RRNG.stream_value(np.uint64(key), np.uint64(c))) for c in range(16)]
+        below = [int(RRNG.u64_below(np.uint64(key), np.uint64(c), np.uint64(c + 1))) for c in range(16)]
+        rows.append((seed, tag, list(idx), key, vals, below))
+    out["keys"] = np.array([r[3] for r in rows], np.uint64)
+    out["values"] = np.array([r[4] for r in rows], np.uint64)
+    out["below"] = np.array([r[5] for r in rows], np.uint64)
+    out["spec"] = np.array([repr((r[0], r[1], tuple(r[2]))) for r in rows])
+
+
+def gen_graphs(out):
+    rows = []
+    for seed, n, pe, wmax in [(1, 125, 0.5, 1), (1, 500, 0.5, 1), (1, 500, 0.5, 100), (3, 50, 0.4, 9),
+                              (5, 300, 0.9, 1), (16, 40, 0.0, 4)]:
+        g = ref_rand_graph(seed, n, pe, wmax=wmax)
+        rows.append((seed, n, pe, wmax, g.m, digest(g.edges), digest(g.weights), digest(g.adj_indptr),
+                     digest(g.adj_indices)))
+    out["rows"] = np.array([repr(r) for r in rows])
+
+
+def main():
+    os.makedirs(HERE, exist_ok=True)
+    for fn, name in [(gen_rng, "rng"), (gen_graphs, "graphs"), (gen_tabucol, "tabucol"),
+                     (gen_wvcp, "wvcp"), (gen_gpx, "gpx"), (gen_distance, "distance")]:
+        out = {}
+        fn(out)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print("done")
+
+
+if __name__ == "__main__":
+    main()
