@@ -51,10 +51,19 @@ extern "C" {
 #define MCB_FLAG_PRODUCTION 0x2u   /* Philox4x32 tie-break + tenure draws instead of SplitMix64 streams */
 #define MCB_FLAG_FORCE_WIDE 0x4u   /* int16 gamma / 32-bit tabu stamps from the start (tests) */
 #define MCB_FLAG_FORCE_GLOBAL 0x8u /* gamma/tabu tables in global memory (L2-resident path, tests) */
+#define MCB_FLAG_PROFILE 0x100u    /* accumulate per-phase clock64 cycles (mcb_debug_phase_cycles) */
 
 const char *mcb_version(void);
 const char *mcb_last_error(void);
 int mcb_device_count(void);
+
+/* Diagnostics: aggregate shared-memory read bandwidth of the current device
+ * (GB/s), measured with a conflict-free LDS.128 stream; the roofline
+ * denominator of the shared-memory-bound kernels. */
+int mcb_probe_smem_bandwidth(double *gbs, double *ms);
+/* Diagnostics: per-phase cycle totals of the TabuCol iteration accumulated
+ * by runs with MCB_FLAG_PROFILE (out: 16 counters; [10] = iterations). */
+int mcb_debug_phase_cycles(unsigned long long *out, int reset);
 
 /* out[i] = stream_value(keys[i], ctrs[i]) (rng.py:56-59); device pointers. */
 int mcb_stream_values(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out, int64_t count,

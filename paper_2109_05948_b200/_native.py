@@ -20,11 +20,13 @@ FLAG_DIAG = 0x1
 FLAG_PRODUCTION = 0x2
 FLAG_FORCE_WIDE = 0x4
 FLAG_FORCE_GLOBAL = 0x8
+FLAG_PROFILE = 0x100
 
 EXPORTS = [
     "mcb_version", "mcb_last_error", "mcb_device_count", "mcb_stream_values",
     "mcb_tabucol_batch", "mcb_tabucol_batch_host", "mcb_wvcp_batch", "mcb_wvcp_batch_host",
     "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_pairwise", "mcb_pairwise_host",
+    "mcb_probe_smem_bandwidth", "mcb_debug_phase_cycles",
 ]
 
 _lib = None
@@ -53,6 +55,8 @@ def _declare(L):
     pw = [P, I64, P, I64, I64, I64, P, P, I64, I64, U32, P]
     L.mcb_pairwise.argtypes = pw
     L.mcb_pairwise_host.argtypes = pw
+    L.mcb_probe_smem_bandwidth.argtypes = [P, P]
+    L.mcb_debug_phase_cycles.argtypes = [P, C.c_int]
     for name in EXPORTS[3:]:
         getattr(L, name).restype = C.c_int
 

@@ -30,6 +30,7 @@ struct TabucolArgs {
     uint32_t flags;
 };
 int tabucol_run(const TabucolArgs &a, cudaStream_t st);
+int tabucol_phase_cycles(unsigned long long *out, int reset);
 
 struct WvcpArgs {
     int32_t *assigns;

@@ -13,22 +13,21 @@
 //   * early exit at zero conflicts (:322), `it` counts no-move iterations (:398),
 //     O(m) scratch check every 1024 iterations -> diag (:398-405).
 //
-// The sequential reservoir is evaluated in parallel and exactly:
-//   pass 1  every row-group (RG lanes) evaluates one conflicting vertex's k-1
-//           candidates from shared memory -> (row min, #candidates at the min);
-//   pass 2  warp 0 runs an exclusive prefix-min over the row minima.  Each tie
-//           event of the sequential scan is a candidate equal to the running
-//           minimum; rows whose minimum is above the running minimum have none,
-//           rows whose minimum equals it have exactly #min of them, and the few
-//           rows that LOWER the running minimum are re-evaluated with an in-row
-//           prefix-min scan.  That gives the total number of tie events, hence
-//           the counter offset E of the final minimum group.
-//   pass 3  the T-1 reservoir draws of the final group are independent
-//           (counter ctr+E+s-2 for rank s); the winner is the LAST rank whose
-//           draw is zero (warp max).
-//   pass 4  locate the winning (v, c), apply tenure.
-//   pass 5  all threads update gamma over N(v) and flag conflict-set events;
-//   pass 6  one thread applies the (few) events in neighbour order.
+// One iteration = two block barriers:
+//   pass 1 (all threads)  thread-per-row: each conflicting vertex's k-1
+//          candidates are evaluated 4 at a time with byte-SIMD (int8 deltas,
+//          u16 wrap-around tabu stamps, aspiration) -> (row min, #at min).
+//   pass 2 (warp 0)       exclusive prefix-min over the row minima.  A tie
+//          event of the sequential reservoir is a candidate equal to the
+//          running minimum: rows above the running minimum contribute none,
+//          rows equal to it contribute #min, and the few rows that LOWER it are
+//          re-walked lane-locally.  That yields the global minimum D, its
+//          multiplicity T and the counter offset E of D's group, so the T-1
+//          reservoir draws (counter ctr+E+s-2 for rank s) are independent: the
+//          winner is the last rank whose draw is zero (warp max).
+//          Then the winner is located, the tenure drawn, gamma updated over
+//          N(v) by the warp (32 neighbours per step) and conflict-set events
+//          applied in neighbour order (ballot order), then v itself.
 //
 // Data layout per individual (shared memory when it fits, else a per-CTA
 // global slice that stays L2-resident):
@@ -36,23 +35,25 @@
 //   tabu   u16  [n][kp]  wrap-around stamps, swept every 16384 iterations
 //                        -- u32 fallback when a tenure exceeds 16383
 //   assign u8 [n], conflict list / positions u16 [n], per-row (min, count) [n].
+//   CSR row offsets in __constant__ memory (u32) when n < 12288.
 // Individuals whose int8/u16 tables would overflow are re-run from their
 // original start by the wide (int16 / u32) instantiation; results are
 // identical by construction (same arithmetic, wider storage).
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
-#include <mutex>
 
 #include "common.cuh"
 #include "launch.h"
 
 namespace mcb {
 
-constexpr int TC_NT = 256;
-constexpr int TC_EVCAP = 64;
 constexpr int TC_BIG = 1 << 20;
+constexpr int TC_CONST_INDPTR = 12288;
+
+__constant__ uint32_t c_indptr[TC_CONST_INDPTR];
 
 struct TabuParams {
     int32_t *assigns;
@@ -79,15 +80,24 @@ struct TabuParams {
     uint8_t *ws_gamma, *ws_stamp;  // per-CTA global slices (global variants)
     size_t ws_g_stride, ws_s_stride;
     uint32_t flags;
-    int rg, wpl, words;
+    int const_indptr;
 };
+
+__device__ unsigned long long g_phase_cycles[16];
+#define PH(i)                                          \
+    if (profile && tid == 0) {                         \
+        const long long _t = clock64();                \
+        ctl.ph[i] += _t - ph_t;                        \
+        ph_t = _t;                                     \
+    }
 
 struct TabuCtrl {
     long long it, conflicts, best, nlog, sum_c, sum_deg, diag;
     unsigned long long ctr;
-    int C, work, mv_v, mv_a, mv_b, mv_gvb, has_move, nev, copy, ovf;
-    long long red[TC_NT / 32];
-    int wcnt[TC_NT / 32];
+    int C, work, ovf;
+    long long ph[12];
+    long long red[32];
+    int wcnt[32];
 };
 
 template <typename G>
@@ -127,108 +137,171 @@ __device__ __forceinline__ bool stamp_active(S st, uint32_t it) {
         return (int32_t)((uint32_t)st - it) > 0;
 }
 
-// Load the EPW stamps of gamma word w of a row.
-template <typename S, int EPW>
-__device__ __forceinline__ void load_stamps(const S *srow, int w, S (&st)[EPW]) {
-    if constexpr (sizeof(S) * EPW == 8) {
-        uint2 x = *reinterpret_cast<const uint2 *>(srow + w * EPW);
-        uint32_t wd[2] = {x.x, x.y};
-#pragma unroll
-        for (int e = 0; e < EPW; e++) {
-            if constexpr (sizeof(S) == 2)
-                st[e] = (S)(wd[e >> 1] >> (16 * (e & 1)));
-            else
-                st[e] = (S)wd[e];
-        }
-    } else if constexpr (sizeof(S) * EPW == 16) {
-        uint4 x = *reinterpret_cast<const uint4 *>(srow + w * EPW);
-        uint32_t wd[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int e = 0; e < EPW; e++) st[e] = (S)wd[e];
-    } else {
-        uint32_t x = *reinterpret_cast<const uint32_t *>(srow + w * EPW);
-#pragma unroll
-        for (int e = 0; e < EPW; e++) st[e] = (S)(x >> (16 * e));
-    }
+// signed byte-min of the 4 bytes of x; *bc = that byte broadcast to 4 lanes
+__device__ __forceinline__ int bmin4(uint32_t x, uint32_t &bc) {
+    uint32_t y = __vmins4(x, __byte_perm(x, 0, 0x3232));
+    y = __vmins4(y, __byte_perm(y, 0, 0x1111));
+    bc = __byte_perm(y, 0, 0x0000);
+    return (int)(int8_t)(y & 0xFFu);
 }
 
-// Evaluate one lane's share of a row: dv[j*EPW+e] = delta of colour
-// (lig + j*RG)*EPW + e if the move is admissible, else TC_BIG.
-template <typename G, typename S, int MAXV>
-__device__ __forceinline__ void eval_row(const G *gamma, const S *stamp, const uint8_t *assign, int v,
-                                         int kp, int k, int lig, int RG, int WPL, int W,
-                                         uint32_t it, int thr, int (&dv)[MAXV]) {
-    constexpr int EPW = 4 / (int)sizeof(G);
-    const int a = assign[v];
-    const G *grow = gamma + (size_t)v * kp;
-    const S *srow = stamp + (size_t)v * kp;
-    const int gva = grow[a];
-#pragma unroll
-    for (int j = 0; j < MAXV / EPW; j++) {
-        const int w = lig + j * RG;
-        if (j < WPL && w < W) {
-            const uint32_t gw = reinterpret_cast<const uint32_t *>(grow)[w];
-            S st[EPW];
-            load_stamps<S, EPW>(srow, w, st);
-#pragma unroll
-            for (int e = 0; e < EPW; e++) {
-                const int c = w * EPW + e;
-                int gv;
-                if constexpr (sizeof(G) == 1)
-                    gv = (int)(int8_t)(gw >> (8 * e));
-                else
-                    gv = (int)(int16_t)(gw >> (16 * e));
-                const int d = gv - gva;
-                const bool tabu = stamp_active<S>(st[e], it);
-                const bool adm = (c < k) && (c != a) && (!tabu || d < thr);
-                dv[j * EPW + e] = adm ? d : TC_BIG;
+// One conflicting vertex's candidate row: delta = gamma[v][c] - gamma[v][a],
+// admissible = c != a && (not tabu || conflicts + delta < best).
+template <typename G, typename S>
+struct Row {
+    const G *g;
+    const S *s;
+    int a, gva, k, W;
+    uint32_t it, gva4, thr4, it2, amask, kmask;
+    int thr, aw;
+
+    __device__ __forceinline__ Row(const G *gamma, const S *stamp, const uint8_t *assign, int v, int kp,
+                                   int k_, uint32_t it_, int thr_) {
+        a = assign[v];
+        g = gamma + (size_t)v * kp;
+        s = stamp + (size_t)v * kp;
+        gva = g[a];
+        k = k_;
+        it = it_;
+        thr = thr_;
+        W = kp / 4;
+        if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
+            gva4 = (uint32_t)gva * 0x01010101u;
+            const int t8 = max(thr, -128);
+            thr4 = (uint32_t)(uint8_t)(int8_t)t8 * 0x01010101u;
+            it2 = ((it & 0xFFFFu) << 16) | (it & 0xFFFFu);
+            aw = a >> 2;
+            amask = 0xFFu << (8 * (a & 3));
+            const int rem = k & 3;
+            kmask = rem ? (0xFFFFFFFFu >> (8 * (4 - rem))) : 0xFFFFFFFFu;
+        }
+    }
+    // narrow path: 4 candidates (colours 4w..4w+3) as signed bytes, 127 = inadmissible
+    __device__ __forceinline__ uint32_t word(int w) const {
+        const uint32_t gw = reinterpret_cast<const uint32_t *>(g)[w];
+        const uint2 st = reinterpret_cast<const uint2 *>(s)[w];
+        const uint32_t d = __vsub4(gw, gva4);
+        const uint32_t m0 = __vcmpgts2(__vsub2(st.x, it2), 0u);
+        const uint32_t m1 = __vcmpgts2(__vsub2(st.y, it2), 0u);
+        const uint32_t tabu = __byte_perm(m0, m1, 0x6420);
+        uint32_t ok = ~tabu | __vcmplts4(d, thr4);
+        if (w == aw) ok &= ~amask;
+        if (w == W - 1) ok &= kmask;
+        return (d & ok) | (0x7F7F7F7Fu & ~ok);
+    }
+    // wide path: one candidate, TC_BIG if inadmissible
+    __device__ __forceinline__ int cand(int c) const {
+        if (c == a) return TC_BIG;
+        const int d = (int)g[c] - gva;
+        if (stamp_active<S>(s[c], it) && !(d < thr)) return TC_BIG;
+        return d;
+    }
+
+    // (row min, #candidates at the min); min = TC_BIG if none admissible
+    __device__ __forceinline__ void scan(int &rmin, int &nq) const {
+        if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
+            int m = 127, cnt = 0;
+#pragma unroll 4
+            for (int w = 0; w < W; w++) {
+                const uint32_t dv = word(w);
+                uint32_t bc;
+                const int wm = bmin4(dv, bc);
+                const int c = __popc(__vcmpeq4(dv, bc)) >> 3;
+                cnt = (wm < m) ? c : (wm == m ? cnt + c : cnt);
+                m = min(m, wm);
             }
+            rmin = (m == 127) ? TC_BIG : m;
+            nq = (m == 127) ? 0 : cnt;
         } else {
-#pragma unroll
-            for (int e = 0; e < EPW; e++) dv[j * EPW + e] = TC_BIG;
-        }
-    }
-}
-
-// Number of sequential tie events inside a row when the scan enters it with
-// running minimum R (group-cooperative, RG lanes, colour order (j, lig, e)).
-template <int EPW, int MAXV>
-__device__ __forceinline__ int row_ties(const int (&dv)[MAXV], int R, int lig, int RG, int WPL) {
-    int running = R, ties = 0;
-#pragma unroll
-    for (int j = 0; j < MAXV / EPW; j++) {
-        if (j < WPL) {
-            int lmin = TC_BIG;
-#pragma unroll
-            for (int e = 0; e < EPW; e++) lmin = min(lmin, dv[j * EPW + e]);
-            const int incl = warp_incl_min(lmin, lig, RG);
-            int excl = __shfl_up_sync(0xffffffffu, incl, 1, RG);
-            if (lig == 0) excl = TC_BIG;
-            int cur = min(running, excl);
-            int cnt = 0;
-#pragma unroll
-            for (int e = 0; e < EPW; e++) {
-                const int x = dv[j * EPW + e];
-                if (x != TC_BIG) {
-                    if (x < cur) cur = x;
-                    else if (x == cur) cnt++;
+            int m = TC_BIG, cnt = 0;
+            for (int c = 0; c < k; c++) {
+                const int x = cand(c);
+                if (x < m) {
+                    m = x;
+                    cnt = 1;
+                } else if (x == m && x != TC_BIG) {
+                    cnt++;
                 }
             }
-            ties += warp_sum(cnt, RG);
-            running = min(running, __shfl_sync(0xffffffffu, incl, RG - 1, RG));
+            rmin = m;
+            nq = cnt;
         }
     }
-    return ties;
-}
+    // (min, count) over words sub, sub+tpr, ... (narrow path only)
+    __device__ __forceinline__ void scan_part(int sub, int tpr, int &rmin, int &nq) const {
+        int m = 127, cnt = 0;
+#pragma unroll 2
+        for (int w = sub; w < W; w += tpr) {
+            const uint32_t dv = word(w);
+            uint32_t bc;
+            const int wm = bmin4(dv, bc);
+            const int c = __popc(__vcmpeq4(dv, bc)) >> 3;
+            cnt = (wm < m) ? c : (wm == m ? cnt + c : cnt);
+            m = min(m, wm);
+        }
+        rmin = (m == 127) ? TC_BIG : m;
+        nq = (m == 127) ? 0 : cnt;
+    }
+    // sequential tie events inside the row when entered with running minimum R
+    __device__ __forceinline__ int ties(int R) const {
+        int cur = R, t = 0;
+        if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
+            for (int w = 0; w < W; w++) {
+                const uint32_t dv = word(w);
+                uint32_t bc;
+                const int wm = bmin4(dv, bc);
+                if (wm == 127 || wm > cur) continue;
+                if (wm == cur) {
+                    t += __popc(__vcmpeq4(dv, bc)) >> 3;
+                    continue;
+                }
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const int x = (int)(int8_t)(dv >> (8 * e));
+                    if (x == 127) continue;
+                    if (x < cur) cur = x;
+                    else if (x == cur) t++;
+                }
+            }
+        } else {
+            for (int c = 0; c < k; c++) {
+                const int x = cand(c);
+                if (x == TC_BIG) continue;
+                if (x < cur) cur = x;
+                else if (x == cur) t++;
+            }
+        }
+        return t;
+    }
+    // colour of the j-th (1-based) admissible candidate with delta D
+    __device__ __forceinline__ int find(int D, int j) const {
+        if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
+            const uint32_t d4 = (uint32_t)(uint8_t)(int8_t)D * 0x01010101u;
+            for (int w = 0; w < W; w++) {
+                const uint32_t eq = __vcmpeq4(word(w), d4);
+                const int c = __popc(eq) >> 3;
+                if (j <= c) {
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        if ((eq >> (8 * e)) & 1u)
+                            if (--j == 0) return 4 * w + e;
+                }
+                j -= c;
+            }
+        } else {
+            for (int c = 0; c < k; c++)
+                if (cand(c) == D && --j == 0) return c;
+        }
+        return -1;
+    }
+};
 
-template <typename G, typename S, bool GSM, bool SSM>
-__global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
-    constexpr int NT = TC_NT;
+template <typename G, typename S, bool GSM, bool SSM, int NT>
+__global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
     constexpr int NW = NT / 32;
-    constexpr int EPW = 4 / (int)sizeof(G);
-    constexpr int MAXV = 8;
     constexpr int GMAX = sizeof(G) == 1 ? 127 : 32767;
     constexpr uint32_t SWEEP = sizeof(S) == 2 ? 16384u : (1u << 30);
+    constexpr unsigned FULL = 0xffffffffu;
     using RI = RowInfoT<G>;
     using RowT = typename RI::T;
 
@@ -258,17 +331,14 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
     uint16_t *cpos = reinterpret_cast<uint16_t *>(smem + off);
     off += (2 * n + 15) & ~15;
     RowT *rinfo = reinterpret_cast<RowT *>(smem + off);
-    off += (sizeof(RowT) * n + 15) & ~15;
-    uint32_t *evl = reinterpret_cast<uint32_t *>(smem + off);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int RG = P.rg, WPL = P.wpl, W = P.words;
-    const int lig = lane & (RG - 1);
-    const int gpw = 32 / RG;  // groups per warp
-    const int gig = lane / RG;
     const bool diagf = (P.flags & MCB_FLAG_DIAG) != 0;
     const bool prod = (P.flags & MCB_FLAG_PRODUCTION) != 0;
+    const bool profile = (P.flags & MCB_FLAG_PROFILE) != 0;
     const size_t tab_elems = (size_t)n * kp;
+    const bool cidx = P.const_indptr != 0;
+    auto row_begin = [&](int v) -> int64_t { return cidx ? (int64_t)c_indptr[v] : P.indptr[v]; };
 
     for (;;) {
         if (tid == 0) ctl.work = atomicAdd(P.work_counter, 1);
@@ -301,6 +371,7 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
         if (tid == 0) {
             ctl.ovf = 0;
             ctl.diag = 0;
+            for (int q = 0; q < 12; q++) ctl.ph[q] = 0;
         }
         __syncthreads();
         // gamma[u][c] = #neighbours of u coloured c; each thread owns its rows
@@ -308,9 +379,9 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
             int bad = 0;
             for (int u = tid; u < n; u += NT) {
                 G *row = gamma + (size_t)u * kp;
-                const int64_t s0 = P.indptr[u], s1 = P.indptr[u + 1];
+                const int64_t s0 = row_begin(u), s1 = row_begin(u + 1);
                 for (int64_t idx = s0; idx < s1; idx++) {
-                    const int c = assign[P.indices[idx]];
+                    const int c = assign[__ldg(P.indices + idx)];
                     const int x = (int)row[c] + 1;
                     if (x > GMAX) bad = 1;
                     else row[c] = (G)x;
@@ -331,7 +402,7 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
                     f = g > 0;
                     c2 += g;
                 }
-                const unsigned bal = __ballot_sync(0xffffffffu, f);
+                const unsigned bal = __ballot_sync(FULL, f);
                 if (lane == 0) ctl.wcnt[warp] = __popc(bal);
                 __syncthreads();
                 int woff = 0, tot = 0;
@@ -375,6 +446,7 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
         // ---------------- iterations (:320-405) ----------------
         if (k >= 2 && !ctl.ovf) {
             for (long long step = 0; step < P.depth; step++) {
+                long long ph_t = clock64();
                 const long long conflicts = ctl.conflicts;
                 if (conflicts == 0 || ctl.ovf) break;
                 const long long it = ctl.it;
@@ -383,132 +455,148 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
                 const int thr = (int)max(best - conflicts, (long long)-TC_BIG);
                 const uint32_t it32 = (uint32_t)it;
 
-                // pass 1: per-row (min, count) over admissible candidates
-                for (int r0 = warp * gpw; r0 < C; r0 += NW * gpw) {
-                    const int li = r0 + gig;
-                    const bool act = li < C;
-                    int dv[MAXV];
-                    eval_row<G, S, MAXV>(gamma, stamp, assign, act ? clist[li] : clist[0], kp, k,
-                                         lig, RG, WPL, W, it32, thr, dv);
-                    int lmin = TC_BIG;
-#pragma unroll
-                    for (int i = 0; i < MAXV; i++) lmin = min(lmin, dv[i]);
-                    const int rmin = warp_min(lmin, RG);
-                    int cnt = 0;
-#pragma unroll
-                    for (int i = 0; i < MAXV; i++) cnt += (dv[i] == rmin && rmin != TC_BIG);
-                    const int nq = warp_sum(cnt, RG);
-                    if (act && lig == 0) rinfo[li] = RI::pack(rmin, nq);
+                // pass 1: (min, count) over admissible candidates of every row;
+                // tpr threads per row (power of two) when rows are few
+                {
+                    int tpr = 1;
+                    if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
+                        const int W = kp / 4;
+                        while (tpr < 16 && tpr * 2 * C <= NT && tpr * 2 <= W) tpr *= 2;
+                    }
+                    const int sub = tid & (tpr - 1);
+                    const int rows_per_pass = NT / tpr;
+                    for (int r0 = 0; r0 < C; r0 += rows_per_pass) {
+                        const int li = r0 + tid / tpr;
+                        int rm = TC_BIG, nq = 0;
+                        if (li < C) {
+                            const Row<G, S> row(gamma, stamp, assign, clist[li], kp, k, it32, thr);
+                            if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
+                                if (tpr == 1) row.scan(rm, nq);
+                                else row.scan_part(sub, tpr, rm, nq);
+                            } else {
+                                row.scan(rm, nq);
+                            }
+                        }
+                        if (tpr > 1) {  // combine the tpr partial (min, count)
+                            for (int o = 1; o < tpr; o <<= 1) {
+                                const int om = __shfl_xor_sync(0xffffffffu, rm, o);
+                                const int oq = __shfl_xor_sync(0xffffffffu, nq, o);
+                                nq = (om < rm) ? oq : (om == rm ? nq + oq : nq);
+                                rm = min(rm, om);
+                            }
+                        }
+                        if (li < C && sub == 0) rinfo[li] = RI::pack(rm, rm == TC_BIG ? 0 : nq);
+                    }
                 }
                 __syncthreads();
 
-                // passes 2-4: warp 0
+                PH(1);
+                // pass 2: warp 0 -- reservoir, move, gamma update, conflict list
                 if (warp == 0) {
-                    int carry = TC_BIG, tsum = 0;
-                    for (int base = 0; base < C; base += 32) {
-                        const int li = base + lane;
-                        int rm = TC_BIG, nq = 0;
-                        if (li < C) RI::unpack(rinfo[li], rm, nq);
-                        const int incl = warp_incl_min(rm, lane);
-                        int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+                    // -- exclusive prefix-min over the row minima, R rows per lane
+                    const int R = C <= 32 ? 1 : (C <= 64 ? 2 : 4);
+                    int carry = TC_BIG, lmin = TC_BIG, lT = 0, lfirst = INT_MAX, tsum = 0;
+                    for (int base = 0; base < C; base += 32 * R) {
+                        const int l0 = base + lane * R;
+                        int rm[4], nq[4];
+                        int lmn = TC_BIG;
+#pragma unroll
+                        for (int r = 0; r < 4; r++) {
+                            rm[r] = TC_BIG;
+                            nq[r] = 0;
+                            if (r < R && l0 + r < C) RI::unpack(rinfo[l0 + r], rm[r], nq[r]);
+                            lmn = min(lmn, rm[r]);
+                        }
+                        const int incl = warp_incl_min(lmn, lane);
+                        int excl = __shfl_up_sync(FULL, incl, 1);
                         if (lane == 0) excl = TC_BIG;
-                        const int RM = min(carry, excl);
-                        if (!prod) {
-                            if (rm == RM && rm != TC_BIG) tsum += nq;
-                            unsigned lm = __ballot_sync(0xffffffffu, rm < RM);
-                            while (lm) {
-                                unsigned mm = lm;
-                                for (int t = 0; t < gig && mm; t++) mm &= mm - 1u;
-                                const int src = mm ? (__ffs(mm) - 1) : -1;
-                                for (int t = 0; t < gpw && lm; t++) lm &= lm - 1u;
-                                const int R2 = __shfl_sync(0xffffffffu, RM, src < 0 ? 0 : src);
-                                const int li2 = base + (src < 0 ? 0 : src);
-                                int dv[MAXV];
-                                eval_row<G, S, MAXV>(gamma, stamp, assign, clist[li2], kp, k, lig, RG,
-                                                     WPL, W, it32, thr, dv);
-                                const int ties = row_ties<EPW, MAXV>(dv, R2, lig, RG, WPL);
-                                if (lig == 0 && src >= 0) tsum += ties;
+                        int RM = min(carry, excl);
+#pragma unroll
+                        for (int r = 0; r < 4; r++) {
+                            if (r >= R) break;
+                            const int x = rm[r];
+                            if (x < lmin) {
+                                lmin = x;
+                                lT = nq[r];
+                                lfirst = l0 + r;
+                            } else if (x == lmin && x != TC_BIG) {
+                                lT += nq[r];
                             }
-                        }
-                        carry = min(carry, __shfl_sync(0xffffffffu, incl, 31));
-                    }
-                    const int D = carry;
-                    int T = 0;
-                    if (D != TC_BIG) {
-                        for (int base = 0; base < C; base += 32) {
-                            const int li = base + lane;
-                            int rm = TC_BIG, nq = 0;
-                            if (li < C) RI::unpack(rinfo[li], rm, nq);
-                            if (rm == D) T += nq;
-                        }
-                    }
-                    T = warp_sum(T);
-                    const int total = warp_sum(tsum);
-                    unsigned long long ctr = ctl.ctr;
-                    int sstar = 1;
-                    if (D != TC_BIG && T > 1) {
-                        if (!prod) {
-                            const unsigned long long c0 = ctr + (unsigned long long)(total - (T - 1));
-                            int smax = 1;
-                            for (int s = 2 + lane; s <= T; s += 32)
-                                if (below_is_zero(key, c0 + (unsigned long long)(s - 2), (uint32_t)s))
-                                    smax = s;
-                            sstar = warp_max(smax);
-                        } else {
-                            sstar = 1 + (int)philox_below(key, ctr, (uint32_t)T);
-                        }
-                    }
-                    if (D != TC_BIG) {
-                        // locate the sstar-th candidate with delta D in scan order
-                        int cum = 0, row_li = 0, need = 1;
-                        for (int base = 0; base < C; base += 32) {
-                            const int li = base + lane;
-                            int rm = TC_BIG, nq = 0;
-                            if (li < C) RI::unpack(rinfo[li], rm, nq);
-                            const int c = (rm == D) ? nq : 0;
-                            const int incl = warp_incl_sum(c, lane);
-                            const int tot = __shfl_sync(0xffffffffu, incl, 31);
-                            if (cum + tot >= sstar) {
-                                const unsigned bm = __ballot_sync(0xffffffffu, cum + incl >= sstar);
-                                const int src = __ffs(bm) - 1;
-                                row_li = base + src;
-                                need = sstar - cum - __shfl_sync(0xffffffffu, incl - c, src);
-                                break;
-                            }
-                            cum += tot;
-                        }
-                        const int v = clist[row_li];
-                        int dv[MAXV];
-                        eval_row<G, S, MAXV>(gamma, stamp, assign, v, kp, k, lig, RG, WPL, W, it32,
-                                             thr, dv);
-                        int b = -1;
-#pragma unroll
-                        for (int j = 0; j < MAXV / EPW; j++) {
-                            if (j < WPL && need > 0) {
-                                int cnt = 0;
-#pragma unroll
-                                for (int e = 0; e < EPW; e++) cnt += dv[j * EPW + e] == D;
-                                const int incl = warp_incl_sum(cnt, lig, RG);
-                                const int tot = __shfl_sync(0xffffffffu, incl, RG - 1, RG);
-                                if (need <= tot) {
-                                    if (incl >= need && incl - cnt < need) {
-                                        int r = need - (incl - cnt);
-#pragma unroll
-                                        for (int e = 0; e < EPW; e++) {
-                                            if (dv[j * EPW + e] == D) {
-                                                if (--r == 0) b = (j * RG + lig) * EPW + e;
-                                            }
-                                        }
-                                    }
-                                    need = 0;
-                                } else {
-                                    need -= tot;
+                            if (!prod && x != TC_BIG) {
+                                if (x == RM) {
+                                    tsum += nq[r];
+                                } else if (x < RM) {  // lowers the running minimum: walk it
+                                    const Row<G, S> row(gamma, stamp, assign, clist[l0 + r], kp, k, it32, thr);
+                                    tsum += row.ties(RM);
                                 }
                             }
+                            RM = min(RM, x);
                         }
-                        b = warp_max(b, 32);
+                        carry = min(carry, __shfl_sync(FULL, incl, 31));
+                    }
+                    const int D = carry;
+                    PH(2);
+                    int mv_v = -1, mv_a = 0, mv_b = 0, gvb = 0;
+                    int64_t s0 = 0, s1 = 0;
+                    constexpr int NB = 8;  // neighbour chunks of 32 held in registers
+                    int uu[NB];
+                    int v_guess = -1;
+                    if (D != TC_BIG) {
+                        const int T = __reduce_add_sync(FULL, lmin == D ? lT : 0);
+                        const int L = (int)__reduce_min_sync(FULL, (unsigned)(lmin == D ? lfirst : INT_MAX));
+                        // speculative prefetch: adjacency of the first D-row's vertex (the
+                        // winner whenever the reservoir keeps rank 1 or stays in that row)
+                        v_guess = clist[L];
+                        {
+                            const int64_t g0 = row_begin(v_guess), g1 = row_begin(v_guess + 1);
+#pragma unroll
+                            for (int j = 0; j < NB; j++) {
+                                const int64_t idx = g0 + j * 32 + lane;
+                                uu[j] = idx < g1 ? __ldg(P.indices + idx) : 0;
+                            }
+                        }
+                        const int total = __reduce_add_sync(FULL, tsum);
+                        const unsigned long long ctr = ctl.ctr;
+                        int sstar = 1;
+                        if (T > 1) {
+                            if (!prod) {
+                                const unsigned long long c0 = ctr + (unsigned long long)(total - (T - 1));
+                                int smax = 1;
+                                for (int s = 2 + lane; s <= T; s += 32)
+                                    if (below_is_zero(key, c0 + (unsigned long long)(s - 2), (uint32_t)s))
+                                        smax = s;
+                                sstar = __reduce_max_sync(FULL, smax);
+                            } else {
+                                sstar = 1 + (int)philox_below(key, ctr, (uint32_t)T);
+                            }
+                        }
+                        PH(3);
+                        int row_li = L, need = 1;
+                        if (sstar > 1) {  // rank sstar among the D-candidates in scan order
+                            int cum = 0;
+                            for (int base = 0; base < C; base += 32) {
+                                const int li = base + lane;
+                                int rm = TC_BIG, nq = 0;
+                                if (li < C) RI::unpack(rinfo[li], rm, nq);
+                                const int c = (rm == D) ? nq : 0;
+                                const int incl = warp_incl_sum(c, lane);
+                                const int tot = __shfl_sync(FULL, incl, 31);
+                                if (cum + tot >= sstar) {
+                                    const unsigned bm = __ballot_sync(FULL, cum + incl >= sstar);
+                                    const int src = __ffs(bm) - 1;
+                                    row_li = base + src;
+                                    need = sstar - cum - __shfl_sync(FULL, incl - c, src);
+                                    break;
+                                }
+                                cum += tot;
+                            }
+                        }
+                        PH(4);
                         if (lane == 0) {
-                            const int a = assign[v];
+                            const int v = clist[row_li];
+                            const Row<G, S> row(gamma, stamp, assign, v, kp, k, it32, thr);
+                            const int b = row.find(D, need);
+                            const int a = row.a;
                             const long long nconf = conflicts + D;
                             unsigned long long c = ctr;
                             uint32_t ll;
@@ -521,16 +609,12 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
                                 c += 2;
                             }
                             const long long tt = (long long)ll + (6LL * nconf) / 10LL;
-                            if (tt >= (long long)SWEEP) ctl.ovf = 1;
+                            if (tt >= (long long)SWEEP || b < 0) ctl.ovf = 1;
                             stamp[(size_t)v * kp + a] = (S)(uint32_t)(it + tt + 1);
-                            ctl.mv_v = v;
-                            ctl.mv_a = a;
-                            ctl.mv_b = b;
-                            ctl.mv_gvb = gamma[(size_t)v * kp + b];
+                            gvb = gamma[(size_t)v * kp + b];
+                            assign[v] = (uint8_t)b;
                             ctl.conflicts = nconf;
                             ctl.ctr = c;
-                            ctl.has_move = 1;
-                            assign[v] = (uint8_t)b;
                             const long long nl = ctl.nlog;
                             if (nl < P.log_cap) {
                                 const size_t o = (size_t)ind * P.log_cap + nl;
@@ -539,46 +623,25 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
                                 P.log_tt[o] = tt;
                                 ctl.nlog = nl + 1;
                             }
-                            ctl.sum_deg += P.indptr[v + 1] - P.indptr[v];
+                            s0 = row_begin(v);
+                            s1 = row_begin(v + 1);
+                            ctl.sum_deg += s1 - s0;
+                            mv_v = v;
+                            mv_a = a;
+                            mv_b = b;
                         }
-                    } else if (lane == 0) {
-                        ctl.has_move = 0;
+                        mv_v = __shfl_sync(FULL, mv_v, 0);
+                        mv_a = __shfl_sync(FULL, mv_a, 0);
+                        mv_b = __shfl_sync(FULL, mv_b, 0);
+                        s0 = __shfl_sync(FULL, s0, 0);
+                        s1 = __shfl_sync(FULL, s1, 0);
                     }
-                    if (lane == 0) {
-                        ctl.sum_c += C;
-                        ctl.nev = 0;
-                    }
-                }
-                __syncthreads();
-
-                // pass 5: gamma update over N(v) + conflict-set events (:356-359)
-                const bool mv = ctl.has_move != 0;
-                if (mv) {
-                    const int v = ctl.mv_v, a = ctl.mv_a, b = ctl.mv_b;
-                    const int64_t s0 = P.indptr[v], s1 = P.indptr[v + 1];
-                    for (int64_t idx = s0 + tid; idx < s1; idx += NT) {
-                        const int u = P.indices[idx];
-                        G *row = gamma + (size_t)u * kp;
-                        const int ga = (int)row[a] - 1;
-                        row[a] = (G)ga;
-                        const int gb = row[b];
-                        if (gb >= GMAX) ctl.ovf = 1;
-                        else row[b] = (G)(gb + 1);
-                        const int au = assign[u];
-                        if ((au == a && ga == 0) || (au == b && gb == 0)) {
-                            const int slot = atomicAdd(&ctl.nev, 1);
-                            if (slot < TC_EVCAP) evl[slot] = ((uint32_t)(idx - s0) << 16) | (uint32_t)u;
-                        }
-                    }
-                }
-                __syncthreads();
-
-                // pass 6: conflict-list maintenance in neighbour order, then v (:368-390)
-                if (tid == 0) {
-                    if (mv) {
-                        const int v = ctl.mv_v;
-                        int Cn = ctl.C;
-                        const int nev = ctl.nev;
+                    PH(5);
+                    if (mv_v >= 0) {
+                        // gamma update over N(v) (:356-359) and conflict-list events in
+                        // neighbour order (:368-385): NB*32 neighbours per batch, all
+                        // loads in flight together, events applied in ballot order
+                        int Cn = C;
                         auto apply = [&](int u, bool in_conf) {
                             const int pu = cpos[u];
                             if (in_conf && pu == 0xFFFF) {
@@ -593,49 +656,77 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
                                 cpos[u] = 0xFFFF;
                             }
                         };
-                        if (nev <= TC_EVCAP) {
-                            for (int i = 1; i < nev; i++) {  // insertion sort by position
-                                const uint32_t x = evl[i];
-                                int j = i - 1;
-                                while (j >= 0 && evl[j] > x) {
-                                    evl[j + 1] = evl[j];
-                                    j--;
+                        bool bad = false;
+                        bool have = (mv_v == v_guess);
+                        for (int64_t b0 = s0; b0 < s1; b0 += 32 * NB) {
+                            if (!have) {
+#pragma unroll
+                                for (int j = 0; j < NB; j++) {
+                                    const int64_t idx = b0 + j * 32 + lane;
+                                    uu[j] = idx < s1 ? __ldg(P.indices + idx) : 0;
                                 }
-                                evl[j + 1] = x;
                             }
-                            for (int i = 0; i < nev; i++) {
-                                const int u = evl[i] & 0xFFFF;
-                                apply(u, cpos[u] == 0xFFFF);  // enter iff outside, leave iff inside
+                            have = false;
+                            unsigned em[NB];
+#pragma unroll
+                            for (int j = 0; j < NB; j++) {
+                                const int64_t idx = b0 + j * 32 + lane;
+                                bool evt = false;
+                                if (idx < s1) {
+                                    const int u = uu[j];
+                                    G *row = gamma + (size_t)u * kp;
+                                    const int ga = (int)row[mv_a] - 1;
+                                    row[mv_a] = (G)ga;
+                                    const int gb = row[mv_b];
+                                    if (gb >= GMAX) bad = true;
+                                    else row[mv_b] = (G)(gb + 1);
+                                    const int au = assign[u];
+                                    evt = (au == mv_a && ga == 0) || (au == mv_b && gb == 0);
+                                }
+                                em[j] = __ballot_sync(FULL, evt);
                             }
-                        } else {
-                            const int64_t s0 = P.indptr[v], s1 = P.indptr[v + 1];
-                            for (int64_t idx = s0; idx < s1; idx++) {
-                                const int u = P.indices[idx];
-                                apply(u, gamma[(size_t)u * kp + assign[u]] > 0);
+#pragma unroll
+                            for (int j = 0; j < NB; j++) {
+                                unsigned e = em[j];
+                                while (e) {
+                                    const int src = __ffs(e) - 1;
+                                    e &= e - 1u;
+                                    const int u = __shfl_sync(FULL, uu[j], src);
+                                    if (lane == 0) apply(u, cpos[u] == 0xFFFF);  // enter iff outside
+                                }
                             }
                         }
-                        apply(v, ctl.mv_gvb > 0);
-                        ctl.C = Cn;
-                        if (ctl.conflicts < ctl.best) {
-                            ctl.best = ctl.conflicts;
-                            ctl.copy = 1;
-                        } else {
-                            ctl.copy = 0;
+                        PH(6);
+                        if (__any_sync(FULL, bad) && lane == 0) ctl.ovf = 1;
+                        bool improved = false;
+                        if (lane == 0) {
+                            apply(mv_v, gvb > 0);
+                            ctl.C = Cn;
+                            if (ctl.conflicts < ctl.best) {
+                                ctl.best = ctl.conflicts;
+                                improved = true;
+                            }
                         }
-                    } else {
-                        ctl.copy = 0;
+                        if (__shfl_sync(FULL, improved, 0)) {
+                            __syncwarp();
+                            for (int v = lane; v < n; v += 32) b_out[v] = assign[v];
+                        }
                     }
-                    ctl.it = it + 1;
+                    if (lane == 0) {
+                        ctl.sum_c += C;
+                        ctl.it = it + 1;
+                    }
+                    PH(7);
                 }
                 __syncthreads();
+                PH(8);
                 const long long itn = it + 1;
                 const bool chk = diagf && (itn % 1024 == 0);
                 const bool swp = (itn % SWEEP) == 0;
-                if (ctl.copy)
-                    for (int v = tid; v < n; v += NT) b_out[v] = assign[v];
                 if (chk) {  // scratch conflicts over the edge list (:398-405)
                     long long c2 = 0;
-                    for (int64_t e = tid; e < P.m; e += NT) c2 += assign[P.eu[e]] == assign[P.ev[e]];
+                    for (int64_t e = tid; e < P.m; e += NT)
+                        c2 += assign[__ldg(P.eu + e)] == assign[__ldg(P.ev + e)];
                     c2 = warp_sum64(c2);
                     if (lane == 0) ctl.red[warp] = c2;
                 }
@@ -650,11 +741,16 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
                     for (int j = 0; j < NW; j++) s += ctl.red[j];
                     if (s != ctl.conflicts) ctl.diag += 1;
                 }
+                PH(9);
             }
         }
         __syncthreads();
 
         // ---------------- outputs (:407-410) ----------------
+        if (profile && tid == 0) {
+            for (int q = 1; q < 10; q++) atomicAdd(&g_phase_cycles[q], (unsigned long long)ctl.ph[q]);
+            atomicAdd(&g_phase_cycles[10], (unsigned long long)ctl.it);
+        }
         if (!ctl.ovf) {
             for (int v = tid; v < n; v += NT) a_io[v] = assign[v];
             if (tid == 0) {
@@ -680,15 +776,20 @@ __global__ void __launch_bounds__(TC_NT) tabucol_kernel(TabuParams P) {
     }
 }
 
+__global__ void indptr_to_u32(const int64_t *in, uint32_t *out, int count) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+        out[i] = (uint32_t)in[i];
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static size_t misc_bytes(int n, size_t rowinfo_bytes) {
     return (size_t)((n + 15) & ~15) + 2 * (size_t)((2 * n + 15) & ~15) +
-           ((rowinfo_bytes * n + 15) & ~(size_t)15) + TC_EVCAP * 4;
+           ((rowinfo_bytes * n + 15) & ~(size_t)15);
 }
 
-template <typename G, typename S, bool GSM, bool SSM>
+template <typename G, typename S, bool GSM, bool SSM, int NT>
 static int launch_variant(TabuParams P, int max_grid, int p_hint, cudaStream_t st, int *grid_out,
                           size_t *smem_out, bool query_only) {
     using RowT = typename RowInfoT<G>::T;
@@ -696,12 +797,12 @@ static int launch_variant(TabuParams P, int max_grid, int p_hint, cudaStream_t s
     size_t smem = misc_bytes(P.n, sizeof(RowT));
     if (GSM) smem += (tab * sizeof(G) + 15) & ~(size_t)15;
     if (SSM) smem += (tab * sizeof(S) + 15) & ~(size_t)15;
-    auto kern = tabucol_kernel<G, S, GSM, SSM>;
+    auto kern = tabucol_kernel<G, S, GSM, SSM, NT>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return set_error(MCB_ERR_CUDA, "cudaFuncSetAttribute(smem=%zu) failed", smem);
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TC_NT, smem) != cudaSuccess || nb < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, smem) != cudaSuccess || nb < 1)
         return set_error(MCB_ERR_CUDA, "tabucol: no occupancy for smem=%zu", smem);
     int grid = std::min(p_hint, nb * num_sms());
     if (max_grid > 0) grid = std::min(grid, max_grid);
@@ -709,12 +810,37 @@ static int launch_variant(TabuParams P, int max_grid, int p_hint, cudaStream_t s
     *grid_out = grid;
     *smem_out = smem;
     if (query_only) return MCB_OK;
-    kern<<<grid, TC_NT, smem, st>>>(P);
+    kern<<<grid, NT, smem, st>>>(P);
     if (cudaGetLastError() != cudaSuccess) return set_error(MCB_ERR_CUDA, "tabucol launch failed");
     return MCB_OK;
 }
 
 static bool fits_smem(size_t bytes) { return bytes <= (size_t)max_smem_optin(); }
+
+static int env_nt() {
+    const char *e = getenv("MCB_TABU_NT");
+    return e ? atoi(e) : 0;
+}
+
+template <int NT>
+static int launch_narrow(int variant, TabuParams &P, int grid_cap, int p, cudaStream_t st, int *grid,
+                         size_t *smem, bool q) {
+    switch (variant) {
+        case 0: return launch_variant<int8_t, uint16_t, true, true, NT>(P, grid_cap, p, st, grid, smem, q);
+        case 1: return launch_variant<int8_t, uint16_t, true, false, NT>(P, grid_cap, p, st, grid, smem, q);
+        default: return launch_variant<int8_t, uint16_t, false, false, NT>(P, grid_cap, p, st, grid, smem, q);
+    }
+}
+
+int tabucol_phase_cycles(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 16) != cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "phase counters unavailable");
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+    }
+    return MCB_OK;
+}
 
 int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     if (A.p < 0 || A.n < 1 || A.k < 1 || A.depth < 0 || A.m < 0)
@@ -761,46 +887,46 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     else if (!force_glob && fits_smem(g8 + s16 + misc8)) variant = 0;
     else if (!force_glob && fits_smem(g8 + misc8)) variant = 1;
     else variant = 2;
+    const int nt = env_nt() == 128 ? 128 : 256;
 
-    // work counters, overflow list, error flag
     const int grid_cap = 8 * num_sms();
     const size_t ctl_bytes = 256 + sizeof(int32_t) * (size_t)A.p;
-    // global tables: narrow variant (per CTA) and wide fallback (per CTA)
     const size_t ng_stride = (tab * 1 + 255) & ~(size_t)255, ns_stride = (tab * 2 + 255) & ~(size_t)255;
     const size_t wg_stride = (tab * 2 + 255) & ~(size_t)255, ws_stride = (tab * 4 + 255) & ~(size_t)255;
     const int wide_grid = std::min<int>((int)A.p, 2 * num_sms());
+    const size_t indptr_bytes = 4 * (size_t)(n + 1);
 
     int grid = 1;
     size_t smem = 0;
     int rc;
-    // query grid for the narrow variant first (to size its workspace)
-    auto set_rows = [&](TabuParams &Q, int gbytes) {
-        const int words = kp * gbytes / 4;
-        int rg = 1;
-        while (rg < words && rg < 32) rg <<= 1;
-        Q.rg = rg;
-        Q.words = words;
-        Q.wpl = (words + rg - 1) / rg;
-    };
     size_t narrow_ws = 0;
     if (variant != 3) {
-        set_rows(P, 1);
-        switch (variant) {
-            case 0: rc = launch_variant<int8_t, uint16_t, true, true>(P, grid_cap, (int)A.p, st, &grid, &smem, true); break;
-            case 1: rc = launch_variant<int8_t, uint16_t, true, false>(P, grid_cap, (int)A.p, st, &grid, &smem, true); break;
-            default: rc = launch_variant<int8_t, uint16_t, false, false>(P, grid_cap, (int)A.p, st, &grid, &smem, true); break;
-        }
+        rc = nt == 128 ? launch_narrow<128>(variant, P, grid_cap, (int)A.p, st, &grid, &smem, true)
+                       : launch_narrow<256>(variant, P, grid_cap, (int)A.p, st, &grid, &smem, true);
         if (rc) return rc;
         if (variant == 1) narrow_ws = (size_t)grid * ns_stride;
         if (variant == 2) narrow_ws = (size_t)grid * (ng_stride + ns_stride);
     }
     const size_t wide_ws = (size_t)wide_grid * (wg_stride + ws_stride);
-    uint8_t *ws = (uint8_t *)workspace(ctl_bytes + narrow_ws + wide_ws + 512);
+    const size_t tables_off = (ctl_bytes + 255) & ~(size_t)255;
+    const size_t indptr_off = tables_off + ((narrow_ws + wide_ws + 255) & ~(size_t)255);
+    uint8_t *ws = (uint8_t *)workspace(indptr_off + indptr_bytes + 256);
     if (!ws) return set_error(MCB_ERR_CUDA, "tabucol: workspace allocation failed");
     int32_t *ctl32 = reinterpret_cast<int32_t *>(ws);  // [0]=work(narrow) [1]=work(wide) [2]=ovf_count [3]=err
     if (cudaMemsetAsync(ws, 0, 256, st) != cudaSuccess) return set_error(MCB_ERR_CUDA, "memset failed");
     P.err_flag = ctl32 + 3;
-    uint8_t *tables = ws + ((ctl_bytes + 255) & ~(size_t)255);
+    uint8_t *tables = ws + tables_off;
+
+    // CSR row offsets -> __constant__ (u32) when they fit
+    P.const_indptr = 0;
+    if (n + 1 <= TC_CONST_INDPTR && 2 * A.m < (int64_t)UINT32_MAX) {
+        uint32_t *tmp = reinterpret_cast<uint32_t *>(ws + indptr_off);
+        indptr_to_u32<<<(n + 256) / 256, 256, 0, st>>>(A.indptr, tmp, n + 1);
+        if (cudaMemcpyToSymbolAsync(c_indptr, tmp, indptr_bytes, 0, cudaMemcpyDeviceToDevice, st) !=
+            cudaSuccess)
+            return set_error(MCB_ERR_CUDA, "tabucol: constant upload failed");
+        P.const_indptr = 1;
+    }
 
     if (variant != 3) {
         P.work_counter = ctl32 + 0;
@@ -815,16 +941,12 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
             P.ws_stamp = tables + (size_t)grid * ng_stride;
             P.ws_s_stride = ns_stride;
         }
-        switch (variant) {
-            case 0: rc = launch_variant<int8_t, uint16_t, true, true>(P, grid_cap, (int)A.p, st, &grid, &smem, false); break;
-            case 1: rc = launch_variant<int8_t, uint16_t, true, false>(P, grid_cap, (int)A.p, st, &grid, &smem, false); break;
-            default: rc = launch_variant<int8_t, uint16_t, false, false>(P, grid_cap, (int)A.p, st, &grid, &smem, false); break;
-        }
+        rc = nt == 128 ? launch_narrow<128>(variant, P, grid_cap, (int)A.p, st, &grid, &smem, false)
+                       : launch_narrow<256>(variant, P, grid_cap, (int)A.p, st, &grid, &smem, false);
         if (rc) return rc;
     }
     // wide pass: either everything (forced) or the overflowed individuals
     TabuParams Q = P;
-    set_rows(Q, 2);
     Q.work_counter = ctl32 + 1;
     Q.ovf_list = nullptr;
     Q.ovf_count = nullptr;
@@ -837,7 +959,8 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     Q.ws_stamp = tables + narrow_ws + (size_t)wide_grid * wg_stride;
     Q.ws_s_stride = ws_stride;
     int g2 = 1;
-    rc = launch_variant<int16_t, uint32_t, false, false>(Q, wide_grid, (int)A.p, st, &g2, &smem, false);
+    rc = launch_variant<int16_t, uint32_t, false, false, 256>(Q, wide_grid, (int)A.p, st, &g2, &smem,
+                                                               false);
     if (rc) return rc;
 
     int32_t err = 0;
