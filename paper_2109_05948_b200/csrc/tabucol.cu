@@ -9,36 +9,38 @@
 //   * tabu test `it < tabu[v,c]` with aspiration `conflicts + d < best` (:336-339);
 //   * reservoir tie-break: the SplitMix64 counter advances once per candidate
 //     that ties the running minimum (:340-350); tenure draw
-//     `U{0..9} + (6*conflicts_after)//10` (:363-366), last-write-wins stamp;
+//     `U{0..9} + (6*conflicts_after)//10` (:363-366), last-write-wins expiry;
 //   * early exit at zero conflicts (:322), `it` counts no-move iterations (:398),
 //     O(m) scratch check every 1024 iterations -> diag (:398-405).
 //
-// One iteration = two block barriers:
-//   pass 1 (all threads)  thread-per-row: each conflicting vertex's k-1
-//          candidates are evaluated 4 at a time with byte-SIMD (int8 deltas,
-//          u16 wrap-around tabu stamps, aspiration) -> (row min, #at min).
-//   pass 2 (warp 0)       exclusive prefix-min over the row minima.  A tie
-//          event of the sequential reservoir is a candidate equal to the
-//          running minimum: rows above the running minimum contribute none,
-//          rows equal to it contribute #min, and the few rows that LOWER it are
-//          re-walked lane-locally.  That yields the global minimum D, its
-//          multiplicity T and the counter offset E of D's group, so the T-1
-//          reservoir draws (counter ctr+E+s-2 for rank s) are independent: the
-//          winner is the last rank whose draw is zero (warp max).
-//          Then the winner is located, the tenure drawn, gamma updated over
-//          N(v) by the warp (32 neighbours per step) and conflict-set events
-//          applied in neighbour order (ballot order), then v itself.
+// Iteration structure (NT threads, two block barriers):
+//   pass 1 (all threads, one conflicting vertex per thread): the row's
+//     candidates are scanned 4 colours per 32-bit word (u8 gamma; native
+//     VIMNMX.U16x2 byte minima and LOP3/IADD zero-byte counts, branch-free --
+//     no emulated video-SIMD), tabu/aspiration exclusions applied as byte
+//     masks -> (row minimum, #candidates at the minimum).
+//   pass 2 (warp 0): exclusive prefix-min over the rows.  A tie event of the
+//     sequential reservoir is a candidate equal to the running minimum, so rows
+//     above the running minimum hold none, rows equal to it hold #min of them,
+//     and only the few rows that LOWER it need an in-row walk -- queued and
+//     walked one per lane in parallel.  That gives the minimum D, its
+//     multiplicity T and the counter offset of D's group; the T-1 reservoir
+//     draws are independent (rank s uses counter ctr + E + s - 2) and the
+//     winner is the last rank whose draw is zero.  Then locate (parallel over
+//     the row's words), tenure, gamma update over N(v) (adjacency prefetched
+//     speculatively), conflict-list events in neighbour order, best copy.
 //
-// Data layout per individual (shared memory when it fits, else a per-CTA
-// global slice that stays L2-resident):
-//   gamma  int8 [n][kp]  (kp = k rounded up to 4)   -- int16 fallback on overflow
-//   tabu   u16  [n][kp]  wrap-around stamps, swept every 16384 iterations
-//                        -- u32 fallback when a tenure exceeds 16383
-//   assign u8 [n], conflict list / positions u16 [n], per-row (min, count) [n].
-//   CSR row offsets in __constant__ memory (u32) when n < 12288.
-// Individuals whose int8/u16 tables would overflow are re-run from their
-// original start by the wide (int16 / u32) instantiation; results are
-// identical by construction (same arithmetic, wider storage).
+// Tabu state: the reference's dense `tabu_pair[n][k]` int64 table is replaced
+// by 4 (colour, expiry) slots per vertex in shared memory; a vertex needing a
+// 5th live entry spills to a dense per-CTA table in global memory (L2
+// resident), flagged per vertex.  Expiries are 16-bit wrap-around stamps,
+// swept every 16384 iterations (32-bit in the wide variant).
+//
+// Shared memory per individual at G(500,.5) k=48: gamma 24 KB + slots 6 KB +
+// lists 5.5 KB = 37 KB -> 6 CTAs per SM.  Individuals whose u8 gamma (max 254)
+// or 16-bit tenure would overflow are re-run from their start by the wide
+// (u16 gamma / u32 expiry) instantiation; results are identical by
+// construction (same arithmetic, wider storage).
 #include <algorithm>
 #include <climits>
 #include <cstdio>
@@ -52,8 +54,18 @@ namespace mcb {
 
 constexpr int TC_BIG = 1 << 20;
 constexpr int TC_CONST_INDPTR = 12288;
+constexpr int TC_NT = 128;
+constexpr int TC_LOWCAP = 192;
 
 __constant__ uint32_t c_indptr[TC_CONST_INDPTR];
+__device__ unsigned long long g_phase_cycles[16];
+
+#define PH(i)                           \
+    if (profile && tid == 0) {          \
+        const long long _t = clock64(); \
+        ctl.ph[i] += _t - ph_t;         \
+        ph_t = _t;                      \
+    }
 
 struct TabuParams {
     int32_t *assigns;
@@ -77,266 +89,236 @@ struct TabuParams {
     int32_t *work_counter;
     int32_t *ovf_list, *ovf_count;  // individuals to redo wide
     int32_t *err_flag;
-    uint8_t *ws_gamma, *ws_stamp;  // per-CTA global slices (global variants)
+    uint8_t *ws_gamma;  // per-CTA gamma slice (when gamma is not in smem)
+    uint8_t *ws_stamp;  // per-CTA dense overflow expiry table
     size_t ws_g_stride, ws_s_stride;
     uint32_t flags;
     int const_indptr;
 };
 
-__device__ unsigned long long g_phase_cycles[16];
-#define PH(i)                                          \
-    if (profile && tid == 0) {                         \
-        const long long _t = clock64();                \
-        ctl.ph[i] += _t - ph_t;                        \
-        ph_t = _t;                                     \
-    }
-
+template <int NW>
 struct TabuCtrl {
     long long it, conflicts, best, nlog, sum_c, sum_deg, diag;
     unsigned long long ctr;
     int C, work, ovf;
-    long long ph[12];
-    long long red[32];
-    int wcnt[32];
-};
-
-template <typename G>
-struct RowInfoT;
-template <>
-struct RowInfoT<int8_t> {
-    using T = uint16_t;
-    static constexpr int NONE = 127;
-    __device__ static T pack(int rm, int nq) {
-        return (T)((uint8_t)(int8_t)(rm >= TC_BIG ? NONE : rm) | ((uint32_t)nq << 8));
-    }
-    __device__ static void unpack(T x, int &rm, int &nq) {
-        rm = (int)(int8_t)(x & 0xFF);
-        if (rm == NONE) rm = TC_BIG;
-        nq = x >> 8;
-    }
-};
-template <>
-struct RowInfoT<int16_t> {
-    using T = uint32_t;
-    static constexpr int NONE = 32767;
-    __device__ static T pack(int rm, int nq) {
-        return (T)((uint16_t)(int16_t)(rm >= TC_BIG ? NONE : rm) | ((uint32_t)nq << 16));
-    }
-    __device__ static void unpack(T x, int &rm, int &nq) {
-        rm = (int)(int16_t)(x & 0xFFFF);
-        if (rm == NONE) rm = TC_BIG;
-        nq = (int)(x >> 16);
-    }
+    long long red[NW];
+    int wcnt[NW];
+    long long ph[10];
 };
 
 template <typename S>
-__device__ __forceinline__ bool stamp_active(S st, uint32_t it) {
+__device__ __forceinline__ bool active(S e, uint32_t it) {
     if constexpr (sizeof(S) == 2)
-        return (int16_t)(uint16_t)((uint16_t)st - (uint16_t)it) > 0;
+        return (int16_t)(uint16_t)((uint16_t)e - (uint16_t)it) > 0;
     else
-        return (int32_t)((uint32_t)st - it) > 0;
+        return (int32_t)((uint32_t)e - it) > 0;
 }
 
-// signed byte-min of the 4 bytes of x; *bc = that byte broadcast to 4 lanes
-__device__ __forceinline__ int bmin4(uint32_t x, uint32_t &bc) {
-    uint32_t y = __vmins4(x, __byte_perm(x, 0, 0x3232));
-    y = __vmins4(y, __byte_perm(y, 0, 0x1111));
-    bc = __byte_perm(y, 0, 0x0000);
-    return (int)(int8_t)(y & 0xFFu);
+// number of bytes of x equal to byte value c
+__device__ __forceinline__ int count_eq_bytes(uint32_t x, uint32_t c) {
+    const uint32_t z = x ^ (c * 0x01010101u);
+    const uint32_t t = ((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z;
+    return __popc(~t & 0x80808080u);
+}
+// unsigned byte minimum (native 16x2 min)
+__device__ __forceinline__ uint32_t min_bytes(uint32_t x) {
+    const uint32_t m2 = __vminu2(x & 0x00FF00FFu, (x >> 8) & 0x00FF00FFu);
+    return min(m2 & 0xFFFFu, m2 >> 16);
+}
+// 4 bits -> 4 byte masks
+__device__ __forceinline__ uint32_t expand_nibble(uint32_t nib) {
+    return ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;
 }
 
-// One conflicting vertex's candidate row: delta = gamma[v][c] - gamma[v][a],
-// admissible = c != a && (not tabu || conflicts + delta < best).
-template <typename G, typename S>
-struct Row {
+// Candidate row of one conflicting vertex v.  Candidates are gamma values g
+// (delta = g - gva); excluded: c == a, and live tabu colours without
+// aspiration (g - gva < thr  <=>  g < A).  KQ = 64-colour words of the
+// exclusion mask (1 when k <= 64).
+template <typename G, typename S, int KQ>
+struct RowEval {
+    static constexpr bool NARROW = sizeof(G) == 1;
     const G *g;
-    const S *s;
-    int a, gva, k, W;
-    uint32_t it, gva4, thr4, it2, amask, kmask;
-    int thr, aw;
+    int a, gva, k, kp;
+    uint64_t ex[KQ];
 
-    __device__ __forceinline__ Row(const G *gamma, const S *stamp, const uint8_t *assign, int v, int kp,
-                                   int k_, uint32_t it_, int thr_) {
+    __device__ __forceinline__ void setbit(int c) {
+        const uint64_t b = 1ull << (c & 63);
+        if constexpr (KQ == 1) {
+            ex[0] |= b;
+        } else {
+#pragma unroll
+            for (int q = 0; q < KQ; q++)
+                if ((c >> 6) == q) ex[q] |= b;
+        }
+    }
+    __device__ __forceinline__ uint64_t exq(int q) const {
+        if constexpr (KQ == 1) {
+            return ex[0];
+        } else {
+            uint64_t r = ex[0];
+#pragma unroll
+            for (int j = 1; j < KQ; j++)
+                if (q == j) r = ex[j];
+            return r;
+        }
+    }
+    __device__ __forceinline__ bool excluded(int c) const { return (exq(c >> 6) >> (c & 63)) & 1ull; }
+    // word w of the row with excluded colours forced to 0xFF (narrow path)
+    __device__ __forceinline__ uint32_t word(int w) const {
+        return reinterpret_cast<const uint32_t *>(g)[w] |
+               expand_nibble((uint32_t)(exq(w >> 4) >> (4 * (w & 15))) & 0xFu);
+    }
+
+    __device__ __forceinline__ void init(const G *gamma, const S *texp, const uint8_t *tcol,
+                                         const S *tovf, const S *gstamp, const uint8_t *assign, int v,
+                                         int kp_, int k_, uint32_t it, int thr) {
+        kp = kp_;
+        k = k_;
         a = assign[v];
         g = gamma + (size_t)v * kp;
-        s = stamp + (size_t)v * kp;
         gva = g[a];
-        k = k_;
-        it = it_;
-        thr = thr_;
-        W = kp / 4;
-        if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
-            gva4 = (uint32_t)gva * 0x01010101u;
-            const int t8 = max(thr, -128);
-            thr4 = (uint32_t)(uint8_t)(int8_t)t8 * 0x01010101u;
-            it2 = ((it & 0xFFFFu) << 16) | (it & 0xFFFFu);
-            aw = a >> 2;
-            amask = 0xFFu << (8 * (a & 3));
-            const int rem = k & 3;
-            kmask = rem ? (0xFFFFFFFFu >> (8 * (4 - rem))) : 0xFFFFFFFFu;
+        const int A = thr + gva;
+#pragma unroll
+        for (int q = 0; q < KQ; q++) ex[q] = 0;
+        setbit(a);
+        const uint32_t cols = reinterpret_cast<const uint32_t *>(tcol)[v];
+        if (cols != 0xFFFFFFFFu) {
+            S e[4];
+            if constexpr (sizeof(S) == 2) {
+                const uint2 x = reinterpret_cast<const uint2 *>(texp)[v];
+                e[0] = (S)x.x;
+                e[1] = (S)(x.x >> 16);
+                e[2] = (S)x.y;
+                e[3] = (S)(x.y >> 16);
+            } else {
+                const uint4 x = reinterpret_cast<const uint4 *>(texp)[v];
+                e[0] = x.x;
+                e[1] = x.y;
+                e[2] = x.z;
+                e[3] = x.w;
+            }
+#pragma unroll
+            for (int s = 0; s < 4; s++) {
+                const int c = (cols >> (8 * s)) & 0xFF;
+                if (c != 0xFF && active<S>(e[s], it) && !((int)g[c] < A)) setbit(c);
+            }
         }
-    }
-    // narrow path: 4 candidates (colours 4w..4w+3) as signed bytes, 127 = inadmissible
-    __device__ __forceinline__ uint32_t word(int w) const {
-        const uint32_t gw = reinterpret_cast<const uint32_t *>(g)[w];
-        const uint2 st = reinterpret_cast<const uint2 *>(s)[w];
-        const uint32_t d = __vsub4(gw, gva4);
-        const uint32_t m0 = __vcmpgts2(__vsub2(st.x, it2), 0u);
-        const uint32_t m1 = __vcmpgts2(__vsub2(st.y, it2), 0u);
-        const uint32_t tabu = __byte_perm(m0, m1, 0x6420);
-        uint32_t ok = ~tabu | __vcmplts4(d, thr4);
-        if (w == aw) ok &= ~amask;
-        if (w == W - 1) ok &= kmask;
-        return (d & ok) | (0x7F7F7F7Fu & ~ok);
-    }
-    // wide path: one candidate, TC_BIG if inadmissible
-    __device__ __forceinline__ int cand(int c) const {
-        if (c == a) return TC_BIG;
-        const int d = (int)g[c] - gva;
-        if (stamp_active<S>(s[c], it) && !(d < thr)) return TC_BIG;
-        return d;
+        if (active<S>(tovf[v], it)) {  // spilled expiries: dense global row (rare)
+            const S *gs = gstamp + (size_t)v * kp;
+            for (int c = 0; c < k; c++)
+                if (active<S>(gs[c], it) && !((int)g[c] < A)) setbit(c);
+        }
     }
 
-    // (row min, #candidates at the min); min = TC_BIG if none admissible
-    __device__ __forceinline__ void scan(int &rmin, int &nq) const {
-        if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
-            int m = 127, cnt = 0;
+    // (row minimum delta or TC_BIG, #admissible candidates at the minimum)
+    __device__ __forceinline__ void min_count(int &rmin, int &cnt) const {
+        if constexpr (NARROW) {
+            const int W = kp >> 2;
+            int m = 0xFF, c = 0;
 #pragma unroll 4
             for (int w = 0; w < W; w++) {
-                const uint32_t dv = word(w);
-                uint32_t bc;
-                const int wm = bmin4(dv, bc);
-                const int c = __popc(__vcmpeq4(dv, bc)) >> 3;
-                cnt = (wm < m) ? c : (wm == m ? cnt + c : cnt);
+                const uint32_t x = word(w);
+                const int wm = (int)min_bytes(x);
+                const int wc = count_eq_bytes(x, (uint32_t)wm);
+                c = (wm < m) ? wc : (wm == m ? c + wc : c);
                 m = min(m, wm);
             }
-            rmin = (m == 127) ? TC_BIG : m;
-            nq = (m == 127) ? 0 : cnt;
+            rmin = (m == 0xFF) ? TC_BIG : m - gva;
+            cnt = (m == 0xFF) ? 0 : c;
         } else {
-            int m = TC_BIG, cnt = 0;
-            for (int c = 0; c < k; c++) {
-                const int x = cand(c);
-                if (x < m) {
-                    m = x;
-                    cnt = 1;
-                } else if (x == m && x != TC_BIG) {
-                    cnt++;
+            int m = INT_MAX, c = 0;
+            for (int cc = 0; cc < k; cc++) {
+                if (excluded(cc)) continue;
+                const int b = g[cc];
+                if (b < m) {
+                    m = b;
+                    c = 1;
+                } else if (b == m) {
+                    c++;
                 }
             }
-            rmin = m;
-            nq = cnt;
+            rmin = (m == INT_MAX) ? TC_BIG : m - gva;
+            cnt = (m == INT_MAX) ? 0 : c;
         }
     }
-    // (min, count) over words sub, sub+tpr, ... (narrow path only)
-    __device__ __forceinline__ void scan_part(int sub, int tpr, int &rmin, int &nq) const {
-        int m = 127, cnt = 0;
-#pragma unroll 2
-        for (int w = sub; w < W; w += tpr) {
-            const uint32_t dv = word(w);
-            uint32_t bc;
-            const int wm = bmin4(dv, bc);
-            const int c = __popc(__vcmpeq4(dv, bc)) >> 3;
-            cnt = (wm < m) ? c : (wm == m ? cnt + c : cnt);
-            m = min(m, wm);
-        }
-        rmin = (m == 127) ? TC_BIG : m;
-        nq = (m == 127) ? 0 : cnt;
-    }
-    // sequential tie events inside the row when entered with running minimum R
-    __device__ __forceinline__ int ties(int R) const {
-        int cur = R, t = 0;
-        if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
+
+    // exact sequential tie count of the row when entered with running minimum R
+    __device__ __forceinline__ int walk_ties(int R) const {
+        int t = 0;
+        if constexpr (NARROW) {
+            int cur = (R >= TC_BIG) ? 0x100 : R + gva;  // g-space; 0x100 = +inf
+            const int W = kp >> 2;
             for (int w = 0; w < W; w++) {
-                const uint32_t dv = word(w);
-                uint32_t bc;
-                const int wm = bmin4(dv, bc);
-                if (wm == 127 || wm > cur) continue;
+                const uint32_t x = word(w);
+                const int wm = (int)min_bytes(x);
+                if (wm == 0xFF || wm > cur) continue;
                 if (wm == cur) {
-                    t += __popc(__vcmpeq4(dv, bc)) >> 3;
+                    t += count_eq_bytes(x, (uint32_t)cur);
                     continue;
                 }
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
-                    const int x = (int)(int8_t)(dv >> (8 * e));
-                    if (x == 127) continue;
-                    if (x < cur) cur = x;
-                    else if (x == cur) t++;
+                    const int b = (x >> (8 * e)) & 0xFF;
+                    if (b == 0xFF) continue;
+                    if (b < cur) cur = b;
+                    else if (b == cur) t++;
                 }
             }
         } else {
+            int cur = R;
             for (int c = 0; c < k; c++) {
-                const int x = cand(c);
-                if (x == TC_BIG) continue;
-                if (x < cur) cur = x;
-                else if (x == cur) t++;
+                if (excluded(c)) continue;
+                const int d = (int)g[c] - gva;
+                if (d < cur) cur = d;
+                else if (d == cur) t++;
             }
         }
         return t;
     }
-    // colour of the j-th (1-based) admissible candidate with delta D
-    __device__ __forceinline__ int find(int D, int j) const {
-        if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
-            const uint32_t d4 = (uint32_t)(uint8_t)(int8_t)D * 0x01010101u;
-            for (int w = 0; w < W; w++) {
-                const uint32_t eq = __vcmpeq4(word(w), d4);
-                const int c = __popc(eq) >> 3;
-                if (j <= c) {
-#pragma unroll
-                    for (int e = 0; e < 4; e++)
-                        if ((eq >> (8 * e)) & 1u)
-                            if (--j == 0) return 4 * w + e;
-                }
-                j -= c;
-            }
-        } else {
-            for (int c = 0; c < k; c++)
-                if (cand(c) == D && --j == 0) return c;
-        }
-        return -1;
-    }
 };
 
-template <typename G, typename S, bool GSM, bool SSM, int NT>
+template <typename G, typename S, bool GSM, int KQ, int NT>
 __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
     constexpr int NW = NT / 32;
-    constexpr int GMAX = sizeof(G) == 1 ? 127 : 32767;
+    constexpr bool NARROW = sizeof(G) == 1;
+    constexpr int GMAX = NARROW ? 254 : 65534;
     constexpr uint32_t SWEEP = sizeof(S) == 2 ? 16384u : (1u << 30);
     constexpr unsigned FULL = 0xffffffffu;
-    using RI = RowInfoT<G>;
-    using RowT = typename RI::T;
+    using RE = RowEval<G, S, KQ>;
 
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ TabuCtrl ctl;
+    __shared__ TabuCtrl<NW> ctl;
 
     const int n = P.n, k = P.k, kp = P.kp;
     size_t off = 0;
     G *gamma;
-    S *stamp;
     if constexpr (GSM) {
         gamma = reinterpret_cast<G *>(smem + off);
         off += ((size_t)n * kp * sizeof(G) + 15) & ~(size_t)15;
     } else {
         gamma = reinterpret_cast<G *>(P.ws_gamma + blockIdx.x * P.ws_g_stride);
     }
-    if constexpr (SSM) {
-        stamp = reinterpret_cast<S *>(smem + off);
-        off += ((size_t)n * kp * sizeof(S) + 15) & ~(size_t)15;
-    } else {
-        stamp = reinterpret_cast<S *>(P.ws_stamp + blockIdx.x * P.ws_s_stride);
-    }
+    S *texp = reinterpret_cast<S *>(smem + off);
+    off += ((size_t)n * 4 * sizeof(S) + 15) & ~(size_t)15;
+    uint8_t *tcol = smem + off;
+    off += ((size_t)n * 4 + 15) & ~(size_t)15;
+    S *tovf = reinterpret_cast<S *>(smem + off);
+    off += ((size_t)n * sizeof(S) + 15) & ~(size_t)15;
     uint8_t *assign = smem + off;
     off += (n + 15) & ~15;
     uint16_t *clist = reinterpret_cast<uint16_t *>(smem + off);
     off += (2 * n + 15) & ~15;
     uint16_t *cpos = reinterpret_cast<uint16_t *>(smem + off);
     off += (2 * n + 15) & ~15;
-    RowT *rinfo = reinterpret_cast<RowT *>(smem + off);
+    int2 *rmc = reinterpret_cast<int2 *>(smem + off);  // per row: (min delta, count)
+    off += ((size_t)8 * n + 15) & ~(size_t)15;
+    int2 *lowl = reinterpret_cast<int2 *>(smem + off);  // queued rows lowering the running min
+    S *gstamp = reinterpret_cast<S *>(P.ws_stamp + blockIdx.x * P.ws_s_stride);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool diagf = (P.flags & MCB_FLAG_DIAG) != 0;
     const bool prod = (P.flags & MCB_FLAG_PRODUCTION) != 0;
     const bool profile = (P.flags & MCB_FLAG_PROFILE) != 0;
-    const size_t tab_elems = (size_t)n * kp;
     const bool cidx = P.const_indptr != 0;
     auto row_begin = [&](int v) -> int64_t { return cidx ? (int64_t)c_indptr[v] : P.indptr[v]; };
 
@@ -359,19 +341,22 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                 c = 0;
             }
             assign[v] = (uint8_t)c;
+            reinterpret_cast<uint32_t *>(tcol)[v] = 0xFFFFFFFFu;
+            tovf[v] = (S)0;
         }
         {
+            // gamma rows: real colours 0, padding colours all-ones (never a candidate)
             uint32_t *g32 = reinterpret_cast<uint32_t *>(gamma);
-            const size_t gw = tab_elems * sizeof(G) / 4;
-            for (size_t i = tid; i < gw; i += NT) g32[i] = 0u;
-            uint32_t *s32 = reinterpret_cast<uint32_t *>(stamp);
-            const size_t sw = tab_elems * sizeof(S) / 4;
-            for (size_t i = tid; i < sw; i += NT) s32[i] = 0u;
+            const int wpr = kp * (int)sizeof(G) / 4;  // words per row
+            const uint32_t padw = NARROW ? ((k & 3) ? (0xFFFFFFFFu << (8 * (k & 3))) : 0u)
+                                         : ((k & 1) ? 0xFFFF0000u : 0u);
+            for (size_t i = tid; i < (size_t)n * wpr; i += NT)
+                g32[i] = ((int)(i % wpr) == wpr - 1) ? padw : 0u;
         }
         if (tid == 0) {
             ctl.ovf = 0;
             ctl.diag = 0;
-            for (int q = 0; q < 12; q++) ctl.ph[q] = 0;
+            for (int q = 0; q < 10; q++) ctl.ph[q] = 0;
         }
         __syncthreads();
         // gamma[u][c] = #neighbours of u coloured c; each thread owns its rows
@@ -398,9 +383,9 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                 const int v = ch + tid;
                 bool f = false;
                 if (v < n) {
-                    const int g = gamma[(size_t)v * kp + assign[v]];
-                    f = g > 0;
-                    c2 += g;
+                    const int gv = gamma[(size_t)v * kp + assign[v]];
+                    f = gv > 0;
+                    c2 += gv;
                 }
                 const unsigned bal = __ballot_sync(FULL, f);
                 if (lane == 0) ctl.wcnt[warp] = __popc(bal);
@@ -455,87 +440,86 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                 const int thr = (int)max(best - conflicts, (long long)-TC_BIG);
                 const uint32_t it32 = (uint32_t)it;
 
-                // pass 1: (min, count) over admissible candidates of every row;
-                // tpr threads per row (power of two) when rows are few
-                {
-                    int tpr = 1;
-                    if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
-                        const int W = kp / 4;
-                        while (tpr < 16 && tpr * 2 * C <= NT && tpr * 2 <= W) tpr *= 2;
-                    }
-                    const int sub = tid & (tpr - 1);
-                    const int rows_per_pass = NT / tpr;
-                    for (int r0 = 0; r0 < C; r0 += rows_per_pass) {
-                        const int li = r0 + tid / tpr;
-                        int rm = TC_BIG, nq = 0;
-                        if (li < C) {
-                            const Row<G, S> row(gamma, stamp, assign, clist[li], kp, k, it32, thr);
-                            if constexpr (sizeof(G) == 1 && sizeof(S) == 2) {
-                                if (tpr == 1) row.scan(rm, nq);
-                                else row.scan_part(sub, tpr, rm, nq);
-                            } else {
-                                row.scan(rm, nq);
-                            }
-                        }
-                        if (tpr > 1) {  // combine the tpr partial (min, count)
-                            for (int o = 1; o < tpr; o <<= 1) {
-                                const int om = __shfl_xor_sync(0xffffffffu, rm, o);
-                                const int oq = __shfl_xor_sync(0xffffffffu, nq, o);
-                                nq = (om < rm) ? oq : (om == rm ? nq + oq : nq);
-                                rm = min(rm, om);
-                            }
-                        }
-                        if (li < C && sub == 0) rinfo[li] = RI::pack(rm, rm == TC_BIG ? 0 : nq);
-                    }
+                // pass 1: (min, count) of every conflicting row, one row per thread
+                for (int li = tid; li < C; li += NT) {
+                    RE re;
+                    re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[li], kp, k, it32, thr);
+                    int rm, cnt;
+                    re.min_count(rm, cnt);
+                    rmc[li] = make_int2(rm, cnt);
                 }
                 __syncthreads();
-
                 PH(1);
-                // pass 2: warp 0 -- reservoir, move, gamma update, conflict list
+                // pass 2a (warp 0): exclusive prefix-min over the rows (R rows per lane).
+                // Rows above the running minimum hold no tie event, rows equal to it
+                // hold #min of them, rows below it are queued and walked in parallel.
+                int carry = TC_BIG, lmin = TC_BIG, lT = 0, lfirst = INT_MAX, tsum = 0;
                 if (warp == 0) {
-                    // -- exclusive prefix-min over the row minima, R rows per lane
-                    const int R = C <= 32 ? 1 : (C <= 64 ? 2 : 4);
-                    int carry = TC_BIG, lmin = TC_BIG, lT = 0, lfirst = INT_MAX, tsum = 0;
-                    for (int base = 0; base < C; base += 32 * R) {
-                        const int l0 = base + lane * R;
-                        int rm[4], nq[4];
+                    constexpr int R = 4;
+                    int nlow = 0;
+                    auto flush = [&]() {
+                        __syncwarp();
+                        for (int j = lane; j < nlow; j += 32) {
+                            const int2 e = lowl[j];
+                            RE re;
+                            re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[e.x], kp, k, it32, thr);
+                            tsum += re.walk_ties(e.y);
+                        }
+                        __syncwarp();
+                        nlow = 0;
+                    };
+                    for (int r0 = 0; r0 < C; r0 += 32 * R) {
+                        if (nlow > TC_LOWCAP - 32 * R) flush();
+                        int2 mc[R];
                         int lmn = TC_BIG;
 #pragma unroll
-                        for (int r = 0; r < 4; r++) {
-                            rm[r] = TC_BIG;
-                            nq[r] = 0;
-                            if (r < R && l0 + r < C) RI::unpack(rinfo[l0 + r], rm[r], nq[r]);
-                            lmn = min(lmn, rm[r]);
+                        for (int r = 0; r < R; r++) {
+                            const int q = r0 + lane * R + r;
+                            mc[r] = q < C ? rmc[q] : make_int2(TC_BIG, 0);
+                            lmn = min(lmn, mc[r].x);
                         }
                         const int incl = warp_incl_min(lmn, lane);
                         int excl = __shfl_up_sync(FULL, incl, 1);
                         if (lane == 0) excl = TC_BIG;
                         int RM = min(carry, excl);
+                        int lowR[R];
+                        unsigned lowbits = 0;
 #pragma unroll
-                        for (int r = 0; r < 4; r++) {
-                            if (r >= R) break;
-                            const int x = rm[r];
+                        for (int r = 0; r < R; r++) {
+                            const int x = mc[r].x;
+                            const int q = r0 + lane * R + r;
                             if (x < lmin) {
                                 lmin = x;
-                                lT = nq[r];
-                                lfirst = l0 + r;
+                                lT = mc[r].y;
+                                lfirst = q;
                             } else if (x == lmin && x != TC_BIG) {
-                                lT += nq[r];
+                                lT += mc[r].y;
                             }
+                            lowR[r] = RM;
                             if (!prod && x != TC_BIG) {
-                                if (x == RM) {
-                                    tsum += nq[r];
-                                } else if (x < RM) {  // lowers the running minimum: walk it
-                                    const Row<G, S> row(gamma, stamp, assign, clist[l0 + r], kp, k, it32, thr);
-                                    tsum += row.ties(RM);
-                                }
+                                if (x == RM) tsum += mc[r].y;
+                                else if (x < RM) lowbits |= 1u << r;
                             }
                             RM = min(RM, x);
                         }
+                        if (!prod) {
+                            const int cl = __popc(lowbits);
+                            const int ci = warp_incl_sum(cl, lane);
+                            int pos = nlow + ci - cl;
+#pragma unroll
+                            for (int r = 0; r < R; r++)
+                                if ((lowbits >> r) & 1u) lowl[pos++] = make_int2(r0 + lane * R + r, lowR[r]);
+                            nlow += __shfl_sync(FULL, ci, 31);
+                        }
                         carry = min(carry, __shfl_sync(FULL, incl, 31));
                     }
+                    if (nlow) flush();
+                }
+                PH(2);
+
+                // pass 2b (warp 0): reservoir, move, gamma update, conflict list
+                if (warp == 0) {
                     const int D = carry;
-                    PH(2);
                     int mv_v = -1, mv_a = 0, mv_b = 0, gvb = 0;
                     int64_t s0 = 0, s1 = 0;
                     constexpr int NB = 8;  // neighbour chunks of 32 held in registers
@@ -544,8 +528,7 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                     if (D != TC_BIG) {
                         const int T = __reduce_add_sync(FULL, lmin == D ? lT : 0);
                         const int L = (int)__reduce_min_sync(FULL, (unsigned)(lmin == D ? lfirst : INT_MAX));
-                        // speculative prefetch: adjacency of the first D-row's vertex (the
-                        // winner whenever the reservoir keeps rank 1 or stays in that row)
+                        // speculative prefetch: adjacency of the first D-row's vertex
                         v_guess = clist[L];
                         {
                             const int64_t g0 = row_begin(v_guess), g1 = row_begin(v_guess + 1);
@@ -576,9 +559,11 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                             int cum = 0;
                             for (int base = 0; base < C; base += 32) {
                                 const int li = base + lane;
-                                int rm = TC_BIG, nq = 0;
-                                if (li < C) RI::unpack(rinfo[li], rm, nq);
-                                const int c = (rm == D) ? nq : 0;
+                                int c = 0;
+                                if (li < C) {
+                                    const int2 mc = rmc[li];
+                                    c = (mc.x == D) ? mc.y : 0;
+                                }
                                 const int incl = warp_incl_sum(c, lane);
                                 const int tot = __shfl_sync(FULL, incl, 31);
                                 if (cum + tot >= sstar) {
@@ -591,12 +576,54 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                                 cum += tot;
                             }
                         }
+                        // locate the need-th D-candidate of the row (lanes over words)
+                        const int v = clist[row_li];
+                        RE re;
+                        re.init(gamma, texp, tcol, tovf, gstamp, assign, v, kp, k, it32, thr);
+                        int b = -1;
+                        {
+                            const int Dg = D + re.gva;
+                            const int units = NARROW ? (kp >> 2) : k;
+                            int cum = 0;
+                            for (int u0 = 0; u0 < units && b < 0; u0 += 32) {
+                                const int u = u0 + lane;
+                                int c = 0;
+                                uint32_t x = 0;
+                                if (u < units) {
+                                    if constexpr (NARROW) {
+                                        const uint64_t m64 = re.exq(u >> 4);
+                                        x = reinterpret_cast<const uint32_t *>(re.g)[u] |
+                                            expand_nibble((uint32_t)(m64 >> (4 * (u & 15))) & 0xFu);
+                                        c = count_eq_bytes(x, (uint32_t)Dg);
+                                    } else {
+                                        c = (!re.excluded(u) && (int)re.g[u] == Dg) ? 1 : 0;
+                                    }
+                                }
+                                const int incl = warp_incl_sum(c, lane);
+                                const int tot = __shfl_sync(FULL, incl, 31);
+                                if (cum + tot >= need) {
+                                    const unsigned bm = __ballot_sync(FULL, cum + incl >= need);
+                                    const int src = __ffs(bm) - 1;
+                                    int r = need - cum - (incl - c);  // rank inside the unit
+                                    int col = -1;
+                                    if (lane == src) {
+                                        if constexpr (NARROW) {
+#pragma unroll
+                                            for (int e = 0; e < 4; e++)
+                                                if ((int)((x >> (8 * e)) & 0xFF) == Dg && --r == 0 && col < 0)
+                                                    col = 4 * u + e;
+                                        } else {
+                                            col = u;
+                                        }
+                                    }
+                                    b = __shfl_sync(FULL, col, src);
+                                }
+                                cum += tot;
+                            }
+                        }
                         PH(4);
                         if (lane == 0) {
-                            const int v = clist[row_li];
-                            const Row<G, S> row(gamma, stamp, assign, v, kp, k, it32, thr);
-                            const int b = row.find(D, need);
-                            const int a = row.a;
+                            const int a = re.a;
                             const long long nconf = conflicts + D;
                             unsigned long long c = ctr;
                             uint32_t ll;
@@ -610,9 +637,35 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                             }
                             const long long tt = (long long)ll + (6LL * nconf) / 10LL;
                             if (tt >= (long long)SWEEP || b < 0) ctl.ovf = 1;
-                            stamp[(size_t)v * kp + a] = (S)(uint32_t)(it + tt + 1);
-                            gvb = gamma[(size_t)v * kp + b];
-                            assign[v] = (uint8_t)b;
+                            // tabu (v, a) until it + tt + 1: slot hit, free slot, or spill
+                            const S e_new = (S)(uint32_t)(it + tt + 1);
+                            const uint32_t cols = reinterpret_cast<const uint32_t *>(tcol)[v];
+                            int s_hit = -1, s_free = -1;
+#pragma unroll
+                            for (int s = 0; s < 4; s++) {
+                                const int cs = (cols >> (8 * s)) & 0xFF;
+                                if (cs == a) s_hit = s;
+                                else if (s_free < 0 && (cs == 0xFF || !active<S>(texp[4 * v + s], it32)))
+                                    s_free = s;
+                            }
+                            const int s = s_hit >= 0 ? s_hit : s_free;
+                            const bool ovf_live = active<S>(tovf[v], it32);
+                            if (s >= 0) {
+                                tcol[4 * v + s] = (uint8_t)a;
+                                texp[4 * v + s] = e_new;
+                                if (ovf_live) gstamp[(size_t)v * kp + a] = (S)it32;  // supersede
+                            } else {
+                                S *gs = gstamp + (size_t)v * kp;
+                                if (!ovf_live) {  // fresh spill row
+                                    for (int cc = 0; cc < k; cc++) gs[cc] = (S)it32;
+                                    tovf[v] = e_new;
+                                } else if (active<S>(e_new, (uint32_t)tovf[v])) {
+                                    tovf[v] = e_new;
+                                }
+                                gs[a] = e_new;
+                            }
+                            gvb = re.g[b < 0 ? 0 : b];
+                            assign[v] = (uint8_t)(b < 0 ? a : b);
                             ctl.conflicts = nconf;
                             ctl.ctr = c;
                             const long long nl = ctl.nlog;
@@ -628,7 +681,7 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                             ctl.sum_deg += s1 - s0;
                             mv_v = v;
                             mv_a = a;
-                            mv_b = b;
+                            mv_b = b < 0 ? a : b;
                         }
                         mv_v = __shfl_sync(FULL, mv_v, 0);
                         mv_a = __shfl_sync(FULL, mv_a, 0);
@@ -685,6 +738,7 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                                 }
                                 em[j] = __ballot_sync(FULL, evt);
                             }
+                            PH(6);
 #pragma unroll
                             for (int j = 0; j < NB; j++) {
                                 unsigned e = em[j];
@@ -696,7 +750,6 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                                 }
                             }
                         }
-                        PH(6);
                         if (__any_sync(FULL, bad) && lane == 0) ctl.ovf = 1;
                         bool improved = false;
                         if (lane == 0) {
@@ -730,10 +783,19 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                     c2 = warp_sum64(c2);
                     if (lane == 0) ctl.red[warp] = c2;
                 }
-                if (swp) {
+                if (swp) {  // keep 16-bit expiries unambiguous
                     const uint32_t itw = (uint32_t)itn;
-                    for (size_t i = tid; i < tab_elems; i += NT)
-                        if (!stamp_active<S>(stamp[i], itw)) stamp[i] = (S)itw;
+                    for (int v = tid; v < n; v += NT) {
+                        for (int s = 0; s < 4; s++)
+                            if (!active<S>(texp[4 * v + s], itw)) tcol[4 * v + s] = 0xFF;
+                        if (active<S>(tovf[v], itw)) {
+                            S *gs = gstamp + (size_t)v * kp;
+                            for (int c = 0; c < k; c++)
+                                if (!active<S>(gs[c], itw)) gs[c] = (S)itw;
+                        } else {
+                            tovf[v] = (S)itw;
+                        }
+                    }
                 }
                 if (chk || swp) __syncthreads();
                 if (chk && tid == 0) {
@@ -784,53 +846,42 @@ __global__ void indptr_to_u32(const int64_t *in, uint32_t *out, int count) {
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static size_t misc_bytes(int n, size_t rowinfo_bytes) {
-    return (size_t)((n + 15) & ~15) + 2 * (size_t)((2 * n + 15) & ~15) +
-           ((rowinfo_bytes * n + 15) & ~(size_t)15);
+template <typename S>
+static size_t misc_bytes(int n, int nt) {
+    auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    return a16((size_t)n * 4 * sizeof(S)) + a16((size_t)n * 4) + a16((size_t)n * sizeof(S)) +
+           a16(n) + 2 * a16(2 * (size_t)n) + a16(8 * (size_t)n) + (size_t)8 * TC_LOWCAP;
 }
 
-template <typename G, typename S, bool GSM, bool SSM, int NT>
+template <typename G, typename S, bool GSM>
+static size_t smem_bytes(int n, int kp) {
+    size_t s = misc_bytes<S>(n, TC_NT);
+    if (GSM) s += ((size_t)n * kp * sizeof(G) + 15) & ~(size_t)15;
+    return s;
+}
+
+template <typename G, typename S, bool GSM>
 static int launch_variant(TabuParams P, int max_grid, int p_hint, cudaStream_t st, int *grid_out,
-                          size_t *smem_out, bool query_only) {
-    using RowT = typename RowInfoT<G>::T;
-    const size_t tab = (size_t)P.n * P.kp;
-    size_t smem = misc_bytes(P.n, sizeof(RowT));
-    if (GSM) smem += (tab * sizeof(G) + 15) & ~(size_t)15;
-    if (SSM) smem += (tab * sizeof(S) + 15) & ~(size_t)15;
-    auto kern = tabucol_kernel<G, S, GSM, SSM, NT>;
+                          bool query_only) {
+    const size_t smem = smem_bytes<G, S, GSM>(P.n, P.kp);
+    auto kern = (GSM && P.kp <= 64) ? tabucol_kernel<G, S, GSM, 1, TC_NT> : tabucol_kernel<G, S, GSM, 4, TC_NT>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return set_error(MCB_ERR_CUDA, "cudaFuncSetAttribute(smem=%zu) failed", smem);
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NT, smem) != cudaSuccess || nb < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TC_NT, smem) != cudaSuccess || nb < 1)
         return set_error(MCB_ERR_CUDA, "tabucol: no occupancy for smem=%zu", smem);
     int grid = std::min(p_hint, nb * num_sms());
     if (max_grid > 0) grid = std::min(grid, max_grid);
     grid = std::max(grid, 1);
     *grid_out = grid;
-    *smem_out = smem;
     if (query_only) return MCB_OK;
-    kern<<<grid, NT, smem, st>>>(P);
+    kern<<<grid, TC_NT, smem, st>>>(P);
     if (cudaGetLastError() != cudaSuccess) return set_error(MCB_ERR_CUDA, "tabucol launch failed");
     return MCB_OK;
 }
 
 static bool fits_smem(size_t bytes) { return bytes <= (size_t)max_smem_optin(); }
-
-static int env_nt() {
-    const char *e = getenv("MCB_TABU_NT");
-    return e ? atoi(e) : 0;
-}
-
-template <int NT>
-static int launch_narrow(int variant, TabuParams &P, int grid_cap, int p, cudaStream_t st, int *grid,
-                         size_t *smem, bool q) {
-    switch (variant) {
-        case 0: return launch_variant<int8_t, uint16_t, true, true, NT>(P, grid_cap, p, st, grid, smem, q);
-        case 1: return launch_variant<int8_t, uint16_t, true, false, NT>(P, grid_cap, p, st, grid, smem, q);
-        default: return launch_variant<int8_t, uint16_t, false, false, NT>(P, grid_cap, p, st, grid, smem, q);
-    }
-}
 
 int tabucol_phase_cycles(unsigned long long *out, int reset) {
     if (cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 16) != cudaSuccess)
@@ -879,33 +930,28 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
 
     const bool force_wide = (A.flags & MCB_FLAG_FORCE_WIDE) != 0;
     const bool force_glob = (A.flags & MCB_FLAG_FORCE_GLOBAL) != 0;
-    const size_t tab = (size_t)n * kp;
-    const size_t misc8 = misc_bytes(n, 2);
-    const size_t g8 = (tab + 15) & ~(size_t)15, s16 = (tab * 2 + 15) & ~(size_t)15;
-    int variant;  // 0: all smem, 1: gamma smem + stamps global, 2: all global (narrow), 3: wide global
-    if (force_wide) variant = 3;
-    else if (!force_glob && fits_smem(g8 + s16 + misc8)) variant = 0;
-    else if (!force_glob && fits_smem(g8 + misc8)) variant = 1;
-    else variant = 2;
-    const int nt = env_nt() == 128 ? 128 : 256;
+    // 0: narrow, gamma in smem; 1: narrow, gamma global; 2: wide only
+    int variant;
+    if (force_wide) variant = 2;
+    else if (!force_glob && fits_smem(smem_bytes<uint8_t, uint16_t, true>(n, kp))) variant = 0;
+    else variant = 1;
 
-    const int grid_cap = 8 * num_sms();
+    const size_t tab = (size_t)n * kp;
+    const int grid_cap = 16 * num_sms();
     const size_t ctl_bytes = 256 + sizeof(int32_t) * (size_t)A.p;
-    const size_t ng_stride = (tab * 1 + 255) & ~(size_t)255, ns_stride = (tab * 2 + 255) & ~(size_t)255;
+    const size_t ng_stride = (tab + 255) & ~(size_t)255, ns_stride = (tab * 2 + 255) & ~(size_t)255;
     const size_t wg_stride = (tab * 2 + 255) & ~(size_t)255, ws_stride = (tab * 4 + 255) & ~(size_t)255;
     const int wide_grid = std::min<int>((int)A.p, 2 * num_sms());
     const size_t indptr_bytes = 4 * (size_t)(n + 1);
 
-    int grid = 1;
-    size_t smem = 0;
-    int rc;
+    int grid = 1, rc;
     size_t narrow_ws = 0;
-    if (variant != 3) {
-        rc = nt == 128 ? launch_narrow<128>(variant, P, grid_cap, (int)A.p, st, &grid, &smem, true)
-                       : launch_narrow<256>(variant, P, grid_cap, (int)A.p, st, &grid, &smem, true);
+    if (variant != 2) {
+        rc = variant == 0
+                 ? launch_variant<uint8_t, uint16_t, true>(P, grid_cap, (int)A.p, st, &grid, true)
+                 : launch_variant<uint8_t, uint16_t, false>(P, grid_cap, (int)A.p, st, &grid, true);
         if (rc) return rc;
-        if (variant == 1) narrow_ws = (size_t)grid * ns_stride;
-        if (variant == 2) narrow_ws = (size_t)grid * (ng_stride + ns_stride);
+        narrow_ws = (size_t)grid * (ns_stride + (variant == 1 ? ng_stride : 0));
     }
     const size_t wide_ws = (size_t)wide_grid * (wg_stride + ws_stride);
     const size_t tables_off = (ctl_bytes + 255) & ~(size_t)255;
@@ -928,21 +974,19 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
         P.const_indptr = 1;
     }
 
-    if (variant != 3) {
+    if (variant != 2) {
         P.work_counter = ctl32 + 0;
         P.ovf_count = ctl32 + 2;
         P.ovf_list = ctl32 + 64;
+        P.ws_stamp = tables;
+        P.ws_s_stride = ns_stride;
         if (variant == 1) {
-            P.ws_stamp = tables;
-            P.ws_s_stride = ns_stride;
-        } else if (variant == 2) {
-            P.ws_gamma = tables;
+            P.ws_gamma = tables + (size_t)grid * ns_stride;
             P.ws_g_stride = ng_stride;
-            P.ws_stamp = tables + (size_t)grid * ng_stride;
-            P.ws_s_stride = ns_stride;
         }
-        rc = nt == 128 ? launch_narrow<128>(variant, P, grid_cap, (int)A.p, st, &grid, &smem, false)
-                       : launch_narrow<256>(variant, P, grid_cap, (int)A.p, st, &grid, &smem, false);
+        rc = variant == 0
+                 ? launch_variant<uint8_t, uint16_t, true>(P, grid_cap, (int)A.p, st, &grid, false)
+                 : launch_variant<uint8_t, uint16_t, false>(P, grid_cap, (int)A.p, st, &grid, false);
         if (rc) return rc;
     }
     // wide pass: either everything (forced) or the overflowed individuals
@@ -950,7 +994,7 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     Q.work_counter = ctl32 + 1;
     Q.ovf_list = nullptr;
     Q.ovf_count = nullptr;
-    if (variant != 3) {
+    if (variant != 2) {
         Q.work = ctl32 + 64;
         Q.nwork_dev = ctl32 + 2;
     }
@@ -959,8 +1003,7 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     Q.ws_stamp = tables + narrow_ws + (size_t)wide_grid * wg_stride;
     Q.ws_s_stride = ws_stride;
     int g2 = 1;
-    rc = launch_variant<int16_t, uint32_t, false, false, 256>(Q, wide_grid, (int)A.p, st, &g2, &smem,
-                                                               false);
+    rc = launch_variant<uint16_t, uint32_t, false>(Q, wide_grid, (int)A.p, st, &g2, false);
     if (rc) return rc;
 
     int32_t err = 0;
