@@ -60,8 +60,8 @@ constexpr int TC_LOWCAP = 192;
 __constant__ uint32_t c_indptr[TC_CONST_INDPTR];
 __device__ unsigned long long g_phase_cycles[16];
 
-#define PH(i)                           \
-    if (profile && tid == 0) {          \
+#define PH(i)                                   \
+    if (profile && warp == 0 && lane == 0) {    \
         const long long _t = clock64(); \
         ctl.ph[i] += _t - ph_t;         \
         ph_t = _t;                      \
@@ -89,6 +89,7 @@ struct TabuParams {
     int32_t *work_counter;
     int32_t *ovf_list, *ovf_count;  // individuals to redo wide
     int32_t *err_flag;
+    int32_t *sm_ticket;  // per-SM counters: master-warp assignment
     uint8_t *ws_gamma;  // per-CTA gamma slice (when gamma is not in smem)
     uint8_t *ws_stamp;  // per-CTA dense overflow expiry table
     size_t ws_g_stride, ws_s_stride;
@@ -138,6 +139,7 @@ template <typename G, typename S, int KQ>
 struct RowEval {
     static constexpr bool NARROW = sizeof(G) == 1;
     const G *g;
+    const uint32_t *lut;  // nibble -> byte mask (shared)
     int a, gva, k, kp;
     uint64_t ex[KQ];
 
@@ -166,12 +168,13 @@ struct RowEval {
     // word w of the row with excluded colours forced to 0xFF (narrow path)
     __device__ __forceinline__ uint32_t word(int w) const {
         return reinterpret_cast<const uint32_t *>(g)[w] |
-               expand_nibble((uint32_t)(exq(w >> 4) >> (4 * (w & 15))) & 0xFu);
+               lut[(uint32_t)(exq(w >> 4) >> (4 * (w & 15))) & 0xFu];
     }
 
     __device__ __forceinline__ void init(const G *gamma, const S *texp, const uint8_t *tcol,
                                          const S *tovf, const S *gstamp, const uint8_t *assign, int v,
-                                         int kp_, int k_, uint32_t it, int thr) {
+                                         int kp_, int k_, uint32_t it, int thr, const uint32_t *lut_) {
+        lut = lut_;
         kp = kp_;
         k = k_;
         a = assign[v];
@@ -212,7 +215,32 @@ struct RowEval {
 
     // (row minimum delta or TC_BIG, #admissible candidates at the minimum)
     __device__ __forceinline__ void min_count(int &rmin, int &cnt) const {
-        if constexpr (NARROW) {
+        if constexpr (NARROW && KQ == 1) {
+            // k <= 64: the row's (<= 16) masked words stay in registers; pass A
+            // takes byte minima as 16x2 lanes (even bytes, odd bytes via PRMT),
+            // pass B counts bytes equal to the minimum
+            const int W = kp >> 2;
+            const uint32_t *g32 = reinterpret_cast<const uint32_t *>(g);
+            uint32_t xw[16];
+            uint32_t acc = 0xFFFFFFFFu;
+#pragma unroll
+            for (int w = 0; w < 16; w++) {
+                if (w < W) {
+                    const uint32_t x = g32[w] | lut[(uint32_t)(ex[0] >> (4 * w)) & 0xFu];
+                    xw[w] = x;
+                    acc = __vminu2(acc, __vminu2(x & 0x00FF00FFu, __byte_perm(x, 0, 0x4341)));
+                }
+            }
+            const int m = (int)min(acc & 0xFFFFu, acc >> 16);
+            int c = 0;
+            if (m != 0xFF) {
+#pragma unroll
+                for (int w = 0; w < 16; w++)
+                    if (w < W) c += count_eq_bytes(xw[w], (uint32_t)m);
+            }
+            rmin = (m == 0xFF) ? TC_BIG : m - gva;
+            cnt = (m == 0xFF) ? 0 : c;
+        } else if constexpr (NARROW) {
             const int W = kp >> 2;
             int m = 0xFF, c = 0;
 #pragma unroll 4
@@ -242,20 +270,33 @@ struct RowEval {
         }
     }
 
-    // exact sequential tie count of the row when entered with running minimum R
-    __device__ __forceinline__ int walk_ties(int R) const {
+    // Exact sequential tie count of the row entered with running minimum R,
+    // warp-cooperative (all 32 lanes, same row): lane = word (narrow) or
+    // colour (wide); an exclusive prefix-min over the units gives each lane the
+    // running minimum entering its unit, then each lane walks its <= 4 bytes.
+    __device__ __forceinline__ int warp_walk_ties(int R, int lane) const {
+        constexpr unsigned FULL = 0xffffffffu;
+        constexpr int NONE = NARROW ? 0xFF : INT_MAX - 1;
+        const int units = NARROW ? (kp >> 2) : k;
+        int carry = (R >= TC_BIG) ? INT_MAX : R + gva;  // g-space
         int t = 0;
-        if constexpr (NARROW) {
-            int cur = (R >= TC_BIG) ? 0x100 : R + gva;  // g-space; 0x100 = +inf
-            const int W = kp >> 2;
-            for (int w = 0; w < W; w++) {
-                const uint32_t x = word(w);
-                const int wm = (int)min_bytes(x);
-                if (wm == 0xFF || wm > cur) continue;
-                if (wm == cur) {
-                    t += count_eq_bytes(x, (uint32_t)cur);
-                    continue;
+        for (int u0 = 0; u0 < units; u0 += 32) {
+            const int u = u0 + lane;
+            uint32_t x = 0xFFFFFFFFu;
+            int um = NONE;
+            if (u < units) {
+                if constexpr (NARROW) {
+                    x = word(u);
+                    um = (int)min_bytes(x);
+                } else {
+                    um = excluded(u) ? NONE : (int)g[u];
                 }
+            }
+            const int incl = warp_incl_min(um, lane);
+            int excl = __shfl_up_sync(FULL, incl, 1);
+            if (lane == 0) excl = INT_MAX;
+            int cur = min(carry, excl);
+            if constexpr (NARROW) {
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
                     const int b = (x >> (8 * e)) & 0xFF;
@@ -263,22 +304,17 @@ struct RowEval {
                     if (b < cur) cur = b;
                     else if (b == cur) t++;
                 }
+            } else {
+                if (um != NONE && um == cur) t++;
             }
-        } else {
-            int cur = R;
-            for (int c = 0; c < k; c++) {
-                if (excluded(c)) continue;
-                const int d = (int)g[c] - gva;
-                if (d < cur) cur = d;
-                else if (d == cur) t++;
-            }
+            carry = min(carry, __shfl_sync(FULL, incl, 31));
         }
-        return t;
+        return __reduce_add_sync(FULL, t);
     }
 };
 
 template <typename G, typename S, bool GSM, int KQ, int NT>
-__global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
+__global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_kernel(TabuParams P) {
     constexpr int NW = NT / 32;
     constexpr bool NARROW = sizeof(G) == 1;
     constexpr int GMAX = NARROW ? 254 : 65534;
@@ -288,6 +324,8 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
 
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ TabuCtrl<NW> ctl;
+    __shared__ uint32_t s_nib[16];
+    if (threadIdx.x < 16) s_nib[threadIdx.x] = expand_nibble(threadIdx.x);
 
     const int n = P.n, k = P.k, kp = P.kp;
     size_t off = 0;
@@ -315,7 +353,20 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
     int2 *lowl = reinterpret_cast<int2 *>(smem + off);  // queued rows lowering the running min
     S *gstamp = reinterpret_cast<S *>(P.ws_stamp + blockIdx.x * P.ws_s_stride);
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, hw_warp = tid >> 5;
+    // The serial part of every iteration runs on one "master" warp.  Warp slot
+    // w of an SM issues from sub-partition w % 4, so CTAs resident on the same
+    // SM take their master round-robin from a per-SM ticket: the serial chains
+    // spread over the 4 schedulers instead of all landing on one.
+    if (tid == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        ctl.work = P.sm_ticket ? atomicAdd(P.sm_ticket + (smid & 255), 1) : 0;
+    }
+    __syncthreads();
+    const int master = ctl.work % NW;
+    const int warp = ((tid >> 5) - master + NW) % NW;  // warp 0 = this CTA's master
+    __syncthreads();
     const bool diagf = (P.flags & MCB_FLAG_DIAG) != 0;
     const bool prod = (P.flags & MCB_FLAG_PRODUCTION) != 0;
     const bool profile = (P.flags & MCB_FLAG_PROFILE) != 0;
@@ -388,13 +439,13 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                     c2 += gv;
                 }
                 const unsigned bal = __ballot_sync(FULL, f);
-                if (lane == 0) ctl.wcnt[warp] = __popc(bal);
+                if (lane == 0) ctl.wcnt[hw_warp] = __popc(bal);
                 __syncthreads();
                 int woff = 0, tot = 0;
 #pragma unroll
                 for (int j = 0; j < NW; j++) {
                     const int cj = ctl.wcnt[j];
-                    woff += (j < warp) ? cj : 0;
+                    woff += (j < hw_warp) ? cj : 0;
                     tot += cj;
                 }
                 if (v < n) {
@@ -410,7 +461,7 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                 __syncthreads();
             }
             c2 = warp_sum64(c2);
-            if (lane == 0) ctl.red[warp] = c2;
+            if (lane == 0) ctl.red[hw_warp] = c2;
             __syncthreads();
             if (tid == 0) {
                 long long s = 0;
@@ -443,7 +494,7 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                 // pass 1: (min, count) of every conflicting row, one row per thread
                 for (int li = tid; li < C; li += NT) {
                     RE re;
-                    re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[li], kp, k, it32, thr);
+                    re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[li], kp, k, it32, thr, s_nib);
                     int rm, cnt;
                     re.min_count(rm, cnt);
                     rmc[li] = make_int2(rm, cnt);
@@ -457,13 +508,14 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                 if (warp == 0) {
                     constexpr int R = 4;
                     int nlow = 0;
-                    auto flush = [&]() {
+                    auto flush = [&]() {  // warp-cooperative walks of the queued rows
                         __syncwarp();
-                        for (int j = lane; j < nlow; j += 32) {
+                        for (int j = 0; j < nlow; j++) {
                             const int2 e = lowl[j];
                             RE re;
-                            re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[e.x], kp, k, it32, thr);
-                            tsum += re.walk_ties(e.y);
+                            re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[e.x], kp, k, it32, thr, s_nib);
+                            const int t = re.warp_walk_ties(e.y, lane);
+                            if (lane == 0) tsum += t;
                         }
                         __syncwarp();
                         nlow = 0;
@@ -579,7 +631,7 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                         // locate the need-th D-candidate of the row (lanes over words)
                         const int v = clist[row_li];
                         RE re;
-                        re.init(gamma, texp, tcol, tovf, gstamp, assign, v, kp, k, it32, thr);
+                        re.init(gamma, texp, tcol, tovf, gstamp, assign, v, kp, k, it32, thr, s_nib);
                         int b = -1;
                         {
                             const int Dg = D + re.gva;
@@ -781,7 +833,7 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
                     for (int64_t e = tid; e < P.m; e += NT)
                         c2 += assign[__ldg(P.eu + e)] == assign[__ldg(P.ev + e)];
                     c2 = warp_sum64(c2);
-                    if (lane == 0) ctl.red[warp] = c2;
+                    if (lane == 0) ctl.red[hw_warp] = c2;
                 }
                 if (swp) {  // keep 16-bit expiries unambiguous
                     const uint32_t itw = (uint32_t)itn;
@@ -809,7 +861,7 @@ __global__ void __launch_bounds__(NT) tabucol_kernel(TabuParams P) {
         __syncthreads();
 
         // ---------------- outputs (:407-410) ----------------
-        if (profile && tid == 0) {
+        if (profile && warp == 0 && lane == 0) {
             for (int q = 1; q < 10; q++) atomicAdd(&g_phase_cycles[q], (unsigned long long)ctl.ph[q]);
             atomicAdd(&g_phase_cycles[10], (unsigned long long)ctl.it);
         }
@@ -938,7 +990,7 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
 
     const size_t tab = (size_t)n * kp;
     const int grid_cap = 16 * num_sms();
-    const size_t ctl_bytes = 256 + sizeof(int32_t) * (size_t)A.p;
+    const size_t ctl_bytes = 256 + 1024 + sizeof(int32_t) * (size_t)A.p;
     const size_t ng_stride = (tab + 255) & ~(size_t)255, ns_stride = (tab * 2 + 255) & ~(size_t)255;
     const size_t wg_stride = (tab * 2 + 255) & ~(size_t)255, ws_stride = (tab * 4 + 255) & ~(size_t)255;
     const int wide_grid = std::min<int>((int)A.p, 2 * num_sms());
@@ -959,8 +1011,9 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     uint8_t *ws = (uint8_t *)workspace(indptr_off + indptr_bytes + 256);
     if (!ws) return set_error(MCB_ERR_CUDA, "tabucol: workspace allocation failed");
     int32_t *ctl32 = reinterpret_cast<int32_t *>(ws);  // [0]=work(narrow) [1]=work(wide) [2]=ovf_count [3]=err
-    if (cudaMemsetAsync(ws, 0, 256, st) != cudaSuccess) return set_error(MCB_ERR_CUDA, "memset failed");
+    if (cudaMemsetAsync(ws, 0, 256 + 1024, st) != cudaSuccess) return set_error(MCB_ERR_CUDA, "memset failed");
     P.err_flag = ctl32 + 3;
+    P.sm_ticket = ctl32 + 64;  // 256 per-SM counters
     uint8_t *tables = ws + tables_off;
 
     // CSR row offsets -> __constant__ (u32) when they fit
@@ -977,7 +1030,7 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     if (variant != 2) {
         P.work_counter = ctl32 + 0;
         P.ovf_count = ctl32 + 2;
-        P.ovf_list = ctl32 + 64;
+        P.ovf_list = ctl32 + 64 + 256;
         P.ws_stamp = tables;
         P.ws_s_stride = ns_stride;
         if (variant == 1) {
@@ -995,7 +1048,7 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     Q.ovf_list = nullptr;
     Q.ovf_count = nullptr;
     if (variant != 2) {
-        Q.work = ctl32 + 64;
+        Q.work = ctl32 + 64 + 256;
         Q.nwork_dev = ctl32 + 2;
     }
     Q.ws_gamma = tables + narrow_ws;
