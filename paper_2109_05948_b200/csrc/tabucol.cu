@@ -97,6 +97,28 @@ struct TabuParams {
     int const_indptr;
 };
 
+// (int, int) pair records: packed int16 x 2 for the narrow variant (deltas in
+// [-254, 254] or TC_BIG), int2 for the wide one
+template <bool NARROW>
+struct RecT;
+template <>
+struct RecT<true> {
+    using T = uint32_t;
+};
+template <>
+struct RecT<false> {
+    using T = int2;
+};
+__device__ __forceinline__ uint32_t rec_pack(int x, int y, uint32_t *) {
+    return (uint32_t)(uint16_t)(int16_t)(x >= TC_BIG ? 0x7FFF : x) | ((uint32_t)y << 16);
+}
+__device__ __forceinline__ int2 rec_pack(int x, int y, int2 *) { return make_int2(x, y); }
+__device__ __forceinline__ int2 rec_unpack(uint32_t r) {
+    const int x = (int)(int16_t)(r & 0xFFFFu);
+    return make_int2(x == 0x7FFF ? TC_BIG : x, (int)(r >> 16));
+}
+__device__ __forceinline__ int2 rec_unpack(int2 r) { return r; }
+
 template <int NW>
 struct TabuCtrl {
     long long it, conflicts, best, nlog, sum_c, sum_deg, diag;
@@ -348,9 +370,10 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
     off += (2 * n + 15) & ~15;
     uint16_t *cpos = reinterpret_cast<uint16_t *>(smem + off);
     off += (2 * n + 15) & ~15;
-    int2 *rmc = reinterpret_cast<int2 *>(smem + off);  // per row: (min delta, count)
-    off += ((size_t)8 * n + 15) & ~(size_t)15;
-    int2 *lowl = reinterpret_cast<int2 *>(smem + off);  // queued rows lowering the running min
+    using Rec = typename RecT<NARROW>::T;
+    Rec *rmc = reinterpret_cast<Rec *>(smem + off);  // per row: (min delta, count)
+    off += (sizeof(Rec) * n + 15) & ~(size_t)15;
+    Rec *lowl = reinterpret_cast<Rec *>(smem + off);  // queued (row, running min) pairs
     S *gstamp = reinterpret_cast<S *>(P.ws_stamp + blockIdx.x * P.ws_s_stride);
 
     const int tid = threadIdx.x, lane = tid & 31, hw_warp = tid >> 5;
@@ -497,7 +520,7 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                     re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[li], kp, k, it32, thr, s_nib);
                     int rm, cnt;
                     re.min_count(rm, cnt);
-                    rmc[li] = make_int2(rm, cnt);
+                    rmc[li] = rec_pack(rm, cnt, (Rec *)nullptr);
                 }
                 __syncthreads();
                 PH(1);
@@ -511,10 +534,10 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                     auto flush = [&]() {  // warp-cooperative walks of the queued rows
                         __syncwarp();
                         for (int j = 0; j < nlow; j++) {
-                            const int2 e = lowl[j];
+                            const int2 e = rec_unpack(lowl[j]);  // (running min, row)
                             RE re;
-                            re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[e.x], kp, k, it32, thr, s_nib);
-                            const int t = re.warp_walk_ties(e.y, lane);
+                            re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[e.y], kp, k, it32, thr, s_nib);
+                            const int t = re.warp_walk_ties(e.x, lane);
                             if (lane == 0) tsum += t;
                         }
                         __syncwarp();
@@ -527,7 +550,7 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
 #pragma unroll
                         for (int r = 0; r < R; r++) {
                             const int q = r0 + lane * R + r;
-                            mc[r] = q < C ? rmc[q] : make_int2(TC_BIG, 0);
+                            mc[r] = q < C ? rec_unpack(rmc[q]) : make_int2(TC_BIG, 0);
                             lmn = min(lmn, mc[r].x);
                         }
                         const int incl = warp_incl_min(lmn, lane);
@@ -560,7 +583,7 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                             int pos = nlow + ci - cl;
 #pragma unroll
                             for (int r = 0; r < R; r++)
-                                if ((lowbits >> r) & 1u) lowl[pos++] = make_int2(r0 + lane * R + r, lowR[r]);
+                                if ((lowbits >> r) & 1u) lowl[pos++] = rec_pack(lowR[r], r0 + lane * R + r, (Rec *)nullptr);
                             nlow += __shfl_sync(FULL, ci, 31);
                         }
                         carry = min(carry, __shfl_sync(FULL, incl, 31));
@@ -613,7 +636,7 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                                 const int li = base + lane;
                                 int c = 0;
                                 if (li < C) {
-                                    const int2 mc = rmc[li];
+                                    const int2 mc = rec_unpack(rmc[li]);
                                     c = (mc.x == D) ? mc.y : 0;
                                 }
                                 const int incl = warp_incl_sum(c, lane);
@@ -901,8 +924,9 @@ __global__ void indptr_to_u32(const int64_t *in, uint32_t *out, int count) {
 template <typename S>
 static size_t misc_bytes(int n, int nt) {
     auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    const size_t rec = sizeof(S) == 2 ? 4 : 8;
     return a16((size_t)n * 4 * sizeof(S)) + a16((size_t)n * 4) + a16((size_t)n * sizeof(S)) +
-           a16(n) + 2 * a16(2 * (size_t)n) + a16(8 * (size_t)n) + (size_t)8 * TC_LOWCAP;
+           a16(n) + 2 * a16(2 * (size_t)n) + a16(rec * (size_t)n) + rec * TC_LOWCAP;
 }
 
 template <typename G, typename S, bool GSM>
@@ -928,6 +952,10 @@ static int launch_variant(TabuParams P, int max_grid, int p_hint, cudaStream_t s
     grid = std::max(grid, 1);
     *grid_out = grid;
     if (query_only) return MCB_OK;
+    if (getenv("MCB_VERBOSE"))
+        fprintf(stderr, "[mcb] tabucol<%s,%s,gsm=%d,kq=%d> grid=%d (%d/SM) smem=%zu\n",
+                sizeof(G) == 1 ? "u8" : "u16", sizeof(S) == 2 ? "u16" : "u32", (int)GSM,
+                (GSM && P.kp <= 64) ? 1 : 4, grid, nb, smem);
     kern<<<grid, TC_NT, smem, st>>>(P);
     if (cudaGetLastError() != cudaSuccess) return set_error(MCB_ERR_CUDA, "tabucol launch failed");
     return MCB_OK;
