@@ -42,7 +42,7 @@ __device__ __forceinline__ uint4 philox4x32_10(uint2 key, uint4 ctr) {
     return ctr;
 }
 // uniform draw in [0, n) from the 64-bit key and a 64-bit draw counter
-__device__ __forceinline__ uint32_t philox_below(uint64_t key, uint64_t ctr, uint32_t n) {
+static __device__ __noinline__ uint32_t philox_below(uint64_t key, uint64_t ctr, uint32_t n) {
     uint4 r = philox4x32_10(make_uint2((uint32_t)key, (uint32_t)(key >> 32)),
                             make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), 0x5eed, 0));
     uint64_t x = ((uint64_t)r.x << 32) | r.y;

@@ -95,6 +95,7 @@ struct TabuParams {
     size_t ws_g_stride, ws_s_stride;
     uint32_t flags;
     int const_indptr;
+    int swz_rs, swz_rm;  // gamma row word rotation: rot(v) = (v >> rs) & rm
 };
 
 // (int, int) pair records: packed int16 x 2 for the narrow variant (deltas in
@@ -137,6 +138,19 @@ __device__ __forceinline__ bool active(S e, uint32_t it) {
         return (int32_t)((uint32_t)e - it) > 0;
 }
 
+// a 5th live tabu entry of a vertex: spill to its dense global row (rare)
+template <typename S>
+__device__ __noinline__ void spill_set(S *gs, S *tovf_v, bool ovf_live, int k, int a, S e_new,
+                                       uint32_t it) {
+    if (!ovf_live) {  // fresh spill row
+        for (int cc = 0; cc < k; cc++) gs[cc] = (S)it;
+        *tovf_v = e_new;
+    } else if (active<S>(e_new, (uint32_t)*tovf_v)) {
+        *tovf_v = e_new;
+    }
+    gs[a] = e_new;
+}
+
 // number of bytes of x equal to byte value c
 __device__ __forceinline__ int count_eq_bytes(uint32_t x, uint32_t c) {
     const uint32_t z = x ^ (c * 0x01010101u);
@@ -162,8 +176,22 @@ struct RowEval {
     static constexpr bool NARROW = sizeof(G) == 1;
     const G *g;
     const uint32_t *lut;  // nibble -> byte mask (shared)
-    int a, gva, k, kp;
+    int a, gva, k, kp, rot;
     uint64_t ex[KQ];
+
+    // physical word of logical word w (rows are rotated by `rot` words so that
+    // rows sharing a bank offset land on different banks)
+    __device__ __forceinline__ int wp(int w) const {
+        const int p = w + rot, W = kp >> 2;
+        return p >= W ? p - W : p;
+    }
+    // gamma value of colour c
+    __device__ __forceinline__ int gv(int c) const {
+        if constexpr (NARROW)
+            return reinterpret_cast<const uint8_t *>(g)[4 * wp(c >> 2) + (c & 3)];
+        else
+            return g[c];
+    }
 
     __device__ __forceinline__ void setbit(int c) {
         const uint64_t b = 1ull << (c & 63);
@@ -189,19 +217,21 @@ struct RowEval {
     __device__ __forceinline__ bool excluded(int c) const { return (exq(c >> 6) >> (c & 63)) & 1ull; }
     // word w of the row with excluded colours forced to 0xFF (narrow path)
     __device__ __forceinline__ uint32_t word(int w) const {
-        return reinterpret_cast<const uint32_t *>(g)[w] |
+        return reinterpret_cast<const uint32_t *>(g)[wp(w)] |
                lut[(uint32_t)(exq(w >> 4) >> (4 * (w & 15))) & 0xFu];
     }
 
     __device__ __forceinline__ void init(const G *gamma, const S *texp, const uint8_t *tcol,
                                          const S *tovf, const S *gstamp, const uint8_t *assign, int v,
-                                         int kp_, int k_, uint32_t it, int thr, const uint32_t *lut_) {
+                                         int kp_, int k_, uint32_t it, int thr, const uint32_t *lut_,
+                                         int swz_rs, int swz_rm) {
         lut = lut_;
         kp = kp_;
         k = k_;
+        rot = (v >> swz_rs) & swz_rm;
         a = assign[v];
         g = gamma + (size_t)v * kp;
-        gva = g[a];
+        gva = gv(a);
         const int A = thr + gva;
 #pragma unroll
         for (int q = 0; q < KQ; q++) ex[q] = 0;
@@ -225,40 +255,36 @@ struct RowEval {
 #pragma unroll
             for (int s = 0; s < 4; s++) {
                 const int c = (cols >> (8 * s)) & 0xFF;
-                if (c != 0xFF && active<S>(e[s], it) && !((int)g[c] < A)) setbit(c);
+                if (c != 0xFF && active<S>(e[s], it) && !(gv(c) < A)) setbit(c);
             }
         }
-        if (active<S>(tovf[v], it)) {  // spilled expiries: dense global row (rare)
-            const S *gs = gstamp + (size_t)v * kp;
-            for (int c = 0; c < k; c++)
-                if (active<S>(gs[c], it) && !((int)g[c] < A)) setbit(c);
-        }
+        if (active<S>(tovf[v], it)) spill_scan(gstamp + (size_t)v * kp, it, A);
+    }
+    // spilled expiries: dense global row (rare; kept out of the hot code)
+    __device__ __noinline__ void spill_scan(const S *gs, uint32_t it, int A) {
+        for (int c = 0; c < k; c++)
+            if (active<S>(gs[c], it) && !(gv(c) < A)) setbit(c);
     }
 
     // (row minimum delta or TC_BIG, #admissible candidates at the minimum)
     __device__ __forceinline__ void min_count(int &rmin, int &cnt) const {
         if constexpr (NARROW && KQ == 1) {
-            // k <= 64: the row's (<= 16) masked words stay in registers; pass A
-            // takes byte minima as 16x2 lanes (even bytes, odd bytes via PRMT),
-            // pass B counts bytes equal to the minimum
+            // k <= 64: one pass, byte minima as 16x2 lanes (even bytes, odd bytes
+            // via PRMT) and the count of bytes at the running minimum
             const int W = kp >> 2;
             const uint32_t *g32 = reinterpret_cast<const uint32_t *>(g);
-            uint32_t xw[16];
-            uint32_t acc = 0xFFFFFFFFu;
-#pragma unroll
-            for (int w = 0; w < 16; w++) {
-                if (w < W) {
-                    const uint32_t x = g32[w] | lut[(uint32_t)(ex[0] >> (4 * w)) & 0xFu];
-                    xw[w] = x;
-                    acc = __vminu2(acc, __vminu2(x & 0x00FF00FFu, __byte_perm(x, 0, 0x4341)));
-                }
-            }
-            const int m = (int)min(acc & 0xFFFFu, acc >> 16);
-            int c = 0;
-            if (m != 0xFF) {
-#pragma unroll
-                for (int w = 0; w < 16; w++)
-                    if (w < W) c += count_eq_bytes(xw[w], (uint32_t)m);
+            uint64_t exm = ex[0];
+            int m = 0xFF, c = 0, p = rot;
+#pragma unroll 2
+            for (int w = 0; w < W; w++) {
+                const uint32_t x = g32[p] | lut[(uint32_t)exm & 0xFu];
+                exm >>= 4;
+                p = (p + 1 == W) ? 0 : p + 1;
+                const uint32_t m2 = __vminu2(x & 0x00FF00FFu, __byte_perm(x, 0, 0x4341));
+                const int wm = (int)min(m2 & 0xFFFFu, m2 >> 16);
+                const int wc = count_eq_bytes(x, (uint32_t)wm);
+                c = (wm < m) ? wc : (wm == m ? c + wc : c);
+                m = min(m, wm);
             }
             rmin = (m == 0xFF) ? TC_BIG : m - gva;
             cnt = (m == 0xFF) ? 0 : c;
@@ -279,7 +305,7 @@ struct RowEval {
             int m = INT_MAX, c = 0;
             for (int cc = 0; cc < k; cc++) {
                 if (excluded(cc)) continue;
-                const int b = g[cc];
+                const int b = gv(cc);
                 if (b < m) {
                     m = b;
                     c = 1;
@@ -311,7 +337,7 @@ struct RowEval {
                     x = word(u);
                     um = (int)min_bytes(x);
                 } else {
-                    um = excluded(u) ? NONE : (int)g[u];
+                    um = excluded(u) ? NONE : gv(u);
                 }
             }
             const int incl = warp_incl_min(um, lane);
@@ -394,6 +420,17 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
     const bool prod = (P.flags & MCB_FLAG_PRODUCTION) != 0;
     const bool profile = (P.flags & MCB_FLAG_PROFILE) != 0;
     const bool cidx = P.const_indptr != 0;
+    const int Wq = kp >> 2;
+    // element offset of (vertex, colour) in gamma, rows rotated by rot(v) words
+    auto goff = [&](int v, int c) -> size_t {
+        if constexpr (NARROW) {
+            int p = (c >> 2) + ((v >> P.swz_rs) & P.swz_rm);
+            if (p >= Wq) p -= Wq;
+            return (size_t)v * kp + 4 * p + (c & 3);
+        } else {
+            return (size_t)v * kp + c;
+        }
+    };
     auto row_begin = [&](int v) -> int64_t { return cidx ? (int64_t)c_indptr[v] : P.indptr[v]; };
 
     for (;;) {
@@ -424,8 +461,12 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
             const int wpr = kp * (int)sizeof(G) / 4;  // words per row
             const uint32_t padw = NARROW ? ((k & 3) ? (0xFFFFFFFFu << (8 * (k & 3))) : 0u)
                                          : ((k & 1) ? 0xFFFF0000u : 0u);
-            for (size_t i = tid; i < (size_t)n * wpr; i += NT)
-                g32[i] = ((int)(i % wpr) == wpr - 1) ? padw : 0u;
+            for (int i = tid; i < n * wpr; i += NT) {
+                const int v = i / wpr, w = i - v * wpr;  // physical word w of row v
+                int lw = w - (NARROW ? ((v >> P.swz_rs) & P.swz_rm) : 0);
+                if (lw < 0) lw += wpr;
+                g32[i] = (lw == wpr - 1) ? padw : 0u;
+            }
         }
         if (tid == 0) {
             ctl.ovf = 0;
@@ -437,13 +478,13 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
         {
             int bad = 0;
             for (int u = tid; u < n; u += NT) {
-                G *row = gamma + (size_t)u * kp;
                 const int64_t s0 = row_begin(u), s1 = row_begin(u + 1);
                 for (int64_t idx = s0; idx < s1; idx++) {
                     const int c = assign[__ldg(P.indices + idx)];
-                    const int x = (int)row[c] + 1;
+                    G *e = gamma + goff(u, c);
+                    const int x = (int)*e + 1;
                     if (x > GMAX) bad = 1;
-                    else row[c] = (G)x;
+                    else *e = (G)x;
                 }
             }
             if (bad) ctl.ovf = 1;
@@ -457,7 +498,7 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                 const int v = ch + tid;
                 bool f = false;
                 if (v < n) {
-                    const int gv = gamma[(size_t)v * kp + assign[v]];
+                    const int gv = gamma[goff(v, assign[v])];
                     f = gv > 0;
                     c2 += gv;
                 }
@@ -517,7 +558,7 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                 // pass 1: (min, count) of every conflicting row, one row per thread
                 for (int li = tid; li < C; li += NT) {
                     RE re;
-                    re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[li], kp, k, it32, thr, s_nib);
+                    re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[li], kp, k, it32, thr, s_nib, P.swz_rs, P.swz_rm);
                     int rm, cnt;
                     re.min_count(rm, cnt);
                     rmc[li] = rec_pack(rm, cnt, (Rec *)nullptr);
@@ -536,7 +577,7 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                         for (int j = 0; j < nlow; j++) {
                             const int2 e = rec_unpack(lowl[j]);  // (running min, row)
                             RE re;
-                            re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[e.y], kp, k, it32, thr, s_nib);
+                            re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[e.y], kp, k, it32, thr, s_nib, P.swz_rs, P.swz_rm);
                             const int t = re.warp_walk_ties(e.x, lane);
                             if (lane == 0) tsum += t;
                         }
@@ -603,16 +644,6 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                     if (D != TC_BIG) {
                         const int T = __reduce_add_sync(FULL, lmin == D ? lT : 0);
                         const int L = (int)__reduce_min_sync(FULL, (unsigned)(lmin == D ? lfirst : INT_MAX));
-                        // speculative prefetch: adjacency of the first D-row's vertex
-                        v_guess = clist[L];
-                        {
-                            const int64_t g0 = row_begin(v_guess), g1 = row_begin(v_guess + 1);
-#pragma unroll
-                            for (int j = 0; j < NB; j++) {
-                                const int64_t idx = g0 + j * 32 + lane;
-                                uu[j] = idx < g1 ? __ldg(P.indices + idx) : 0;
-                            }
-                        }
                         const int total = __reduce_add_sync(FULL, tsum);
                         const unsigned long long ctr = ctl.ctr;
                         int sstar = 1;
@@ -651,10 +682,21 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                                 cum += tot;
                             }
                         }
-                        // locate the need-th D-candidate of the row (lanes over words)
+                        // the winner's vertex is known: start its adjacency loads now so
+                        // they overlap the in-row locate and the tenure/slot bookkeeping
                         const int v = clist[row_li];
+                        v_guess = v;
+                        {
+                            const int64_t g0 = row_begin(v), g1 = row_begin(v + 1);
+#pragma unroll
+                            for (int j = 0; j < NB; j++) {
+                                const int64_t idx = g0 + j * 32 + lane;
+                                uu[j] = idx < g1 ? __ldg(P.indices + idx) : 0;
+                            }
+                        }
+                        // locate the need-th D-candidate of the row (lanes over words)
                         RE re;
-                        re.init(gamma, texp, tcol, tovf, gstamp, assign, v, kp, k, it32, thr, s_nib);
+                        re.init(gamma, texp, tcol, tovf, gstamp, assign, v, kp, k, it32, thr, s_nib, P.swz_rs, P.swz_rm);
                         int b = -1;
                         {
                             const int Dg = D + re.gva;
@@ -667,11 +709,11 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                                 if (u < units) {
                                     if constexpr (NARROW) {
                                         const uint64_t m64 = re.exq(u >> 4);
-                                        x = reinterpret_cast<const uint32_t *>(re.g)[u] |
+                                        x = reinterpret_cast<const uint32_t *>(re.g)[re.wp(u)] |
                                             expand_nibble((uint32_t)(m64 >> (4 * (u & 15))) & 0xFu);
                                         c = count_eq_bytes(x, (uint32_t)Dg);
                                     } else {
-                                        c = (!re.excluded(u) && (int)re.g[u] == Dg) ? 1 : 0;
+                                        c = (!re.excluded(u) && re.gv(u) == Dg) ? 1 : 0;
                                     }
                                 }
                                 const int incl = warp_incl_sum(c, lane);
@@ -730,16 +772,9 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                                 texp[4 * v + s] = e_new;
                                 if (ovf_live) gstamp[(size_t)v * kp + a] = (S)it32;  // supersede
                             } else {
-                                S *gs = gstamp + (size_t)v * kp;
-                                if (!ovf_live) {  // fresh spill row
-                                    for (int cc = 0; cc < k; cc++) gs[cc] = (S)it32;
-                                    tovf[v] = e_new;
-                                } else if (active<S>(e_new, (uint32_t)tovf[v])) {
-                                    tovf[v] = e_new;
-                                }
-                                gs[a] = e_new;
+                                spill_set(gstamp + (size_t)v * kp, tovf + v, ovf_live, k, a, e_new, it32);
                             }
-                            gvb = re.g[b < 0 ? 0 : b];
+                            gvb = re.gv(b < 0 ? 0 : b);
                             assign[v] = (uint8_t)(b < 0 ? a : b);
                             ctl.conflicts = nconf;
                             ctl.ctr = c;
@@ -802,12 +837,13 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                                 bool evt = false;
                                 if (idx < s1) {
                                     const int u = uu[j];
-                                    G *row = gamma + (size_t)u * kp;
-                                    const int ga = (int)row[mv_a] - 1;
-                                    row[mv_a] = (G)ga;
-                                    const int gb = row[mv_b];
+                                    G *pa = gamma + goff(u, mv_a);
+                                    G *pb = gamma + goff(u, mv_b);
+                                    const int ga = (int)*pa - 1;
+                                    *pa = (G)ga;
+                                    const int gb = *pb;
                                     if (gb >= GMAX) bad = true;
-                                    else row[mv_b] = (G)(gb + 1);
+                                    else *pb = (G)(gb + 1);
                                     const int au = assign[u];
                                     evt = (au == mv_a && ga == 0) || (au == mv_b && gb == 0);
                                 }
@@ -1007,6 +1043,18 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     P.counters = A.counters;
     P.flags = A.flags;
     P.nwork = (int)A.p;
+    {
+        // rows of W words: bank base (v*W) mod 32 repeats every Pd = 32/g rows
+        // with g = gcd(W, 32); rotating row v by (v / Pd) mod g words fills the gaps
+        const int W = kp / 4;
+        int g = 1;
+        while (g < 32 && W % (2 * g) == 0) g *= 2;
+        int pd = 32 / g, rs = 0;
+        while ((1 << rs) < pd) rs++;
+        P.swz_rs = rs;
+        P.swz_rm = g - 1;
+        if (!getenv("MCB_SWIZZLE")) P.swz_rm = 0;  // measured: no gain at k=48 (latency-bound)
+    }
 
     const bool force_wide = (A.flags & MCB_FLAG_FORCE_WIDE) != 0;
     const bool force_glob = (A.flags & MCB_FLAG_FORCE_GLOBAL) != 0;
