@@ -1,12 +1,633 @@
-// wvcp.cu -- batched weighted-colouring tabu search (placeholder until the
-// kernel lands).
+// wvcp.cu -- batched weighted-colouring tabu search for sm_100a, one
+// individual per CTA.
+//
+// Replaces the numba kernel `_wvcp_batch` (reference
+// pkg/src/memcolor/localsearch.py:89-263, with _refresh_class :46-67 and
+// _wvcp_scratch :70-86).  Reproduced exactly:
+//   * objective g = fp64(d_score) + phi * fp64(d_conf), a separate fp64 multiply
+//     and add (__dmul_rn / __dadd_rn: the reference's numba code has no FMA,
+//     :193); candidates compared with fp64 < and == (:194-210);
+//   * full scan v = 0..n-1, c = 0..k-1 (c != a) with
+//       rem = uniq_drop[a] if rank(v) == max_rank[a] else 0,
+//       d_add = max(0, w_v - max_val[c]), d_score = d_add - rem (:172-186);
+//   * frozen vertex (it < tabu_until[v]) admissible only if the move is legal
+//     and strictly improves the best legal score (:187-192);
+//   * reservoir tie-break on the SplitMix64 stream (:202-210), tenure
+//     U{0..9} + tt_base on the same stream (:228-231), tabu_until reset at every
+//     round start (:160-161), phi halved/doubled after each round and forced on
+//     the last (:157-159, :251-258), scratch check every 1024 iterations (:245-249).
+//
+// Parallel evaluation of the sequential reservoir, as in tabucol.cu: pass 1
+// computes every row's (min g, #candidates at the min) -- one vertex per thread,
+// all n rows; warp 0 runs the exclusive prefix-min over the rows in vertex
+// order, counts tie events of rows equal to the running minimum and walks the
+// rows that lower it (warp-cooperative, lanes over colours), giving the
+// counter offset of the final minimum group; the draws are then independent.
+//
+// State per individual: gamma u16[n][k] and the per-vertex arrays in shared
+// memory; the per-class weight-rank counts wc[k][nranks] in a per-CTA global
+// slice (touched for two classes per move).
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch.h"
 
 namespace mcb {
-int wvcp_run(const WvcpArgs &a, cudaStream_t st) {
-    (void)a;
-    (void)st;
-    return set_error(MCB_ERR_UNSUPPORTED, "wvcp kernel not built yet");
+
+constexpr int WV_NT = 256;
+constexpr int WV_INF_SCORE_SHIFT = 62;
+
+struct WvParams {
+    int32_t *assigns;
+    int32_t *best_assigns;
+    const int64_t *indptr;
+    const int32_t *indices;
+    const int32_t *eu, *ev;
+    int64_t m;
+    const int32_t *wranks;
+    const int64_t *wvals;
+    int nranks;
+    const int64_t *weights;
+    int n, k;
+    int64_t depth, rounds;
+    int schedule_on;
+    const double *phi0s;
+    double forced_phi;
+    int64_t tt_base;
+    const uint64_t *keys;
+    int64_t *best_scores, *end_scores, *end_conflicts;
+    double *phi_used;
+    int64_t *diag;
+    int64_t log_cap;
+    int32_t *log_v;
+    int64_t *log_iter, *log_tt;
+    int8_t *log_asp;
+    int64_t *log_cnt;
+    uint32_t flags;
+    int nwork;
+    int32_t *work_counter;
+    int32_t *err_flag;
+    uint16_t *ws_wc;  // per-CTA [k][nranks]
+    size_t ws_wc_stride;
+};
+
+struct WvCtrl {
+    long long it, score, conflicts, best, nlog, diag;
+    unsigned long long ctr;
+    double phi;
+    int work, mv_v, mv_a, mv_b, has_move;
+    long long red[WV_NT / 32];
+    long long red2[WV_NT / 32];
+};
+
+__device__ __forceinline__ double gval_of(long long ds, long long dc, double phi) {
+    return __dadd_rn((double)ds, __dmul_rn(phi, (double)dc));  // no FMA (:193)
 }
+
+__device__ __forceinline__ double shfl_up_d(double x, int o) {
+    return __longlong_as_double(__shfl_up_sync(0xffffffffu, __double_as_longlong(x), o));
+}
+__device__ __forceinline__ double shfl_d(double x, int src) {
+    return __longlong_as_double(__shfl_sync(0xffffffffu, __double_as_longlong(x), src));
+}
+
+__global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
+    constexpr int NT = WV_NT, NW = NT / 32;
+    constexpr unsigned FULL = 0xffffffffu;
+    const double INF = __longlong_as_double(0x7ff0000000000000LL);
+    const long long INF_SCORE = 1LL << WV_INF_SCORE_SHIFT;
+
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ WvCtrl ctl;
+    const int n = P.n, k = P.k, nranks = P.nranks;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        uint8_t *p = smem + off;
+        off += (bytes + 15) & ~(size_t)15;
+        return p;
+    };
+    uint16_t *gamma = reinterpret_cast<uint16_t *>(take((size_t)n * k * 2));
+    uint32_t *tabu_until = reinterpret_cast<uint32_t *>(take((size_t)n * 4));
+    int32_t *wgt = reinterpret_cast<int32_t *>(take((size_t)n * 4));
+    uint16_t *wrk = reinterpret_cast<uint16_t *>(take((size_t)n * 2));
+    uint8_t *assign = take((size_t)n);
+    double *rmin = reinterpret_cast<double *>(take((size_t)n * 8));
+    uint16_t *rcnt = reinterpret_cast<uint16_t *>(take((size_t)n * 2));
+    int32_t *max_rank = reinterpret_cast<int32_t *>(take((size_t)k * 4));
+    int64_t *max_val = reinterpret_cast<int64_t *>(take((size_t)k * 8));
+    int64_t *uniq_drop = reinterpret_cast<int64_t *>(take((size_t)k * 8));
+    int32_t *cmax = reinterpret_cast<int32_t *>(take((size_t)k * 4));  // scratch
+    int32_t *lowq = reinterpret_cast<int32_t *>(take((size_t)2 * n * 4));  // (row, pos in R table)
+    double *lowR = reinterpret_cast<double *>(take((size_t)n * 8));
+    uint16_t *wc = P.ws_wc + blockIdx.x * P.ws_wc_stride;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool diagf = (P.flags & MCB_FLAG_DIAG) != 0;
+    const bool prod = (P.flags & MCB_FLAG_PRODUCTION) != 0;
+
+    for (int v = tid; v < n; v += NT) {
+        wgt[v] = (int32_t)P.weights[v];
+        wrk[v] = (uint16_t)P.wranks[v];
+    }
+
+    // refresh_class (:46-67) by one warp: highest rank with a member, and the
+    // drop of the class max if that member were the only one at its rank
+    auto refresh_class = [&](int c) {
+        const uint16_t *row = wc + (size_t)c * nranks;
+        int mr = -1;
+        for (int r0 = nranks - 1; r0 >= 0 && mr < 0; r0 -= 32) {
+            const int r = r0 - lane;
+            const bool has = r >= 0 && row[r] > 0;
+            const unsigned b = __ballot_sync(FULL, has);
+            if (b) mr = r0 - (__ffs(b) - 1);
+        }
+        long long mv = 0, ud = 0;
+        if (mr >= 0) {
+            mv = P.wvals[mr];
+            if (row[mr] > 1) {
+                ud = 0;
+            } else {
+                int sr = -1;
+                for (int r0 = mr - 1; r0 >= 0 && sr < 0; r0 -= 32) {
+                    const int r = r0 - lane;
+                    const bool has = r >= 0 && row[r] > 0;
+                    const unsigned b = __ballot_sync(FULL, has);
+                    if (b) sr = r0 - (__ffs(b) - 1);
+                }
+                ud = mv - (sr >= 0 ? P.wvals[sr] : 0);
+            }
+        }
+        if (lane == 0) {
+            max_rank[c] = mr;
+            max_val[c] = mv;
+            uniq_drop[c] = ud;
+        }
+    };
+
+    for (;;) {
+        if (tid == 0) ctl.work = atomicAdd(P.work_counter, 1);
+        __syncthreads();
+        const int ind = ctl.work;
+        if (ind >= P.nwork) break;
+        const uint64_t key = P.keys[ind];
+        int32_t *a_io = P.assigns + (size_t)ind * n;
+        int32_t *b_out = P.best_assigns + (size_t)ind * n;
+        double *phis = P.phi_used + (size_t)ind * (P.rounds + 1);
+
+        // ---------------- init (:120-154) ----------------
+        for (int v = tid; v < n; v += NT) {
+            int c = a_io[v];
+            if (c < 0 || c >= k) {
+                atomicExch(P.err_flag, 1);
+                c = 0;
+            }
+            assign[v] = (uint8_t)c;
+        }
+        for (size_t i = tid; i < (size_t)n * k / 2; i += NT) reinterpret_cast<uint32_t *>(gamma)[i] = 0u;
+        if ((n * k) & 1) gamma[n * k - 1] = 0;
+        for (size_t i = tid; i < (size_t)k * nranks; i += NT) wc[i] = 0;
+        __syncthreads();
+        for (int u = tid; u < n; u += NT) {  // gamma rows owned per thread
+            uint16_t *row = gamma + (size_t)u * k;
+            for (int64_t idx = P.indptr[u]; idx < P.indptr[u + 1]; idx++) row[assign[__ldg(P.indices + idx)]]++;
+        }
+        __syncthreads();
+        {  // wc[c][rank] member counts (u16 pairs updated with 32-bit atomics)
+            for (int v = tid; v < n; v += NT) {
+                const size_t e = (size_t)assign[v] * nranks + wrk[v];
+                unsigned int *w32 = reinterpret_cast<unsigned int *>(wc) + (e >> 1);
+                atomicAdd(w32, 1u << (16 * (e & 1)));
+            }
+        }
+        __syncthreads();
+        for (int c = warp; c < k; c += NW) refresh_class(c);
+        __syncthreads();
+        // scratch score / conflicts (:70-86)
+        {
+            long long sc = 0, cf = 0;
+            for (int c = tid; c < k; c += NT) sc += max_rank[c] >= 0 ? P.wvals[max_rank[c]] : 0;
+            for (int64_t e = tid; e < P.m; e += NT) cf += assign[__ldg(P.eu + e)] == assign[__ldg(P.ev + e)];
+            __syncthreads();
+            sc = warp_sum64(sc);
+            cf = warp_sum64(cf);
+            if (lane == 0) {
+                ctl.red[warp] = sc;
+                ctl.red2[warp] = cf;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                long long s = 0, f = 0;
+                for (int j = 0; j < NW; j++) {
+                    s += ctl.red[j];
+                    f += ctl.red2[j];
+                }
+                ctl.score = s;
+                ctl.conflicts = f;
+                ctl.best = (f == 0) ? s : INF_SCORE;
+                ctl.it = 0;
+                ctl.ctr = 0;
+                ctl.nlog = 0;
+                ctl.diag = 0;
+                ctl.phi = P.phi0s[ind];
+                phis[0] = ctl.phi;
+            }
+            __syncthreads();
+        }
+        if (ctl.conflicts == 0)
+            for (int v = tid; v < n; v += NT) b_out[v] = assign[v];
+
+        // ---------------- rounds (:156-258) ----------------
+        for (int64_t rnd = 0; rnd < P.rounds; rnd++) {
+            if (tid == 0 && P.schedule_on && rnd == P.rounds - 1) {
+                ctl.phi = P.forced_phi;
+                phis[P.rounds] = ctl.phi;
+            }
+            for (int v = tid; v < n; v += NT) tabu_until[v] = 0;
+            __syncthreads();
+            for (int64_t step = 0; step < P.depth; step++) {
+                const long long it = ctl.it, score = ctl.score, conflicts = ctl.conflicts,
+                                best = ctl.best;
+                const double phi = ctl.phi;
+                // pass 1: (min g, count) per vertex row over admissible candidates
+                for (int v = tid; v < n; v += NT) {
+                    const int a = assign[v];
+                    const long long rem = (wrk[v] == max_rank[a]) ? uniq_drop[a] : 0;
+                    const uint16_t *row = gamma + (size_t)v * k;
+                    const int gva = row[a];
+                    const bool frozen = (uint64_t)it < tabu_until[v];
+                    const long long wv = wgt[v];
+                    double m = INF;
+                    int cnt = 0;
+                    for (int c = 0; c < k; c++) {
+                        if (c == a) continue;
+                        const long long dc = (long long)row[c] - gva;
+                        long long dadd = wv - max_val[c];
+                        if (dadd < 0) dadd = 0;
+                        const long long ds = dadd - rem;
+                        if (frozen && (conflicts + dc != 0 || score + ds >= best)) continue;
+                        const double gv = gval_of(ds, dc, phi);
+                        if (gv < m) {
+                            m = gv;
+                            cnt = 1;
+                        } else if (gv == m) {
+                            cnt++;
+                        }
+                    }
+                    rmin[v] = m;
+                    rcnt[v] = (uint16_t)cnt;
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    // prefix-min over rows in vertex order (chunks of 32 rows)
+                    double carry = INF, lmin = INF;
+                    int lT = 0, lfirst = INT_MAX, tsum = 0, nlow = 0;
+                    for (int base = 0; base < n; base += 32) {
+                        const int v = base + lane;
+                        const double x = v < n ? rmin[v] : INF;
+                        const int nq = v < n ? rcnt[v] : 0;
+                        double incl = x;
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const double t = shfl_up_d(incl, o);
+                            if (lane >= o) incl = fmin(incl, t);
+                        }
+                        double excl = shfl_up_d(incl, 1);
+                        if (lane == 0) excl = INF;
+                        const double RM = fmin(carry, excl);
+                        if (x < lmin) {
+                            lmin = x;
+                            lT = nq;
+                            lfirst = v;
+                        } else if (x == lmin && x != INF) {
+                            lT += nq;
+                        }
+                        bool low = false;
+                        if (!prod && x != INF) {
+                            if (x == RM) tsum += nq;
+                            else if (x < RM) low = true;
+                        }
+                        const unsigned lb = __ballot_sync(FULL, low);
+                        if (low) {
+                            const int pos = nlow + __popc(lb & ((1u << lane) - 1u));
+                            lowq[pos] = v;
+                            lowR[pos] = RM;
+                        }
+                        nlow += __popc(lb);
+                        carry = fmin(carry, shfl_d(incl, 31));
+                    }
+                    __syncwarp();
+                    // walk the rows that lower the running minimum (lanes over colours)
+                    for (int j = 0; j < nlow; j++) {
+                        const int v = lowq[j];
+                        const double R = lowR[j];
+                        const int a = assign[v];
+                        const long long rem = (wrk[v] == max_rank[a]) ? uniq_drop[a] : 0;
+                        const uint16_t *row = gamma + (size_t)v * k;
+                        const int gva = row[a];
+                        const bool frozen = (uint64_t)it < tabu_until[v];
+                        const long long wv = wgt[v];
+                        double cr = R;
+                        int t = 0;
+                        for (int c0 = 0; c0 < k; c0 += 32) {
+                            const int c = c0 + lane;
+                            double gv = INF;
+                            if (c < k && c != a) {
+                                const long long dc = (long long)row[c] - gva;
+                                long long dadd = wv - max_val[c];
+                                if (dadd < 0) dadd = 0;
+                                const long long ds = dadd - rem;
+                                if (!(frozen && (conflicts + dc != 0 || score + ds >= best)))
+                                    gv = gval_of(ds, dc, phi);
+                            }
+                            double incl = gv;
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const double tt = shfl_up_d(incl, o);
+                                if (lane >= o) incl = fmin(incl, tt);
+                            }
+                            double excl = shfl_up_d(incl, 1);
+                            if (lane == 0) excl = INF;
+                            const double cur = fmin(cr, excl);
+                            if (gv != INF && gv == cur) t++;
+                            cr = fmin(cr, shfl_d(incl, 31));
+                        }
+                        tsum += __reduce_add_sync(FULL, t) * (lane == 0 ? 1 : 0);
+                    }
+                    const double D = carry;
+                    int mv_v = -1, mv_b = 0;
+                    long long mv_ds = 0, mv_dc = 0;
+                    bool mv_tabu = false;
+                    if (D != INF) {
+                        // all lanes agree on D; T, first row, total ties
+                        const int T = __reduce_add_sync(FULL, lmin == D ? lT : 0);
+                        const int L = (int)__reduce_min_sync(FULL, (unsigned)(lmin == D ? lfirst : INT_MAX));
+                        const int total = __reduce_add_sync(FULL, tsum);
+                        const unsigned long long ctr = ctl.ctr;
+                        int sstar = 1;
+                        if (T > 1) {
+                            if (!prod) {
+                                const unsigned long long c0 = ctr + (unsigned long long)(total - (T - 1));
+                                int smax = 1;
+                                for (int s = 2 + lane; s <= T; s += 32)
+                                    if (below_is_zero(key, c0 + (unsigned long long)(s - 2), (uint32_t)s))
+                                        smax = s;
+                                sstar = __reduce_max_sync(FULL, smax);
+                            } else {
+                                sstar = 1 + (int)philox_below(key, ctr, (uint32_t)T);
+                            }
+                        }
+                        int row = L, need = 1;
+                        if (sstar > 1) {
+                            int cum = 0;
+                            for (int base = 0; base < n; base += 32) {
+                                const int v = base + lane;
+                                const int c = (v < n && rmin[v] == D) ? rcnt[v] : 0;
+                                const int incl = warp_incl_sum(c, lane);
+                                const int tot = __shfl_sync(FULL, incl, 31);
+                                if (cum + tot >= sstar) {
+                                    const unsigned bm = __ballot_sync(FULL, cum + incl >= sstar);
+                                    const int src = __ffs(bm) - 1;
+                                    row = base + src;
+                                    need = sstar - cum - __shfl_sync(FULL, incl - c, src);
+                                    break;
+                                }
+                                cum += tot;
+                            }
+                        }
+                        // within the row: the need-th colour with g == D
+                        const int v = row;
+                        const int a = assign[v];
+                        const long long rem = (wrk[v] == max_rank[a]) ? uniq_drop[a] : 0;
+                        const uint16_t *rw = gamma + (size_t)v * k;
+                        const int gva = rw[a];
+                        const bool frozen = (uint64_t)it < tabu_until[v];
+                        const long long wv = wgt[v];
+                        int cum = 0, b = -1;
+                        long long bds = 0, bdc = 0;
+                        for (int c0 = 0; c0 < k && b < 0; c0 += 32) {
+                            const int c = c0 + lane;
+                            bool hit = false;
+                            long long ds = 0, dc = 0;
+                            if (c < k && c != a) {
+                                dc = (long long)rw[c] - gva;
+                                long long dadd = wv - max_val[c];
+                                if (dadd < 0) dadd = 0;
+                                ds = dadd - rem;
+                                if (!(frozen && (conflicts + dc != 0 || score + ds >= best)))
+                                    hit = gval_of(ds, dc, phi) == D;
+                            }
+                            const unsigned hm = __ballot_sync(FULL, hit);
+                            const int hc = __popc(hm);
+                            if (cum + hc >= need) {
+                                unsigned mm = hm;
+                                for (int q = 1; q < need - cum; q++) mm &= mm - 1u;
+                                const int src = __ffs(mm) - 1;
+                                b = c0 + src;
+                                bds = __shfl_sync(FULL, ds, src);
+                                bdc = __shfl_sync(FULL, dc, src);
+                            }
+                            cum += hc;
+                        }
+                        mv_v = v;
+                        mv_b = b;
+                        mv_ds = bds;
+                        mv_dc = bdc;
+                        mv_tabu = frozen;
+                        if (lane == 0) {
+                            unsigned long long c = ctr;
+                            uint32_t ll;
+                            if (!prod) {
+                                c += (unsigned long long)total;
+                                ll = u64_below32(key, c, 10u);
+                                c += 1;
+                            } else {
+                                ll = philox_below(key, c + 1, 10u);
+                                c += 2;
+                            }
+                            const long long tt = (long long)ll + P.tt_base;
+                            tabu_until[v] = (uint32_t)(it + tt + 1);
+                            ctl.ctr = c;
+                            ctl.mv_v = v;
+                            ctl.mv_a = a;
+                            ctl.mv_b = b;
+                            ctl.score = score + mv_ds;
+                            ctl.conflicts = conflicts + mv_dc;
+                            const long long nl = ctl.nlog;
+                            if (nl < P.log_cap) {
+                                const size_t o = (size_t)ind * P.log_cap + nl;
+                                P.log_v[o] = v;
+                                P.log_iter[o] = it;
+                                P.log_tt[o] = tt;
+                                P.log_asp[o] = mv_tabu ? 1 : 0;
+                                ctl.nlog = nl + 1;
+                            }
+                            if (b < 0) atomicExch(P.err_flag, 3);
+                        }
+                    }
+                    if (lane == 0) ctl.has_move = (mv_v >= 0);
+                    (void)mv_b;
+                }
+                __syncthreads();
+                if (ctl.has_move) {
+                    const int v = ctl.mv_v, a = ctl.mv_a, b = ctl.mv_b;
+                    // gamma over N(v) (:218-221)
+                    for (int64_t idx = P.indptr[v] + tid; idx < P.indptr[v + 1]; idx += NT) {
+                        const int u = __ldg(P.indices + idx);
+                        gamma[(size_t)u * k + a]--;
+                        gamma[(size_t)u * k + b]++;
+                    }
+                    if (tid == 0) {
+                        const int r = wrk[v];
+                        wc[(size_t)a * nranks + r]--;
+                        wc[(size_t)b * nranks + r]++;
+                        assign[v] = (uint8_t)b;
+                    }
+                    __syncthreads();
+                    if (warp == 0) refresh_class(a);
+                    else if (warp == 1) refresh_class(b);
+                    __syncthreads();
+                    if (tid == 0 && ctl.conflicts == 0 && ctl.score < ctl.best) {
+                        ctl.best = ctl.score;
+                        ctl.red[0] = 1;  // copy flag
+                    } else if (tid == 0) {
+                        ctl.red[0] = 0;
+                    }
+                    __syncthreads();
+                    if (ctl.red[0])
+                        for (int u = tid; u < n; u += NT) b_out[u] = assign[u];
+                }
+                if (tid == 0) ctl.it = it + 1;
+                const long long itn = it + 1;
+                if (diagf && itn % 1024 == 0) {  // scratch check (:245-249)
+                    for (int c = tid; c < k; c += NT) cmax[c] = -1;
+                    __syncthreads();
+                    for (int u = tid; u < n; u += NT) atomicMax(&cmax[assign[u]], (int)wrk[u]);
+                    long long cf = 0;
+                    for (int64_t e = tid; e < P.m; e += NT) cf += assign[__ldg(P.eu + e)] == assign[__ldg(P.ev + e)];
+                    __syncthreads();
+                    long long sc = 0;
+                    for (int c = tid; c < k; c += NT) sc += cmax[c] >= 0 ? P.wvals[cmax[c]] : 0;
+                    sc = warp_sum64(sc);
+                    cf = warp_sum64(cf);
+                    if (lane == 0) {
+                        ctl.red[warp] = sc;
+                        ctl.red2[warp] = cf;
+                    }
+                    __syncthreads();
+                    if (tid == 0) {
+                        long long s = 0, f = 0;
+                        for (int j = 0; j < NW; j++) {
+                            s += ctl.red[j];
+                            f += ctl.red2[j];
+                        }
+                        if (s != ctl.score || f != ctl.conflicts) ctl.diag += 1;
+                    }
+                }
+                __syncthreads();
+            }
+            if (tid == 0) {  // phi schedule (:251-258)
+                if (P.schedule_on && rnd < P.rounds - 1) {
+                    ctl.phi = (ctl.conflicts == 0) ? ctl.phi / 2.0 : ctl.phi * 2.0;
+                    phis[rnd + 1] = ctl.phi;
+                } else if (!P.schedule_on) {
+                    phis[rnd + 1] = ctl.phi;
+                }
+            }
+            __syncthreads();
+        }
+        for (int v = tid; v < n; v += NT) a_io[v] = assign[v];
+        if (tid == 0) {
+            P.end_scores[ind] = ctl.score;
+            P.end_conflicts[ind] = ctl.conflicts;
+            P.best_scores[ind] = ctl.best;
+            P.diag[ind] = ctl.diag;
+            if (P.log_cnt) P.log_cnt[ind] = ctl.nlog;
+        }
+        __syncthreads();
+    }
+}
+
+static size_t wv_smem(int n, int k) {
+    auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    return a16((size_t)n * k * 2) + a16((size_t)n * 4) + a16((size_t)n * 4) + a16((size_t)n * 2) +
+           a16((size_t)n) + a16((size_t)n * 8) + a16((size_t)n * 2) + a16((size_t)k * 4) +
+           2 * a16((size_t)k * 8) + a16((size_t)k * 4) + a16((size_t)2 * n * 4) + a16((size_t)n * 8);
+}
+
+int wvcp_run(const WvcpArgs &A, cudaStream_t st) {
+    if (A.p < 0 || A.n < 1 || A.k < 1 || A.depth < 0 || A.rounds < 0 || A.nranks < 1)
+        return set_error(MCB_ERR_VALUE, "wvcp: bad shape");
+    if (A.k > 255 || A.n > 65535)
+        return set_error(MCB_ERR_UNSUPPORTED, "wvcp: k<=255 and n<=65535 required");
+    if (A.rounds * A.depth >= (int64_t)1 << 31)
+        return set_error(MCB_ERR_UNSUPPORTED, "wvcp: rounds*depth must be < 2^31");
+    if (A.p == 0) return MCB_OK;
+    const size_t smem = wv_smem((int)A.n, (int)A.k);
+    if (smem > (size_t)max_smem_optin())
+        return set_error(MCB_ERR_UNSUPPORTED, "wvcp: n*k too large for shared memory (%zu B)", smem);
+    if (cudaFuncSetAttribute(wvcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "wvcp: smem attribute failed");
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wvcp_kernel, WV_NT, smem);
+    nb = std::max(nb, 1);
+    const int grid = (int)std::min<int64_t>(A.p, (int64_t)nb * num_sms());
+    const size_t wc_stride = (((size_t)A.k * A.nranks + 1) / 2 * 2 + 127) & ~(size_t)127;  // u16 elements
+    uint8_t *ws = (uint8_t *)workspace(256 + (size_t)grid * wc_stride * 2);
+    if (!ws) return set_error(MCB_ERR_CUDA, "wvcp: workspace");
+    cudaMemsetAsync(ws, 0, 256, st);
+    WvParams P{};
+    P.assigns = A.assigns;
+    P.best_assigns = A.best_assigns;
+    P.indptr = A.indptr;
+    P.indices = A.indices;
+    P.eu = A.eu;
+    P.ev = A.ev;
+    P.m = A.m;
+    P.wranks = A.wranks;
+    P.wvals = A.wvals;
+    P.nranks = (int)A.nranks;
+    P.weights = A.weights;
+    P.n = (int)A.n;
+    P.k = (int)A.k;
+    P.depth = A.depth;
+    P.rounds = A.rounds;
+    P.schedule_on = A.schedule_on;
+    P.phi0s = A.phi0s;
+    P.forced_phi = A.forced_phi;
+    P.tt_base = A.tt_base;
+    P.keys = A.keys;
+    P.best_scores = A.best_scores;
+    P.end_scores = A.end_scores;
+    P.end_conflicts = A.end_conflicts;
+    P.phi_used = A.phi_used;
+    P.diag = A.diag;
+    P.log_cap = A.log_cap;
+    P.log_v = A.log_v;
+    P.log_iter = A.log_iter;
+    P.log_tt = A.log_tt;
+    P.log_asp = A.log_asp;
+    P.log_cnt = A.log_cnt;
+    P.flags = A.flags;
+    P.nwork = (int)A.p;
+    int32_t *ctl32 = reinterpret_cast<int32_t *>(ws);
+    P.work_counter = ctl32;
+    P.err_flag = ctl32 + 1;
+    P.ws_wc = reinterpret_cast<uint16_t *>(ws + 256);
+    P.ws_wc_stride = wc_stride;
+    if (getenv("MCB_VERBOSE")) fprintf(stderr, "[mcb] wvcp grid=%d (%d/SM) smem=%zu\n", grid, nb, smem);
+    wvcp_kernel<<<grid, WV_NT, smem, st>>>(P);
+    int32_t err = 0;
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(&err, P.err_flag, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "wvcp kernel failed: %s", cudaGetErrorString(cudaGetLastError()));
+    if (err == 1) return set_error(MCB_ERR_RANGE, "color id out of range [0, k)");
+    if (err) return set_error(MCB_ERR_CUDA, "wvcp: internal error %d", err);
+    return MCB_OK;
+}
+
 }  // namespace mcb
