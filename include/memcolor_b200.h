@@ -127,6 +127,14 @@ int mcb_gpx_batch(const int32_t *pop, int64_t p, int64_t n, const int64_t *match
 int mcb_gpx_batch_host(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches,
                        int64_t K, int64_t k, const uint64_t *keys, int32_t *out, uint32_t flags,
                        void *stream);
+/*
+ * Sharded GPX: the offspring of rows [row_off, row_off + rows) only; matches,
+ * keys and out hold just those rows (matches[r,j] index the full population).
+ * mcb_gpx_batch == mcb_gpx_rows with rows = p, row_off = 0.
+ */
+int mcb_gpx_rows(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches, int64_t rows,
+                 int64_t row_off, int64_t K, int64_t k, const uint64_t *keys, int32_t *out,
+                 uint32_t flags, void *stream);
 
 /*
  * Approximate partition distances over the reference's linear job space

@@ -25,7 +25,7 @@ FLAG_PROFILE = 0x100
 EXPORTS = [
     "mcb_version", "mcb_last_error", "mcb_device_count", "mcb_stream_values",
     "mcb_tabucol_batch", "mcb_tabucol_batch_host", "mcb_wvcp_batch", "mcb_wvcp_batch_host",
-    "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_pairwise", "mcb_pairwise_host",
+    "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_gpx_rows", "mcb_pairwise", "mcb_pairwise_host",
     "mcb_probe_smem_bandwidth", "mcb_debug_phase_cycles",
 ]
 
@@ -52,6 +52,7 @@ def _declare(L):
     gp = [P, I64, I64, P, I64, I64, P, P, U32, P]
     L.mcb_gpx_batch.argtypes = gp
     L.mcb_gpx_batch_host.argtypes = gp
+    L.mcb_gpx_rows.argtypes = [P, I64, I64, P, I64, I64, I64, I64, P, P, U32, P]
     pw = [P, I64, P, I64, I64, I64, P, P, I64, I64, U32, P]
     L.mcb_pairwise.argtypes = pw
     L.mcb_pairwise_host.argtypes = pw

@@ -325,6 +325,13 @@ int mcb_gpx_batch_host(const int32_t *pop, int64_t p, int64_t n, const int64_t *
     return ar.download();
 }
 
+int mcb_gpx_rows(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches, int64_t rows,
+                 int64_t row_off, int64_t K, int64_t k, const uint64_t *keys, int32_t *out,
+                 uint32_t flags, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return gpx_rows_run(pop, p, n, matches, rows, row_off, K, k, keys, out, flags, (cudaStream_t)stream);
+}
+
 int mcb_pairwise(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n,
                  int64_t k, int32_t *cross, int32_t *within, int64_t job_begin, int64_t job_end,
                  uint32_t flags, void *stream) {

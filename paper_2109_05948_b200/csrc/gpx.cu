@@ -24,8 +24,8 @@ constexpr int GPX_WARPS = 4;
 
 __global__ void __launch_bounds__(GPX_WARPS * 32)
     gpx_kernel(const int32_t *__restrict__ pop, int64_t p, int n, const int64_t *__restrict__ matches,
-               int64_t K, int k, const uint64_t *__restrict__ keys, int32_t *__restrict__ out,
-               int32_t *err) {
+               int64_t rows, int64_t row_off, int64_t K, int k, const uint64_t *__restrict__ keys,
+               int32_t *__restrict__ out, int32_t *err) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // per-warp layout
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(GPX_WARPS * 32)
     uint16_t *mem_b = mem_a + n;
     int16_t *child = reinterpret_cast<int16_t *>(mem_b + n);
 
-    const int64_t njobs = p * K;
+    const int64_t njobs = rows * K;
     for (int64_t job = (int64_t)blockIdx.x * GPX_WARPS + warp; job < njobs;
          job += (int64_t)gridDim.x * GPX_WARPS) {
         const int64_t i = job / K, j = job % K;
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(GPX_WARPS * 32)
             if (lane == 0) atomicExch(err, 1);
             continue;
         }
-        const int32_t *pa = pop + (size_t)i * n;
+        const int32_t *pa = pop + (size_t)(row_off + i) * n;
         const int32_t *pb = pop + (size_t)mi * n;
         const uint64_t key = keys[job];
         for (int c = lane; c < kp; c += 32) {
@@ -154,11 +154,20 @@ __global__ void __launch_bounds__(GPX_WARPS * 32)
 
 int gpx_run(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches, int64_t K, int64_t k,
             const uint64_t *keys, int32_t *out, uint32_t flags, cudaStream_t st) {
+    return gpx_rows_run(pop, p, n, matches, p, 0, K, k, keys, out, flags, st);
+}
+
+int gpx_rows_run(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches, int64_t rows,
+                 int64_t row_off, int64_t K, int64_t k, const uint64_t *keys, int32_t *out,
+                 uint32_t flags, cudaStream_t st) {
+    if (rows < 0 || row_off < 0 || row_off + rows > p)
+        return set_error(MCB_ERR_VALUE, "gpx: row range [%lld, %lld) outside the population",
+                         (long long)row_off, (long long)(row_off + rows));
     if (p < 0 || n < 0 || K < 0 || k < 1)
         return set_error(MCB_ERR_VALUE, "gpx: bad shape p=%lld n=%lld K=%lld k=%lld", (long long)p,
                          (long long)n, (long long)K, (long long)k);
     if (n > 65535 || k > 32767) return set_error(MCB_ERR_UNSUPPORTED, "gpx: n<=65535, k<=32767");
-    if (p == 0 || K == 0 || n == 0) return MCB_OK;
+    if (rows == 0 || K == 0 || n == 0) return MCB_OK;
     const int kp = ((int)k + 3) & ~3;
     const size_t per = (size_t)4 * kp * 4 + (size_t)2 * n * 2 + (size_t)n * 2 + 64;
     const size_t smem = GPX_WARPS * ((per + 15) & ~(size_t)15);
@@ -169,12 +178,13 @@ int gpx_run(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches, in
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gpx_kernel, GPX_WARPS * 32, smem);
     nb = std::max(nb, 1);
-    const int64_t jobs = p * K;
+    const int64_t jobs = rows * K;
     const int grid = (int)std::min<int64_t>((jobs + GPX_WARPS - 1) / GPX_WARPS, (int64_t)nb * num_sms());
     int32_t *err = (int32_t *)workspace(256);
     if (!err) return set_error(MCB_ERR_CUDA, "gpx: workspace");
     cudaMemsetAsync(err, 0, 4, st);
-    gpx_kernel<<<grid, GPX_WARPS * 32, smem, st>>>(pop, p, (int)n, matches, K, (int)k, keys, out, err);
+    gpx_kernel<<<grid, GPX_WARPS * 32, smem, st>>>(pop, p, (int)n, matches, rows, row_off, K, (int)k,
+                                                   keys, out, err);
     int32_t herr = 0;
     if (cudaGetLastError() != cudaSuccess ||
         cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||

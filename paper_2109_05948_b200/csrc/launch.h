@@ -64,6 +64,9 @@ int wvcp_run(const WvcpArgs &a, cudaStream_t st);
 
 int gpx_run(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches, int64_t K, int64_t k,
             const uint64_t *keys, int32_t *out, uint32_t flags, cudaStream_t st);
+int gpx_rows_run(const int32_t *pop, int64_t p, int64_t n, const int64_t *matches, int64_t rows,
+                 int64_t row_off, int64_t K, int64_t k, const uint64_t *keys, int32_t *out,
+                 uint32_t flags, cudaStream_t st);
 int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n, int64_t k,
                  int32_t *cross, int32_t *within, int64_t job_begin, int64_t job_end,
                  uint32_t flags, cudaStream_t st);

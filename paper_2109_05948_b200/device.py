@@ -119,3 +119,15 @@ def pairwise(pop, off, k, job_begin=0, job_end=-1, cross=None, within=None):
     N.check(N.lib().mcb_pairwise(N.ptr(pop), p, N.ptr(off), q, n, int(k), N.ptr(cross),
                                  N.ptr(within), int(job_begin), int(job_end), 0, _stream_handle()))
     return cross, within
+
+
+def gpx_rows(pop, matches_rows, row_off, k, keys_rows, out=None):
+    """Offspring of population rows [row_off, row_off + rows) (sharded GPX,
+    `mcb_gpx_rows`); `matches_rows` indexes the full population `pop`."""
+    p, n = pop.shape
+    rows, K = matches_rows.shape
+    if out is None:
+        out = torch.empty((rows, K, n), dtype=torch.int32, device=pop.device)
+    N.check(N.lib().mcb_gpx_rows(N.ptr(pop), p, n, N.ptr(matches_rows), rows, int(row_off), K,
+                                 int(k), N.ptr(keys_rows), N.ptr(out), 0, _stream_handle()))
+    return out

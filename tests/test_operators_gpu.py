@@ -90,3 +90,22 @@ def test_distance_job_range_sharding():
     np.testing.assert_array_equal(c, c_full)
     np.testing.assert_array_equal(w, w_full)
     assert (np.diagonal(w) == 0).all() and (w == w.T).all()
+
+
+def test_gpx_rows_sharding_matches_full():
+    import torch
+
+    from paper_2109_05948_b200 import device as D
+
+    P = random_col_assigns(700, 30, 10, 5)
+    rs = np.random.default_rng(3)
+    matches = rs.integers(0, 10, size=(10, 4)).astype(np.int64)
+    keys = stream_keys(5, TAG_CROSS, 1, 40)
+    full = CX.gpx_batch(P, matches, 30, keys)
+    pop = torch.from_numpy(P).cuda()
+    parts = []
+    for lo, hi in ((0, 3), (3, 10)):
+        m = torch.from_numpy(matches[lo:hi].copy()).cuda()
+        kk = D.keys_to_tensor(keys[lo * 4:hi * 4], "cuda")
+        parts.append(D.gpx_rows(pop, m, lo, 30, kk).cpu().numpy())
+    np.testing.assert_array_equal(np.concatenate(parts), full)
