@@ -348,7 +348,7 @@ def run_ours(args):
                      "hbm_peak_gbs": peaks.get("hbm_gbs")},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": 3 * args.steps,  # per step: CSR offsets -> constant, narrow + wide TabuCol
         "clocks": clocks,
         "collective_ms_per_step": statistics.mean(coll_ms) if world > 1 else 0.0,
         "mean_C": sumc_all / moves_all, "mean_deg": sumdeg_all / moves_all,

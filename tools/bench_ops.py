@@ -1,0 +1,123 @@
+"""Throughput of the secondary hot-path operators on one GPU, beside the CPU
+restatement of the reference on this host (oracle/, OpenMP, all cores).
+
+* WVCP moves/s      config 3 shape: G(500,.5) w in [1,100], k=60 (D, depth reduced)
+* GPX offspring/s   config 2 shape: n=1000, k=83, parents (i, uniform j != i)
+* distance pairs/s  config 2 shape: n=1000, k=83 pairwise_distances(P, P')
+
+Each line: {"op", "gpu": units/s, "cpu": units/s, "cores", "sample", ...}.
+Synthetic inputs; device-resident inputs, CUDA-event timing.
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import oracle  # noqa: E402
+from paper_2109_05948_b200 import _native as N  # noqa: E402
+from paper_2109_05948_b200 import device as Dv  # noqa: E402
+from paper_2109_05948_b200 import localsearch as LS  # noqa: E402
+from paper_2109_05948_b200.graph import rand_graph  # noqa: E402
+from paper_2109_05948_b200.init import random_col_assigns  # noqa: E402
+from paper_2109_05948_b200.rng import TAG_CROSS, TAG_LS, TAG_MISC, stream_keys  # noqa: E402
+
+
+def timed(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps, out
+
+
+def bench_wvcp(a):
+    g = rand_graph(1, 500, 0.5, wmax=100)
+    k, D, depth, rounds = 60, a.wvcp_pop, a.wvcp_depth, 10
+    A = random_col_assigns(500, k, D, 1)
+    keys = stream_keys(1, TAG_LS, 0, D)
+    dg = Dv.DeviceGraph(g, "cuda")
+    kd = Dv.keys_to_tensor(keys, "cuda")
+    a0 = torch.from_numpy(A).cuda()
+    phi0 = LS.default_wvcp_phi0(g, k)
+    t, _ = timed(lambda: Dv.wvcp_batch(dg, a0.clone(), k, kd, depth, rounds, True, phi0))
+    moves = D * depth * rounds
+    cores = os.cpu_count()
+    nc = max(16, cores)
+    t0 = time.perf_counter()
+    oracle.wvcp_batch(g, A[:nc].copy(), k, keys[:nc], depth, rounds, True, phi0, threads=cores)
+    tc = time.perf_counter() - t0
+    return {"op": "wvcp", "unit": "moves/s", "gpu": moves / t, "cpu": nc * depth * rounds / tc,
+            "cores": cores, "config": f"G(500,.5) w<=100 k=60 D={D} {rounds}x{depth}",
+            "cpu_sample": f"{nc} individuals x {rounds}x{depth}", "gpu_ms": 1e3 * t}
+
+
+def bench_gpx(a):
+    n, k, p, K = 1000, 83, a.gpx_pop, 16
+    P = random_col_assigns(n, k, p, 1)
+    rs = np.random.default_rng(7)
+    matches = (np.arange(p)[:, None] + 1 + rs.integers(0, p - 1, size=(p, K))) % p  # j != i
+    keys = stream_keys(1, TAG_CROSS, 0, p * K)
+    pop = torch.from_numpy(P).cuda()
+    m = torch.from_numpy(matches.astype(np.int64)).cuda()
+    kd = Dv.keys_to_tensor(keys, "cuda")
+    out = torch.empty((p, K, n), dtype=torch.int32, device="cuda")
+    t, _ = timed(lambda: Dv.gpx_batch(pop, m, k, kd, out))
+    cores = os.cpu_count()
+    pc = min(p, 512)
+    t0 = time.perf_counter()
+    oracle.gpx_batch(P[:pc], matches[:pc] % pc, k, keys[:pc * K], threads=cores)
+    tc = time.perf_counter() - t0
+    return {"op": "gpx", "unit": "offspring/s", "gpu": p * K / t, "cpu": pc * K / tc,
+            "cores": cores, "config": f"n={n} k={k} p={p} K={K}",
+            "cpu_sample": f"{pc}x{K} offspring", "gpu_ms": 1e3 * t,
+            "alg_bytes_per_offspring": 3 * n}
+
+
+def bench_distance(a):
+    n, k, p = 1000, 83, a.dist_pop
+    P = random_col_assigns(n, k, p, 1)
+    Q = random_col_assigns(n, k, p, 2)
+    pd, qd = torch.from_numpy(P).cuda(), torch.from_numpy(Q).cuda()
+    cross = torch.zeros((p, p), dtype=torch.int32, device="cuda")
+    within = torch.zeros((p, p), dtype=torch.int32, device="cuda")
+    t, _ = timed(lambda: Dv.pairwise(pd, qd, k, cross=cross, within=within), reps=2)
+    pairs = p * p + p * (p - 1) // 2
+    cores = os.cpu_count()
+    pc = 96
+    t0 = time.perf_counter()
+    oracle.pairwise(P[:pc], Q[:pc], k, threads=cores)
+    tc = time.perf_counter() - t0
+    return {"op": "distance", "unit": "pairs/s", "gpu": pairs / t,
+            "cpu": (pc * pc + pc * (pc - 1) // 2) / tc, "cores": cores,
+            "config": f"n={n} k={k} p=q={p} (random colourings)", "cpu_sample": f"p=q={pc}",
+            "gpu_ms": 1e3 * t, "alg_bytes_per_pair": 6 * n}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ops", default="wvcp,gpx,distance")
+    ap.add_argument("--wvcp-pop", type=int, default=592)
+    ap.add_argument("--wvcp-depth", type=int, default=500)
+    ap.add_argument("--gpx-pop", type=int, default=16384)
+    ap.add_argument("--dist-pop", type=int, default=4096)
+    a = ap.parse_args()
+    N.lib()
+    oracle.build()
+    for op in a.ops.split(","):
+        r = {"wvcp": bench_wvcp, "gpx": bench_gpx, "distance": bench_distance}[op](a)
+        r["speedup_vs_cpu"] = r["gpu"] / r["cpu"]
+        print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
