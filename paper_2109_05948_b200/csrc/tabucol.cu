@@ -124,7 +124,8 @@ template <int NW>
 struct TabuCtrl {
     long long it, conflicts, best, nlog, sum_c, sum_deg, diag;
     unsigned long long ctr;
-    int C, work, ovf;
+    long long s0, s1;
+    int C, work, ovf, mv_v, mv_a, mv_b, gvb;
     long long red[NW];
     int wcnt[NW];
     long long ph[10];
@@ -261,7 +262,7 @@ struct RowEval {
         if (active<S>(tovf[v], it)) spill_scan(gstamp + (size_t)v * kp, it, A);
     }
     // spilled expiries: dense global row (rare; kept out of the hot code)
-    __device__ __noinline__ void spill_scan(const S *gs, uint32_t it, int A) {
+    __device__ __forceinline__ void spill_scan(const S *gs, uint32_t it, int A) {
         for (int c = 0; c < k; c++)
             if (active<S>(gs[c], it) && !(gv(c) < A)) setbit(c);
     }
@@ -361,6 +362,43 @@ struct RowEval {
     }
 };
 
+// conflict-list membership update (:374-385): append, or swap-with-last remove
+__device__ __forceinline__ void cl_apply(uint16_t *clist, uint16_t *cpos, int &Cn, int u, bool in_conf) {
+    const int pu = cpos[u];
+    if (in_conf && pu == 0xFFFF) {
+        cpos[u] = (uint16_t)Cn;
+        clist[Cn] = (uint16_t)u;
+        Cn++;
+    } else if (!in_conf && pu != 0xFFFF) {
+        const int last = clist[Cn - 1];
+        clist[pu] = (uint16_t)last;
+        cpos[last] = (uint16_t)pu;
+        Cn--;
+        cpos[u] = 0xFFFF;
+    }
+}
+
+// warp-cooperative walks of the queued (running min, row) pairs; returns the
+// tie events on lane 0 (0 elsewhere)
+template <typename G, typename S, int KQ, typename Rec>
+__device__ __forceinline__ int walk_queued(const Rec *lowl, int nlow, const G *gamma, const S *texp,
+                                           const uint8_t *tcol, const S *tovf, const S *gstamp,
+                                           const uint8_t *assign, const uint16_t *clist, int kp, int k,
+                                           uint32_t it32, int thr, const uint32_t *lut, int rs, int rm,
+                                           int lane) {
+    __syncwarp();
+    int t = 0;
+    for (int j = 0; j < nlow; j++) {
+        const int2 e = rec_unpack(lowl[j]);  // (running min, row)
+        RowEval<G, S, KQ> re;
+        re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[e.y], kp, k, it32, thr, lut, rs, rm);
+        const int tj = re.warp_walk_ties(e.x, lane);
+        if (lane == 0) t += tj;
+    }
+    __syncwarp();
+    return t;
+}
+
 template <typename G, typename S, bool GSM, int KQ, int NT>
 __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_kernel(TabuParams P) {
     constexpr int NW = NT / 32;
@@ -400,6 +438,10 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
     Rec *rmc = reinterpret_cast<Rec *>(smem + off);  // per row: (min delta, count)
     off += (sizeof(Rec) * n + 15) & ~(size_t)15;
     Rec *lowl = reinterpret_cast<Rec *>(smem + off);  // queued (row, running min) pairs
+    off += sizeof(Rec) * TC_LOWCAP;
+    uint16_t *nbs = reinterpret_cast<uint16_t *>(smem + off);  // staged N(v)
+    off += (2 * (size_t)n + 15) & ~(size_t)15;
+    uint32_t *evm = reinterpret_cast<uint32_t *>(smem + off);  // event ballots per 32 neighbours
     S *gstamp = reinterpret_cast<S *>(P.ws_stamp + blockIdx.x * P.ws_s_stride);
 
     const int tid = threadIdx.x, lane = tid & 31, hw_warp = tid >> 5;
@@ -420,18 +462,19 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
     const bool prod = (P.flags & MCB_FLAG_PRODUCTION) != 0;
     const bool profile = (P.flags & MCB_FLAG_PROFILE) != 0;
     const bool cidx = P.const_indptr != 0;
-    const int Wq = kp >> 2;
+    const int Wq = kp >> 2, swz_rs = P.swz_rs, swz_rm = P.swz_rm;
     // element offset of (vertex, colour) in gamma, rows rotated by rot(v) words
-    auto goff = [&](int v, int c) -> size_t {
+    auto goff = [=](int v, int c) -> size_t {
         if constexpr (NARROW) {
-            int p = (c >> 2) + ((v >> P.swz_rs) & P.swz_rm);
+            int p = (c >> 2) + ((v >> swz_rs) & swz_rm);
             if (p >= Wq) p -= Wq;
             return (size_t)v * kp + 4 * p + (c & 3);
         } else {
             return (size_t)v * kp + c;
         }
     };
-    auto row_begin = [&](int v) -> int64_t { return cidx ? (int64_t)c_indptr[v] : P.indptr[v]; };
+    const int64_t *indptr_g = P.indptr;
+    auto row_begin = [=](int v) -> int64_t { return cidx ? (int64_t)c_indptr[v] : indptr_g[v]; };
 
     for (;;) {
         if (tid == 0) ctl.work = atomicAdd(P.work_counter, 1);
@@ -558,7 +601,7 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                 // pass 1: (min, count) of every conflicting row, one row per thread
                 for (int li = tid; li < C; li += NT) {
                     RE re;
-                    re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[li], kp, k, it32, thr, s_nib, P.swz_rs, P.swz_rm);
+                    re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[li], kp, k, it32, thr, s_nib, swz_rs, swz_rm);
                     int rm, cnt;
                     re.min_count(rm, cnt);
                     rmc[li] = rec_pack(rm, cnt, (Rec *)nullptr);
@@ -572,20 +615,12 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                 if (warp == 0) {
                     constexpr int R = 4;
                     int nlow = 0;
-                    auto flush = [&]() {  // warp-cooperative walks of the queued rows
-                        __syncwarp();
-                        for (int j = 0; j < nlow; j++) {
-                            const int2 e = rec_unpack(lowl[j]);  // (running min, row)
-                            RE re;
-                            re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[e.y], kp, k, it32, thr, s_nib, P.swz_rs, P.swz_rm);
-                            const int t = re.warp_walk_ties(e.x, lane);
-                            if (lane == 0) tsum += t;
-                        }
-                        __syncwarp();
-                        nlow = 0;
-                    };
                     for (int r0 = 0; r0 < C; r0 += 32 * R) {
-                        if (nlow > TC_LOWCAP - 32 * R) flush();
+                        if (nlow > TC_LOWCAP - 32 * R) {
+                            tsum += walk_queued<G, S, KQ>(lowl, nlow, gamma, texp, tcol, tovf, gstamp, assign,
+                                                          clist, kp, k, it32, thr, s_nib, swz_rs, swz_rm, lane);
+                            nlow = 0;
+                        }
                         int2 mc[R];
                         int lmn = TC_BIG;
 #pragma unroll
@@ -629,7 +664,9 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                         }
                         carry = min(carry, __shfl_sync(FULL, incl, 31));
                     }
-                    if (nlow) flush();
+                    if (nlow)
+                        tsum += walk_queued<G, S, KQ>(lowl, nlow, gamma, texp, tcol, tovf, gstamp, assign,
+                                                      clist, kp, k, it32, thr, s_nib, swz_rs, swz_rm, lane);
                 }
                 PH(2);
 
@@ -640,7 +677,6 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                     int64_t s0 = 0, s1 = 0;
                     constexpr int NB = 8;  // neighbour chunks of 32 held in registers
                     int uu[NB];
-                    int v_guess = -1;
                     if (D != TC_BIG) {
                         const int T = __reduce_add_sync(FULL, lmin == D ? lT : 0);
                         const int L = (int)__reduce_min_sync(FULL, (unsigned)(lmin == D ? lfirst : INT_MAX));
@@ -685,7 +721,6 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                         // the winner's vertex is known: start its adjacency loads now so
                         // they overlap the in-row locate and the tenure/slot bookkeeping
                         const int v = clist[row_li];
-                        v_guess = v;
                         {
                             const int64_t g0 = row_begin(v), g1 = row_begin(v + 1);
 #pragma unroll
@@ -696,7 +731,7 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                         }
                         // locate the need-th D-candidate of the row (lanes over words)
                         RE re;
-                        re.init(gamma, texp, tcol, tovf, gstamp, assign, v, kp, k, it32, thr, s_nib, P.swz_rs, P.swz_rm);
+                        re.init(gamma, texp, tcol, tovf, gstamp, assign, v, kp, k, it32, thr, s_nib, swz_rs, swz_rm);
                         int b = -1;
                         {
                             const int Dg = D + re.gva;
@@ -800,71 +835,76 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                         s1 = __shfl_sync(FULL, s1, 0);
                     }
                     PH(5);
+                    // publish the move and stage the (prefetched) adjacency of v
+                    if (lane == 0) {
+                        ctl.mv_v = mv_v;
+                        ctl.mv_a = mv_a;
+                        ctl.mv_b = mv_b;
+                        ctl.gvb = gvb;
+                        ctl.s0 = s0;
+                        ctl.s1 = s1;
+                    }
                     if (mv_v >= 0) {
-                        // gamma update over N(v) (:356-359) and conflict-list events in
-                        // neighbour order (:368-385): NB*32 neighbours per batch, all
-                        // loads in flight together, events applied in ballot order
-                        int Cn = C;
-                        auto apply = [&](int u, bool in_conf) {
-                            const int pu = cpos[u];
-                            if (in_conf && pu == 0xFFFF) {
-                                cpos[u] = (uint16_t)Cn;
-                                clist[Cn] = (uint16_t)u;
-                                Cn++;
-                            } else if (!in_conf && pu != 0xFFFF) {
-                                const int last = clist[Cn - 1];
-                                clist[pu] = (uint16_t)last;
-                                cpos[last] = (uint16_t)pu;
-                                Cn--;
-                                cpos[u] = 0xFFFF;
-                            }
-                        };
-                        bool bad = false;
-                        bool have = (mv_v == v_guess);
-                        for (int64_t b0 = s0; b0 < s1; b0 += 32 * NB) {
-                            if (!have) {
 #pragma unroll
-                                for (int j = 0; j < NB; j++) {
-                                    const int64_t idx = b0 + j * 32 + lane;
-                                    uu[j] = idx < s1 ? __ldg(P.indices + idx) : 0;
-                                }
+                        for (int j = 0; j < NB; j++)
+                            if (s0 + j * 32 + lane < s1) nbs[j * 32 + lane] = (uint16_t)uu[j];
+                    }
+                }
+                __syncthreads();
+                // all warps: gamma update over N(v) (:356-359), one neighbour per
+                // thread; each warp publishes the ballot of conflict-set events of
+                // its 32 consecutive neighbours
+                const int mvv = ctl.mv_v;
+                if (mvv >= 0) {
+                    const int ma = ctl.mv_a, mb = ctl.mv_b;
+                    const int64_t s0 = ctl.s0;
+                    const int deg = (int)(ctl.s1 - s0);
+                    bool bad = false;
+                    for (int j0 = 0; j0 < deg; j0 += NT) {
+                        const int j = j0 + tid;
+                        bool evt = false;
+                        if (j < deg) {
+                            int u;
+                            if (j < 32 * 8) {
+                                u = nbs[j];
+                            } else {
+                                u = __ldg(P.indices + s0 + j);
+                                nbs[j] = (uint16_t)u;
                             }
-                            have = false;
-                            unsigned em[NB];
-#pragma unroll
-                            for (int j = 0; j < NB; j++) {
-                                const int64_t idx = b0 + j * 32 + lane;
-                                bool evt = false;
-                                if (idx < s1) {
-                                    const int u = uu[j];
-                                    G *pa = gamma + goff(u, mv_a);
-                                    G *pb = gamma + goff(u, mv_b);
-                                    const int ga = (int)*pa - 1;
-                                    *pa = (G)ga;
-                                    const int gb = *pb;
-                                    if (gb >= GMAX) bad = true;
-                                    else *pb = (G)(gb + 1);
-                                    const int au = assign[u];
-                                    evt = (au == mv_a && ga == 0) || (au == mv_b && gb == 0);
-                                }
-                                em[j] = __ballot_sync(FULL, evt);
-                            }
-                            PH(6);
-#pragma unroll
-                            for (int j = 0; j < NB; j++) {
-                                unsigned e = em[j];
-                                while (e) {
-                                    const int src = __ffs(e) - 1;
-                                    e &= e - 1u;
-                                    const int u = __shfl_sync(FULL, uu[j], src);
-                                    if (lane == 0) apply(u, cpos[u] == 0xFFFF);  // enter iff outside
-                                }
-                            }
+                            G *pa = gamma + goff(u, ma);
+                            G *pb = gamma + goff(u, mb);
+                            const int ga = (int)*pa - 1;
+                            *pa = (G)ga;
+                            const int gb = *pb;
+                            if (gb >= GMAX) bad = true;
+                            else *pb = (G)(gb + 1);
+                            const int au = assign[u];
+                            evt = (au == ma && ga == 0) || (au == mb && gb == 0);
                         }
-                        if (__any_sync(FULL, bad) && lane == 0) ctl.ovf = 1;
+                        const unsigned em = __ballot_sync(FULL, evt);
+                        if (lane == 0) evm[(j0 >> 5) + hw_warp] = em;
+                    }
+                    if (bad) ctl.ovf = 1;
+                }
+                __syncthreads();
+                PH(6);
+                // master: conflict-list events in neighbour order (:368-385), then v
+                if (warp == 0) {
+                    if (mvv >= 0) {
                         bool improved = false;
                         if (lane == 0) {
-                            apply(mv_v, gvb > 0);
+                            int Cn = C;
+                            const int deg = (int)(ctl.s1 - ctl.s0);
+                            for (int c = 0; c * 32 < deg; c++) {
+                                unsigned e = evm[c];
+                                while (e) {
+                                    const int bit = __ffs(e) - 1;
+                                    e &= e - 1u;
+                                    const int u = nbs[c * 32 + bit];
+                                    cl_apply(clist, cpos, Cn, u, cpos[u] == 0xFFFF);  // enter iff outside
+                                }
+                            }
+                            cl_apply(clist, cpos, Cn, mvv, ctl.gvb > 0);
                             ctl.C = Cn;
                             if (ctl.conflicts < ctl.best) {
                                 ctl.best = ctl.conflicts;
@@ -962,7 +1002,8 @@ static size_t misc_bytes(int n, int nt) {
     auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
     const size_t rec = sizeof(S) == 2 ? 4 : 8;
     return a16((size_t)n * 4 * sizeof(S)) + a16((size_t)n * 4) + a16((size_t)n * sizeof(S)) +
-           a16(n) + 2 * a16(2 * (size_t)n) + a16(rec * (size_t)n) + rec * TC_LOWCAP;
+           a16(n) + 2 * a16(2 * (size_t)n) + a16(rec * (size_t)n) + rec * TC_LOWCAP +
+           a16(2 * (size_t)n) + a16(4 * (size_t)((n + 31) / 32));
 }
 
 template <typename G, typename S, bool GSM>
