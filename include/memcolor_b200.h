@@ -52,6 +52,7 @@ extern "C" {
 #define MCB_FLAG_FORCE_WIDE 0x4u   /* int16 gamma / 32-bit tabu stamps from the start (tests) */
 #define MCB_FLAG_FORCE_GLOBAL 0x8u /* gamma/tabu tables in global memory (L2-resident path, tests) */
 #define MCB_FLAG_PROFILE 0x100u    /* accumulate per-phase clock64 cycles (mcb_debug_phase_cycles) */
+#define MCB_FLAG_WSTATS 0x200u     /* warp kernel: event counters + phase cycles (mcb_debug_warp_stats) */
 
 const char *mcb_version(void);
 const char *mcb_last_error(void);
@@ -64,6 +65,12 @@ int mcb_probe_smem_bandwidth(double *gbs, double *ms);
 /* Diagnostics: per-phase cycle totals of the TabuCol iteration accumulated
  * by runs with MCB_FLAG_PROFILE (out: 16 counters; [10] = iterations). */
 int mcb_debug_phase_cycles(unsigned long long *out, int reset);
+/* Diagnostics: counters of the last warp-kernel TabuCol launch made with
+ * MCB_FLAG_WSTATS (out: 32 counters, see tabucol_warp.cu WS_*). */
+int mcb_debug_warp_stats(unsigned long long *out);
+/* Diagnostics: the exact fp64 divisibility test of the reservoir draws against
+ * the 64-bit integer %, on `count` pseudo-random pairs; out: #mismatches. */
+int mcb_debug_modcheck(int64_t count, unsigned long long *mismatches);
 
 /* out[i] = stream_value(keys[i], ctrs[i]) (rng.py:56-59); device pointers. */
 int mcb_stream_values(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out, int64_t count,

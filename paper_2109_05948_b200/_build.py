@@ -44,18 +44,33 @@ def _stale():
 
 
 def build(force=False, verbose=False):
-    """Compile every .cu under csrc/ into one shared library (sm_100a)."""
+    """Compile every .cu under csrc/ (one nvcc per file, in parallel) and link
+    them into one shared library (sm_100a)."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    ccbin = ["-ccbin", "/usr/bin/g++"] if os.path.exists("/usr/bin/g++") else []
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include")]
+    comp = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [nvcc(), *ccbin, *ARCH, *comp, *inc, "-c", src, "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(one, sources()))
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
+    cmd = [nvcc(), *ccbin, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd))
-    env = dict(os.environ)
-    # nvcc's host compiler: prefer the system gcc (the image's $CC wrapper lacks libgomp spec)
-    if os.path.exists("/usr/bin/g++"):
-        cmd[1:1] = ["-ccbin", "/usr/bin/g++"]
-    subprocess.run(cmd, check=True, env=env)
+    subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
     return LIB
 

@@ -21,12 +21,14 @@ FLAG_PRODUCTION = 0x2
 FLAG_FORCE_WIDE = 0x4
 FLAG_FORCE_GLOBAL = 0x8
 FLAG_PROFILE = 0x100
+FLAG_WSTATS = 0x200
 
 EXPORTS = [
     "mcb_version", "mcb_last_error", "mcb_device_count", "mcb_stream_values",
     "mcb_tabucol_batch", "mcb_tabucol_batch_host", "mcb_wvcp_batch", "mcb_wvcp_batch_host",
     "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_gpx_rows", "mcb_pairwise", "mcb_pairwise_host",
-    "mcb_probe_smem_bandwidth", "mcb_debug_phase_cycles",
+    "mcb_probe_smem_bandwidth", "mcb_debug_phase_cycles", "mcb_debug_warp_stats",
+    "mcb_debug_modcheck",
 ]
 
 _lib = None
@@ -58,6 +60,8 @@ def _declare(L):
     L.mcb_pairwise_host.argtypes = pw
     L.mcb_probe_smem_bandwidth.argtypes = [P, P]
     L.mcb_debug_phase_cycles.argtypes = [P, C.c_int]
+    L.mcb_debug_warp_stats.argtypes = [P]
+    L.mcb_debug_modcheck.argtypes = [I64, P]
     for name in EXPORTS[3:]:
         getattr(L, name).restype = C.c_int
 

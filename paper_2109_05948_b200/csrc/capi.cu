@@ -44,24 +44,41 @@ int max_smem_optin() {
     return cache[d];
 }
 
+static void *grow_buffer(void **buf, size_t *cap, size_t bytes);
+
 void *workspace(size_t bytes) {
     static void *buf[64] = {nullptr};
     static size_t cap[64] = {0};
     const int d = cur_dev();
-    if (bytes <= cap[d]) return buf[d];
-    if (buf[d]) {
+    return grow_buffer(&buf[d], &cap[d], bytes);
+}
+
+// second independent scratch (kernels that need their own tables while the
+// first holds control words of the same call)
+void *workspace2(size_t bytes) {
+    static void *buf[64] = {nullptr};
+    static size_t cap[64] = {0};
+    const int d = cur_dev();
+    return grow_buffer(&buf[d], &cap[d], bytes);
+}
+
+static void *grow_buffer(void **bufp, size_t *capp, size_t bytes) {
+    void *&b = *bufp;
+    size_t &c = *capp;
+    if (bytes <= c) return b;
+    if (b) {
         cudaDeviceSynchronize();
-        cudaFree(buf[d]);
-        buf[d] = nullptr;
-        cap[d] = 0;
+        cudaFree(b);
+        b = nullptr;
+        c = 0;
     }
     size_t want = bytes + bytes / 4;
-    if (cudaMalloc(&buf[d], want) != cudaSuccess) {
+    if (cudaMalloc(&b, want) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
     }
-    cap[d] = want;
-    return buf[d];
+    c = want;
+    return b;
 }
 
 __global__ void stream_values_kernel(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out,

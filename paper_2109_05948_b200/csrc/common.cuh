@@ -23,6 +23,21 @@ __host__ __device__ __forceinline__ uint64_t stream_value(uint64_t key, uint64_t
 __device__ __forceinline__ bool below_is_zero(uint64_t key, uint64_t ctr, uint32_t n) {
     return (stream_value(key, ctr) % (uint64_t)n) == 0;
 }
+// x % s == 0 for any 32-bit s >= 1, exactly, without the 64-bit integer
+// division helper: two fp64 reciprocal steps.  q1 = x * (1/s) is within
+// 2^14/s + 1 of x/s, so r = x - q1 s (mod 2^64, exact as a signed value) has
+// |r| < 2^14 + 2s, exact in fp64; one rounded quotient more leaves |r2| <= s.
+// (checked against % by mcb_debug_modcheck)
+__device__ __forceinline__ bool mod_is_zero(uint64_t x, uint32_t s) {
+    const double inv = __drcp_rn((double)s);
+    const uint64_t q1 = __double2ull_rz(__dmul_rz(__ull2double_rz(x), inv));
+    const long long r = (long long)(x - q1 * (uint64_t)s);
+    const long long q2 = __double2ll_rn(__dmul_rn((double)r, inv));
+    long long r2 = r - q2 * (long long)s;
+    if (r2 < 0) r2 += s;
+    else if (r2 >= (long long)s) r2 -= s;
+    return r2 == 0;
+}
 __device__ __forceinline__ uint32_t u64_below32(uint64_t key, uint64_t ctr, uint32_t n) {
     return (uint32_t)(stream_value(key, ctr) % (uint64_t)n);
 }

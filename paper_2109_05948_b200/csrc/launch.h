@@ -13,6 +13,7 @@ int max_smem_optin();
 // Grow-only per-device scratch buffer (stream-ordered users must be done with
 // the previous contents; every entry point synchronises before returning).
 void *workspace(size_t bytes);
+void *workspace2(size_t bytes);
 
 struct TabucolArgs {
     int32_t *assigns;
@@ -30,7 +31,11 @@ struct TabucolArgs {
     uint32_t flags;
 };
 int tabucol_run(const TabucolArgs &a, cudaStream_t st);
+// warp-per-individual kernel (tabucol_warp.cu); -1 = shape outside its envelope
+int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *work_counter, int32_t *ovf_list,
+                        int32_t *ovf_count, int32_t *err_flag);
 int tabucol_phase_cycles(unsigned long long *out, int reset);
+int tabucol_warp_stats(unsigned long long *out);
 
 struct WvcpArgs {
     int32_t *assigns;

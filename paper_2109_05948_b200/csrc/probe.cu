@@ -56,3 +56,30 @@ extern "C" int mcb_probe_smem_bandwidth(double *gbs, double *ms) { return mcb::s
 extern "C" int mcb_debug_phase_cycles(unsigned long long *out, int reset) {
     return mcb::tabucol_phase_cycles(out, reset);
 }
+
+extern "C" int mcb_debug_warp_stats(unsigned long long *out) { return mcb::tabucol_warp_stats(out); }
+
+// Diagnostics: mod_is_zero (common.cuh) against the 64-bit % on `count`
+// pseudo-random (x, s) pairs, s drawn log-uniformly from [1, 2^32).
+__global__ void modcheck_kernel(int64_t count, unsigned long long *bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t x0 = mcb::stream_value(0x1234567ull, (uint64_t)i);
+        const uint64_t y = mcb::stream_value(0x89abcdefull, (uint64_t)i);
+        const int bits = 1 + (int)(y % 32);
+        uint32_t s = (uint32_t)((y >> 8) & ((bits >= 32) ? 0xFFFFFFFFull : ((1ull << bits) - 1)));
+        if (s == 0) s = 1;
+        // half the samples are exact multiples (the case the draws test for)
+        const uint64_t x = (i & 1) ? x0 : (x0 / s) * s;
+        if (mcb::mod_is_zero(x, s) != (x % s == 0)) atomicAdd(bad, 1ull);
+    }
+}
+extern "C" int mcb_debug_modcheck(int64_t count, unsigned long long *mismatches) {
+    unsigned long long *d = nullptr;
+    if (cudaMalloc(&d, sizeof(*d)) != cudaSuccess) return MCB_ERR_CUDA;
+    cudaMemset(d, 0, sizeof(*d));
+    modcheck_kernel<<<1184, 256>>>(count, d);
+    const cudaError_t e = cudaMemcpy(mismatches, d, sizeof(*d), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? MCB_OK : MCB_ERR_CUDA;
+}

@@ -1144,7 +1144,15 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
         P.const_indptr = 1;
     }
 
-    if (variant != 2) {
+    // fast path: one individual per warp (tabucol_warp.cu); overflowing
+    // individuals land on the same list the wide pass below consumes
+    bool warp_done = false;
+    if (variant == 0) {
+        rc = tabucol_warp_launch(A, st, ctl32 + 0, ctl32 + 64 + 256, ctl32 + 2, ctl32 + 3);
+        if (rc > 0) return rc;
+        warp_done = rc == MCB_OK;
+    }
+    if (variant != 2 && !warp_done) {
         P.work_counter = ctl32 + 0;
         P.ovf_count = ctl32 + 2;
         P.ovf_list = ctl32 + 64 + 256;
