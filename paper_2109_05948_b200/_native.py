@@ -70,7 +70,8 @@ def load(path=None):
     """Load the library (no device needed).  Raises if it is not built."""
     global _lib
     if _lib is None:
-        path = path or LIB
+        # MCB_LIB: an alternative build of the same ABI (A/B experiments, tools/)
+        path = path or os.environ.get("MCB_LIB") or LIB
         if not os.path.exists(path):
             raise NativeUnavailable(
                 f"{path} is missing: build it with `python -m paper_2109_05948_b200._build`")

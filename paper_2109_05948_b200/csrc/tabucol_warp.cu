@@ -23,18 +23,19 @@
 //     bit 6  TABU  (vertex, colour) is tabu this iteration
 //     bits 0-5     gamma = #neighbours of that colour (<= 63, else the
 //                  individual is re-run by the wide CTA kernel, tabucol.cu)
-//     padding colours 0xFF.
+//     padding colours 0x7F.
 // So a row's candidate moves are exactly its bytes < 0x40, and the row minimum
 // is a branch-free SIMD byte minimum.  Aspiration (a tabu move reaching a new
 // best: gamma < gva + best - conflicts) is only possible when gva + best -
 // conflicts > 0; then the row's tabu bytes are folded in (bytes ^ 0x40).
 //
 // Tabu expiry is exact and eager: every tabu entry (v, c, expiry) lives in a
-// register ring (lane = insertion % 32, register = insertion / 32 mod 32,
-// 1024 live entries); each ring row tracks its earliest expiry (lane-
-// distributed), and only rows whose earliest expiry has come are touched --
-// expired entries clear their TABU bit.  Re-tabu of a tabu pair invalidates
-// the older entry (last write wins, :366).
+// register ring ordered by age -- register row 0 holds the newest 32 entries
+// (lane = insertion % 32), the rows shift down once per 32 insertions -- so
+// every access uses a static register index; each iteration checks the rows
+// that still hold live entries (2 in steady state, 1024 entries at most) and
+// clears the TABU bit of entries expiring now.  Re-tabu of a tabu pair
+// invalidates the older entry (last write wins, :366).
 //
 // Per CTA: the adjacency as a bitset, row v = 32 lane chunks of CH bits (lane
 // L owns vertices [L*CH, L*CH+CH)), so the neighbour update of a move is one
@@ -42,6 +43,7 @@
 // bitset does not fit use the CSR (u16 indices, L2) variant.
 #include <algorithm>
 #include <climits>
+#include <utility>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -103,6 +105,13 @@ enum {
     WS_CY_EVENTS,
     WS_CY_TAIL,
     WS_CY_EXPIRE,
+    WS_CY_ROWMIN,
+    WS_CY_PREFIX,
+    WS_CY_LIST,
+    WS_CY_WALK,
+    WS_CY_P2,
+    WS_CY_DRAW,
+    WS_CY_LOCROW,
     WS_N = 32
 };
 #define WST(i, x) \
@@ -128,6 +137,28 @@ template <>
 struct ChunkT<32> {
     using T = uint32_t;
 };
+
+// explicit shared-window byte access with compile-time offsets (keeps the
+// unrolled neighbour update at one LDS/STS per byte, [reg + imm] addressing)
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+template <int OFF>
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF));
+    return v;
+}
+template <int OFF>
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0+%1], %2;" ::"r"(a), "n"(OFF), "r"(v) : "memory");
+}
+template <typename F, int... I>
+__device__ __forceinline__ void static_for_impl(F &&f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F &&f) {
+    static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 // 0x80 in every byte of x that is zero
 __device__ __forceinline__ uint32_t zero_flags(uint32_t z) {
@@ -190,6 +221,16 @@ __device__ __forceinline__ int row_min(const uint32_t (&x)[KW], uint32_t xorv) {
     const uint32_t mm = __vminu2(__vminu2(m0, m1), __vminu2(m2, m3));
     return (int)min(mm & 0xFFFFu, mm >> 16);
 }
+// gamma of the row's own colour: the only byte with bit 7 set
+template <int KW>
+__device__ __forceinline__ int own_gamma(const uint32_t (&x)[KW]) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int w = 0; w < KW; w++) acc |= x[w] & (((x[w] & 0x80808080u) >> 7) * GM);
+    acc |= acc >> 16;
+    acc |= acc >> 8;
+    return (int)(acc & GM);
+}
 // #bytes of the row equal to byte value b
 template <int KW>
 __device__ __forceinline__ int row_count(const uint32_t (&x)[KW], uint32_t b) {
@@ -200,17 +241,54 @@ __device__ __forceinline__ int row_count(const uint32_t (&x)[KW], uint32_t b) {
     return c;
 }
 // candidate bytes of word x (gamma value), every non-candidate 0xFF: plain
-// bytes < 0x40, plus (A > 0) tabu bytes of gamma < A (aspiration)
+// bytes < 0x40, plus (A > 0) tabu bytes of gamma < A (aspiration).  SIMD over
+// the 4 bytes: low + (64 - A) has bit 6 set iff low >= A (no carry out).
 __device__ __forceinline__ uint32_t cand_word(uint32_t x, int A) {
     uint32_t y = x | ((((x | (x << 1)) & 0x80808080u) >> 7) * 0xFFu);
     if (A > 0) {
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            const uint32_t b = (x >> (8 * e)) & 0xFFu;
-            if ((b & 0xC0u) == TABU && (int)(b & GM) < A) y = (y & ~(0xFFu << (8 * e))) | ((b & GM) << (8 * e));
-        }
+        const uint32_t low = x & 0x3F3F3F3Fu;
+        const uint32_t ge = (low + (uint32_t)(64 - A) * 0x01010101u) & 0x40404040u;
+        const uint32_t asp = x & ~(x >> 1) & ~ge & 0x40404040u;  // tabu, not own, gamma < A
+        const uint32_t full = (asp >> 6) * 0xFFu;
+        y = (y & ~full) | (low & full);
     }
     return y;
+}
+
+// tie events of one row entered with running minimum Pg (gamma space): the
+// candidates equal to the running minimum when scanned in colour order
+// (localsearch.py:340-350).  One lane, logical words read from shared memory.
+template <int KW>
+__device__ __forceinline__ int walk_words(const uint32_t (&w)[KW], int A, int Pg) {
+    uint32_t y[KW];
+    int wm[KW];
+#pragma unroll
+    for (int i = 0; i < KW; i++) {
+        y[i] = cand_word(w[i], A);
+        const uint32_t m2 = __vminu2(y[i] & 0x00FF00FFu, __byte_perm(y[i], 0, 0x4341));
+        wm[i] = (int)min(m2 & 0xFFFFu, m2 >> 16);
+    }
+    // candidates are <= 63 and non-candidates 0xFF, so a running minimum
+    // clamped to 0xFE is never lowered or tied by a non-candidate.  The
+    // running minimum entering word i is a short chain over word minima; the
+    // 4-byte chains of different words are independent.
+    int M = min(Pg, 0xFE), t[KW];
+#pragma unroll
+    for (int i = 0; i < KW; i++) {
+        // exclusive prefix minima of the 4 bytes, packed; events = equal bytes
+        const int c0 = M;
+        const int c1 = min(c0, (int)(y[i] & 0xFFu));
+        const int c2 = min(c1, (int)__byte_perm(y[i], 0, 0x4441));
+        const int c3 = min(c2, (int)__byte_perm(y[i], 0, 0x4442));
+        const uint32_t Cp = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+        t[i] = count_eq(y[i], Cp);
+        M = min(M, wm[i]);
+    }
+#pragma unroll
+    for (int d = 1; d < KW; d <<= 1)
+#pragma unroll
+        for (int i = 0; i + d < KW; i += 2 * d) t[i] += t[i + d];
+    return t[0];
 }
 
 template <int W>
@@ -231,27 +309,6 @@ __device__ __forceinline__ int seg_sum(int v) {
     return v;
 }
 
-// ring register access with a uniform row index (jump table; keeps the ring
-// in registers)
-#define TW_C4(b) TW_C(b) TW_C(b + 1) TW_C(b + 2) TW_C(b + 3)
-__device__ __forceinline__ uint32_t ring_get(const uint32_t (&r)[KE], int j) {
-    uint32_t x = 0;
-    switch (j) {
-#define TW_C(J) \
-    case J: x = r[J]; break;
-        TW_C4(0) TW_C4(4) TW_C4(8) TW_C4(12) TW_C4(16) TW_C4(20) TW_C4(24) TW_C4(28)
-#undef TW_C
-    }
-    return x;
-}
-__device__ __forceinline__ void ring_set(uint32_t (&r)[KE], int j, uint32_t x) {
-    switch (j) {
-#define TW_C(J) \
-    case J: r[J] = x; break;
-        TW_C4(0) TW_C4(4) TW_C4(8) TW_C4(12) TW_C4(16) TW_C4(20) TW_C4(24) TW_C4(28)
-#undef TW_C
-    }
-}
 // entry: [valid:1][v:10][c:7][expiry mod 2^14:14]
 __device__ __forceinline__ uint32_t ent_pack(int v, int c, uint32_t e) {
     return 0x80000000u | ((uint32_t)v << 21) | ((uint32_t)c << 14) | (e & 0x3FFFu);
@@ -263,19 +320,38 @@ __device__ __forceinline__ uint32_t ent_dist(uint32_t ent, uint32_t it) { return
 // ---------------------------------------------------------------------------
 // the kernel
 //   KV     = 16-byte vectors per gamma row (KP = 16 KV >= k)
-//   CH     = bitset chunk bits per lane (BITSET) -- n <= 32 CH
+//   CH     = bitset chunk bits per lane (BITSET): lane L owns vertices
+//            L + 32 q, q < CH  (n <= 32 CH)
+// Row u is stored rotated by g(u) words (g depends on u mod 32 only), so that
+// the 32 lanes of the neighbour update -- rows L + 32 q for one q -- hit
+// distinct banks.  Scans read whole rows (order-free); walks / locate / single
+// bytes translate colours with phys().
 // ---------------------------------------------------------------------------
+template <int KW>
+struct Swz {
+    static constexpr int G = (KW % 32 == 0) ? 32 : (KW % 16 == 0) ? 16 : (KW % 8 == 0) ? 8 : (KW % 4 == 0) ? 4 : (KW % 2 == 0) ? 2 : 1;
+    static constexpr int SH = G == 32 ? 0 : G == 16 ? 1 : G == 8 ? 2 : G == 4 ? 3 : G == 2 ? 4 : 5;
+    __device__ __forceinline__ static int g(int u) { return (u >> SH) & (G - 1); }
+    // physical word of logical word w in a row rotated by g
+    __device__ __forceinline__ static int pw(int w, int gg) {
+        const int p = w + gg;
+        return p >= KW ? p - KW : p;
+    }
+    __device__ __forceinline__ static int phys(int c, int gg) { return 4 * pw(c >> 2, gg) + (c & 3); }
+};
+
 template <int KV, int CH, bool BITSET>
 __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(WarpTabuParams P) {
     constexpr int KP = 16 * KV, KW = 4 * KV;
-    constexpr int SW = KW <= 4 ? 4 : KW <= 8 ? 8 : KW <= 16 ? 16 : 32;  // walk segment width
-    constexpr int RPP = 32 / SW;                                          // rows per walk pass
+    constexpr int RW = 2;  // conflicting rows per lane per scan round
     static_assert(KW <= 32, "k <= 128");
+    using S = Swz<KW>;
     using CT = typename ChunkT<BITSET ? CH : 32>::T;
 
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int n = P.n, k = P.k;
+    const unsigned lt_mask = (1u << lane) - 1u;
 
     // CTA-shared adjacency bitset (read-only afterwards; warps never sync again)
     if constexpr (BITSET) {
@@ -287,7 +363,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
     uint8_t *base = smem + P.bitset_bytes + (size_t)wid * P.warp_smem;
     uint8_t *gam = base;
     size_t off = (size_t)n * KP;
-    uint32_t *rmc = reinterpret_cast<uint32_t *>(base + off);  // per scanned row: (int16 delta) | count << 16
+    uint32_t *rmc = reinterpret_cast<uint32_t *>(base + off);  // compact list of scanned rows
     off += 4 * (size_t)n;
     uint16_t *clist = reinterpret_cast<uint16_t *>(base + off);
     off += (2 * (size_t)n + 15) & ~(size_t)15;
@@ -302,6 +378,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
     long long st[WS_N];
     if (stats)
         for (int i = 0; i < WS_N; i++) st[i] = 0;
+    const int g_lane = S::g(lane);  // rotation of every row this lane owns (u = lane + 32q)
 
     for (;;) {
         int wi = 0;
@@ -325,37 +402,45 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
             b_out[v] = c;
         }
         {
-            const uint32_t padw = (k & 3) ? (0xFFFFFFFFu << (8 * (k & 3))) : 0u;
+            // logical padding colours >= k are 0xFF; rows rotated by g(u)
             uint32_t *g32 = reinterpret_cast<uint32_t *>(gam);
+            // padding colours 0x7F: never a candidate (gamma 63 >= any A), and the
+            // own colour is the only byte of a row with bit 7 set
+            const uint32_t padw = (k & 3) ? (0x7F7F7F7Fu << (8 * (k & 3))) : 0u;
             for (int i = lane; i < n * KW; i += 32) {
-                const int w = i % KW;
-                g32[i] = (4 * w + 4 <= k) ? 0u : (4 * w >= k ? 0xFFFFFFFFu : padw);
+                const int u = i / KW, p = i - u * KW;
+                int w = p - S::g(u);
+                if (w < 0) w += KW;
+                g32[i] = (4 * w + 4 <= k) ? 0u : (4 * w >= k ? 0x7F7F7F7Fu : padw);
             }
         }
         __syncwarp();
-        // gamma[u][c] = #neighbours of u coloured c; lane-private rows
+        // gamma[u][c] = #neighbours of u coloured c; lane-private rows u = lane + 32j
         for (int u = lane; u < n; u += 32) {
             uint8_t *row = gam + (size_t)u * KP;
+            const int gu = S::g(u);
             if constexpr (BITSET) {
                 const CT *br = reinterpret_cast<const CT *>(smem + (size_t)u * 4 * CH);
                 for (int L = 0; L < 32; L++) {
                     uint32_t ch = br[L];
                     while (ch) {
-                        const int j = __ffs(ch) - 1;
+                        const int q = __ffs(ch) - 1;
                         ch &= ch - 1;
-                        const int c = asg[L * CH + j];
-                        const int x = row[c] + 1;
+                        const int c = asg[L + 32 * q];
+                        uint8_t *e = row + S::phys(c, gu);
+                        const int x = *e + 1;
                         if (x > (int)GM) bad = true;
-                        else row[c] = (uint8_t)x;
+                        else *e = (uint8_t)x;
                     }
                 }
             } else {
                 const uint32_t s0 = P.indptr32[u], s1 = P.indptr32[u + 1];
                 for (uint32_t idx = s0; idx < s1; idx++) {
                     const int c = asg[P.nbr16[idx]];
-                    const int x = row[c] + 1;
+                    uint8_t *e = row + S::phys(c, gu);
+                    const int x = *e + 1;
                     if (x > (int)GM) bad = true;
-                    else row[c] = (uint8_t)x;
+                    else *e = (uint8_t)x;
                 }
             }
         }
@@ -368,7 +453,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                 const int v = v0 + lane;
                 bool f = false;
                 if (v < n) {
-                    uint8_t *p = gam + (size_t)v * KP + asg[v];
+                    uint8_t *p = gam + (size_t)v * KP + S::phys(asg[v], S::g(v));
                     const int g = *p;
                     *p = (uint8_t)(g | OWN);
                     f = g > 0;
@@ -376,7 +461,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                 }
                 const unsigned bal = __ballot_sync(FULLM, f);
                 if (f) {
-                    const int pos = C + __popc(bal & ((1u << lane) - 1u));
+                    const int pos = C + __popc(bal & lt_mask);
                     clist[pos] = (uint16_t)v;
                     cpos[v] = (uint16_t)pos;
                 }
@@ -392,13 +477,11 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
 
         long long it = 0, nlog = 0, sum_c = 0, sum_deg = 0, diag = 0;
         unsigned long long ctr = 0;
-        // tabu ring (see header); rlive/rmin: live count and earliest expiry of
-        // ring row `lane`
+        // tabu ring (see header): rows [0, nrows) may hold live entries
         uint32_t ring[KE];
 #pragma unroll
         for (int j = 0; j < KE; j++) ring[j] = 0u;
-        int rlive = 0;
-        uint32_t rmin = 0;
+        int nrows = 0;
         uint32_t ins = 0;
 
         // ---------------- iterations (:320-405) ----------------
@@ -412,116 +495,102 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
 
                 // ---- tabu expiry: it < tabu[v,c] fails from it == expiry on
                 {
-                    unsigned due = __ballot_sync(FULLM, rlive > 0 && (int)(rmin - it32) <= 0);
-                    while (due) {
-                        const int j = __ffs(due) - 1;
-                        due &= due - 1;
-                        WST(WS_EXPIRE_ROWS, 1);
-                        const uint32_t e = ring_get(ring, j);
-                        const bool valid = (e >> 31) != 0u;
-                        const uint32_t dist = ent_dist(e, it32);
-                        const bool hit = valid && dist == 0u;
+                    int last = -1;
+#pragma unroll
+                    for (int j = 0; j < KE; j++) {
+                        if (j >= nrows) break;
+                        const uint32_t e = ring[j];
+                        const bool hit = (e >> 31) != 0u && ent_dist(e, it32) == 0u;
                         if (hit) {
                             const int v = (e >> 21) & 0x3FF, c = (e >> 14) & 0x7F;
-                            gam[(size_t)v * KP + c] &= (uint8_t)~TABU;
-                            ring_set(ring, j, 0u);
+                            gam[(size_t)v * KP + S::phys(c, S::g(v))] &= (uint8_t)~TABU;
                         }
-                        const bool still = valid && !hit;
-                        const int cnt = __popc(__ballot_sync(FULLM, still));
-                        const unsigned dmin = __reduce_min_sync(FULLM, still ? dist : 0xFFFFu);
-                        if (lane == j) {
-                            rlive = cnt;
-                            rmin = it32 + dmin;
-                        }
+                        ring[j] = hit ? 0u : e;
+                        if (__any_sync(FULLM, (ring[j] >> 31) != 0u)) last = j;
                     }
+                    WST(WS_EXPIRE_ROWS, nrows);
+                    nrows = last + 1;
                     __syncwarp();
                 }
                 WPH(WS_CY_EXPIRE);
 
-                // ---- scan, phase 1 (localsearch.py:328-350): row minima, one
-                // conflicting row per lane; running prefix-min over the rows in list
-                // order; exact walks of the rows that lower it.  Rows at or below
-                // the running minimum -- the only ones holding reservoir events --
-                // are appended to a compact list (rmc) for phase 2.
+                // ---- scan, phase 1 (localsearch.py:328-350): row minima of the
+                // conflicting rows, RW rows per lane per round (rows b0 + 32 h +
+                // lane, independent chains); running prefix-min over the rows in
+                // list order; in-lane walks of the rows that lower it.  Rows at or
+                // below the running minimum -- the only ones holding reservoir
+                // events -- are appended to a compact list (rmc) for phase 2.
                 int carry = TW_BIG, total = 0, ncl = 0;
                 const int nr = (C + 31) >> 5;
 #pragma unroll 1
-                for (int r = 0; r < nr; r++) {
-                    const int li = r * 32 + lane;
-                    int rm = TW_BIG, v = 0, gva = 0, A = 0;
-                    if (li < C) {
-                        v = clist[li];
-                        const uint8_t *grow = gam + (size_t)v * KP;
-                        const int a = asg[v];
-                        uint32_t x[KW];
-                        load_row<KV>(grow, x);
-                        gva = grow[a] & GM;
-                        A = gva + thr;
-                        int m = row_min<KW>(x, 0u);  // non-own, non-tabu (bytes < 0x40)
-                        if (A > 0) {
-                            // aspiration: tabu colours with gamma < A are admissible
-                            const int mt = row_min<KW>(x, TABU * 0x01010101u);
-                            if (mt < A) m = min(m, mt);
+                for (int b0 = 0; b0 < C; b0 += 32 * RW) {
+                    int rm[RW], v[RW], gva[RW], A[RW];
+#pragma unroll
+                    for (int h = 0; h < RW; h++) {
+                        const int li = b0 + 32 * h + lane;
+                        rm[h] = TW_BIG;
+                        v[h] = 0;
+                        gva[h] = 0;
+                        A[h] = 0;
+                        if (li < C) {
+                            v[h] = clist[li];
+                            uint32_t x[KW];
+                            load_row<KV>(gam + (size_t)v[h] * KP, x);
+                            gva[h] = own_gamma<KW>(x);
+                            A[h] = gva[h] + thr;
+                            int m = row_min<KW>(x, 0u);  // non-own, non-tabu (bytes < 0x40)
+                            if (A[h] > 0) {
+                                // aspiration: tabu colours with gamma < A are admissible
+                                const int mt = row_min<KW>(x, TABU * 0x01010101u);
+                                if (mt < A[h]) m = min(m, mt);
+                            }
+                            if (m < (int)TABU) rm[h] = m - gva[h];
                         }
-                        if (m < (int)TABU) rm = m - gva;
                     }
-                    if (stats) WST(WS_ASP_ROUNDS, __any_sync(FULLM, A > 0));
-                    // running minimum entering this row
-                    int incl = rm;
+                    if (stats) WST(WS_ASP_ROUNDS, __any_sync(FULLM, A[0] > 0));
+                    WPH(WS_CY_ROWMIN);
+                    // running minimum entering each row (RW interleaved scans)
+                    int in[RW];
+#pragma unroll
+                    for (int h = 0; h < RW; h++) in[h] = rm[h];
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
-                        const int t = __shfl_up_sync(FULLM, incl, o);
-                        if (lane >= o) incl = min(incl, t);
-                    }
-                    int Pl = __shfl_up_sync(FULLM, incl, 1);
-                    if (lane == 0) Pl = TW_BIG;
-                    Pl = min(Pl, carry);
-                    {
-                        const bool lst = rm < TW_BIG && rm <= Pl;
-                        const unsigned nb = __ballot_sync(FULLM, lst);
-                        if (lst)
-                            rmc[ncl + __popc(nb & ((1u << lane) - 1u))] =
-                                (uint32_t)li | ((uint32_t)(rm + 64) << 16) | (rm == Pl ? 1u << 24 : 0u);
-                        ncl += __popc(nb);
-                    }
-                    if (!prod) {
-                        // rows that lower the running minimum: exact in-row walks,
-                        // RPP rows per pass (lanes over words)
-                        unsigned low = __ballot_sync(FULLM, rm < Pl);
-                        while (low) {
-                            WST(WS_WALK_PASSES, 1);
-                            const int g = lane / SW, wl = lane % SW;
-                            unsigned tmp = low;
+                        int t[RW];
 #pragma unroll
-                            for (int q = 0; q < RPP - 1; q++)
-                                if (q < g) tmp &= tmp - 1;
-                            const int src = tmp ? __ffs(tmp) - 1 : -1;
-                            const int s = src < 0 ? 0 : src;
-                            const int wv = __shfl_sync(FULLM, v, s);
-                            const int wg = __shfl_sync(FULLM, gva, s);
-                            const int wA = __shfl_sync(FULLM, A, s);
-                            const int wP = __shfl_sync(FULLM, Pl, s);
-                            uint32_t x = 0xFFFFFFFFu;
-                            if (src >= 0 && wl < KW)
-                                x = cand_word(reinterpret_cast<const uint32_t *>(gam + (size_t)wv * KP)[wl], wA);
-                            const int um = (int)min_bytes(x);
-                            const int ex = seg_excl_min<SW>(um == 0xFF ? INT_MAX : um, wl);
-                            int cur = min(wP >= TW_BIG ? INT_MAX : wP + wg, ex);
-                            int t = 0;
+                        for (int h = 0; h < RW; h++) t[h] = __shfl_up_sync(FULLM, in[h], o);
+                        if (lane >= o) {
 #pragma unroll
-                            for (int e = 0; e < 4; e++) {
-                                const int b = (x >> (8 * e)) & 0xFF;
-                                if (b == 0xFF) continue;
-                                if (b < cur) cur = b;
-                                else if (b == cur) t++;
-                            }
-                            t = seg_sum<SW>(t);
-                            if (wl == 0 && src >= 0) total += t;
-#pragma unroll
-                            for (int q = 0; q < RPP; q++) low &= low - 1;
+                            for (int h = 0; h < RW; h++) in[h] = min(in[h], t[h]);
                         }
                     }
-                    carry = min(carry, __shfl_sync(FULLM, incl, 31));
+                    int Pl[RW];
+                    {
+                        int cc = carry;
+#pragma unroll
+                        for (int h = 0; h < RW; h++) {
+                            int ex = __shfl_up_sync(FULLM, in[h], 1);
+                            const int tot = __shfl_sync(FULLM, in[h], 31);
+                            if (lane == 0) ex = TW_BIG;
+                            Pl[h] = min(cc, ex);
+                            cc = min(cc, tot);
+                        }
+                        carry = cc;
+                    }
+                    WPH(WS_CY_PREFIX);
+                    // list entry: row | (rm + 64) << 16 | (entering minimum + 64, 127 =
+                    // none) << 23; rm == entering minimum marks a tie row, rm below it a
+                    // row that lowers it (walked in phase 2)
+#pragma unroll
+                    for (int h = 0; h < RW; h++) {
+                        const bool lst = rm[h] < TW_BIG && rm[h] <= Pl[h];
+                        const unsigned nb = __ballot_sync(FULLM, lst);
+                        if (lst)
+                            rmc[ncl + __popc(nb & lt_mask)] = (uint32_t)(b0 + 32 * h + lane) |
+                                                              ((uint32_t)(rm[h] + 64) << 16) |
+                                                              ((uint32_t)(Pl[h] >= TW_BIG ? 127 : Pl[h] + 64) << 23);
+                        ncl += __popc(nb);
+                    }
+                    WPH(WS_CY_LIST);
                 }
                 __syncwarp();
                 const int D = carry;
@@ -533,33 +602,59 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                 if (D < TW_BIG) {
                     // ---- phase 2: tie counts of the listed rows.  Rows equal to the
                     // running minimum contribute all their minimum candidates as tie
-                    // events; rows at D contribute T, the final group.
-                    int T = 0;
-                    for (int b0 = 0; b0 < ncl; b0 += 32) {
-                        const int i = b0 + lane;
-                        int cD = 0;
+                    // events; rows at D contribute T, the final group.  The first 32
+                    // list entries keep (row, exclusive D-count prefix) in registers.
+                    int T = 0, e_li = 0, e_cD = 0, e_ex = 0;
+                    for (int i0 = 0; i0 < ncl; i0 += 32) {
+                        const int i = i0 + lane;
+                        int cD = 0, li = 0;
                         if (i < ncl) {
                             const uint32_t e = rmc[i];
-                            const int li = (int)(e & 0xFFFFu), rm = (int)((e >> 16) & 0xFFu) - 64;
-                            const bool tie = (e >> 24) & 1u;
+                            li = (int)(e & 0xFFFFu);
+                            const int rmi = (int)((e >> 16) & 0x7Fu) - 64;
+                            const int pe = (int)(e >> 23);
+                            const bool tie = rmi == pe - 64, lower = rmi < pe - 64;
                             int cnt = 0;
-                            if (tie || rm == D) {
+                            if (tie || rmi == D || (lower && !prod)) {
+                                // the row in colour order (logical words)
                                 const int v = clist[li];
                                 const uint8_t *grow = gam + (size_t)v * KP;
+                                const int gvv = S::g(v);
                                 uint32_t x[KW];
-                                load_row<KV>(grow, x);
-                                const int gva = grow[asg[v]] & GM;
-                                const int m = rm + gva;
-                                cnt = row_count<KW>(x, (uint32_t)m);
-                                if (m < gva + thr) cnt += row_count<KW>(x, (uint32_t)m | TABU);
+#pragma unroll
+                                for (int q = 0; q < KW; q++) x[q] = reinterpret_cast<const uint32_t *>(grow)[S::pw(q, gvv)];
+                                const int gv = own_gamma<KW>(x);
+                                const int m = rmi + gv, A = gv + thr;
+                                if (tie || rmi == D) {
+                                    cnt = row_count<KW>(x, (uint32_t)m);
+                                    if (m < A) cnt += row_count<KW>(x, (uint32_t)m | TABU);
+                                }
+                                if (lower && !prod) {
+                                    // rows that lower the running minimum: exact walk
+                                    total += walk_words<KW>(x, A, pe == 127 ? INT_MAX : pe - 64 + gv);
+                                }
                             }
                             if (tie) total += cnt;
-                            if (rm == D) cD = cnt;
+                            if (rmi == D) cD = cnt;
                             rmc[i] = (uint32_t)li | ((uint32_t)cD << 16);
                         }
-                        T += __reduce_add_sync(FULLM, cD);
+                        if (i0 == 0) {
+                            int incl = cD;
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const int t = __shfl_up_sync(FULLM, incl, o);
+                                if (lane >= o) incl += t;
+                            }
+                            e_li = li;
+                            e_cD = cD;
+                            e_ex = incl - cD;
+                            T = __shfl_sync(FULLM, incl, 31);
+                        } else {
+                            T += __reduce_add_sync(FULLM, cD);
+                        }
                     }
                     const int tot = prod ? 0 : __reduce_add_sync(FULLM, total);
+                    WPH(WS_CY_P2);
                     // tenure draw (:363-365), issued early so it overlaps the reservoir
                     const long long nconf = conflicts + D;
                     uint32_t ll;
@@ -580,66 +675,100 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             sstar = 1 + (int)philox_below(key, ctr, (uint32_t)T);
                         }
                     }
-                    // ---- locate the sstar-th D-candidate in scan order
-                    int row_li = 0, need = sstar;
+                    WPH(WS_CY_DRAW);
+                    // ---- locate the sstar-th D-candidate in scan order: the row, then
+                    // (in the lane that owns it) the colour
+                    int src, need;
                     {
-                        int cum = 0;
-                        for (int b0 = 0; b0 < ncl; b0 += 32) {
-                            const int i = b0 + lane;
-                            int cc = 0, li = 0;
-                            if (i < ncl) {
-                                const uint32_t e = rmc[i];
-                                li = (int)(e & 0xFFFFu);
-                                cc = (int)(e >> 16);
-                            }
-                            int incl = cc;
+                        unsigned bm = __ballot_sync(FULLM, e_cD > 0 && e_ex < sstar && sstar <= e_ex + e_cD);
+                        if (bm) {
+                            src = __ffs(bm) - 1;
+                            need = sstar - e_ex;  // valid in lane src
+                        } else {
+                            // beyond the first 32 list entries (rare)
+                            int cum = 0;
+                            src = -1;
+                            for (int i0 = 0; i0 < ncl; i0 += 32) {
+                                const int i = i0 + lane;
+                                int cc = 0, li = 0;
+                                if (i < ncl) {
+                                    const uint32_t e = rmc[i];
+                                    li = (int)(e & 0xFFFFu);
+                                    cc = (int)(e >> 16);
+                                }
+                                int incl = cc;
 #pragma unroll
-                            for (int o = 1; o < 32; o <<= 1) {
-                                const int t = __shfl_up_sync(FULLM, incl, o);
-                                if (lane >= o) incl += t;
+                                for (int o = 1; o < 32; o <<= 1) {
+                                    const int t = __shfl_up_sync(FULLM, incl, o);
+                                    if (lane >= o) incl += t;
+                                }
+                                const int rt = __shfl_sync(FULLM, incl, 31);
+                                if (cum + rt >= sstar) {
+                                    const unsigned b2 = __ballot_sync(FULLM, cum + incl >= sstar);
+                                    src = __ffs(b2) - 1;
+                                    e_li = li;
+                                    need = sstar - cum - (incl - cc);
+                                    break;
+                                }
+                                cum += rt;
                             }
-                            const int rt = __shfl_sync(FULLM, incl, 31);
-                            if (cum + rt >= sstar) {
-                                const unsigned bm = __ballot_sync(FULLM, cum + incl >= sstar);
-                                const int src = __ffs(bm) - 1;
-                                row_li = __shfl_sync(FULLM, li, src);
-                                need = sstar - cum - __shfl_sync(FULLM, incl - cc, src);
-                                break;
-                            }
-                            cum += rt;
                         }
                     }
-                    const int v = clist[row_li];
+                    WPH(WS_CY_LOCROW);
+                    // in lane src: the row, its own colour and the need-th candidate
+                    // equal to D in colour order
+                    int v = 0, a = 0, b = -1, gva = 0;
+                    if (lane == src) {
+                        v = clist[e_li];
+                        const uint8_t *grow = gam + (size_t)v * KP;
+                        const int gvv = S::g(v);
+                        uint32_t w[KW];
+#pragma unroll
+                        for (int i = 0; i < KW; i++) w[i] = reinterpret_cast<const uint32_t *>(grow)[S::pw(i, gvv)];
+                        // own colour: the byte with bit 7
+                        int ow = 0;
+                        uint32_t owv = 0;
+#pragma unroll
+                        for (int i = 0; i < KW; i++) {
+                            const uint32_t hb = w[i] & 0x80808080u;
+                            if (hb) {
+                                ow = i;
+                                owv = hb;
+                            }
+                        }
+                        a = 4 * ow + ((__ffs(owv) - 1) >> 3);
+                        uint32_t wo = w[0];
+#pragma unroll
+                        for (int i = 1; i < KW; i++)
+                            if (i == ow) wo = w[i];
+                        gva = (wo >> (8 * (a & 3))) & GM;
+                        const int Dg_ = D + gva, A_ = gva + thr;
+                        const uint32_t M = (uint32_t)Dg_ * 0x01010101u;
+                        int rr = need;
+#pragma unroll
+                        for (int i = 0; i < KW; i++) {
+                            const uint32_t y = cand_word(w[i], A_);
+                            const uint32_t z = zero_flags(y ^ M);
+                            const int c = __popc(z);
+                            if (b < 0) {
+                                if (rr <= c) {
+                                    uint32_t zz = z;
+                                    for (int q = 1; q < rr; q++) zz &= zz - 1;
+                                    b = 4 * i + ((__ffs(zz) - 1) >> 3);
+                                }
+                                rr -= c;
+                            }
+                        }
+                    }
+                    v = __shfl_sync(FULLM, v, src);
+                    a = __shfl_sync(FULLM, a, src);
+                    b = __shfl_sync(FULLM, b, src);
+                    gva = __shfl_sync(FULLM, gva, src);
                     uint8_t *grow = gam + (size_t)v * KP;
-                    const int a = asg[v];
-                    const int gva = grow[a] & GM;
-                    const int A = gva + thr;
+                    const int gvv = S::g(v);
+                    const int pa = S::phys(a, gvv);
+                    const uint32_t ba = grow[pa];
                     Dg = D + gva;
-                    int b = -1;
-                    {
-                        uint32_t x = 0xFFFFFFFFu;
-                        int cc = 0;
-                        if (lane < KW) {
-                            x = cand_word(reinterpret_cast<const uint32_t *>(grow)[lane], A);
-                            cc = count_eq(x, (uint32_t)Dg * 0x01010101u);
-                        }
-                        int incl = cc;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int t = __shfl_up_sync(FULLM, incl, o);
-                            if (lane >= o) incl += t;
-                        }
-                        const unsigned bm = __ballot_sync(FULLM, incl >= need);
-                        const int src = bm ? __ffs(bm) - 1 : 0;
-                        int col = -1;
-                        if (lane == src && bm) {
-                            int rr = need - (incl - cc);
-#pragma unroll
-                            for (int e = 0; e < 4; e++)
-                                if ((int)((x >> (8 * e)) & 0xFF) == Dg && --rr == 0 && col < 0) col = 4 * lane + e;
-                        }
-                        b = __shfl_sync(FULLM, col, src);
-                    }
                     if (b < 0) {
                         bad = true;  // cannot happen; route to the wide kernel
                         break;
@@ -654,42 +783,40 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                         break;
                     }
                     const uint32_t e_new = it32 + (uint32_t)tt + 1u;
-                    const uint32_t ba = grow[a];
                     if (ba & TABU) {
                         // (v, a) is re-tabu'd while tabu: the older entry is void
                         WST(WS_SUPERSEDE, 1);
                         const uint32_t key_vc = ent_pack(v, a, 0) & 0xFFFFC000u;
-                        unsigned lv = __ballot_sync(FULLM, rlive > 0);
-                        while (lv) {
-                            const int j = __ffs(lv) - 1;
-                            lv &= lv - 1;
-                            const uint32_t e = ring_get(ring, j);
-                            const bool hit = (e & 0xFFFFC000u) == key_vc;
-                            const unsigned hb = __ballot_sync(FULLM, hit);
-                            if (hb) {
-                                if (hit) ring_set(ring, j, 0u);
-                                if (lane == j) rlive--;
-                                break;
-                            }
+#pragma unroll
+                        for (int j = 0; j < KE; j++) {
+                            if (j >= nrows) break;
+                            const bool hit = (ring[j] & 0xFFFFC000u) == key_vc;
+                            if (hit) ring[j] = 0u;
+                            if (__any_sync(FULLM, hit)) break;
                         }
                     }
                     {
-                        const int j = (int)((ins >> 5) % KE), L = (int)(ins & 31u);
-                        if (L == 0 && __shfl_sync(FULLM, rlive, j) > 0) {
-                            bad = true;  // a tabu entry outlived 1000 insertions
-                            break;
+                        // insert at (row 0, lane ins % 32); a full row 0 shifts the rows
+                        const int L = (int)(ins & 31u);
+                        if (L == 0 && ins != 0u) {
+                            if (__any_sync(FULLM, (ring[KE - 1] >> 31) != 0u)) {
+                                bad = true;  // > 1024 live tabu entries
+                                break;
+                            }
+#pragma unroll
+                            for (int j = KE - 1; j > 0; j--) ring[j] = ring[j - 1];
+                            ring[0] = 0u;
+                            nrows = min(nrows + 1, KE);
                         }
-                        if (lane == L) ring_set(ring, j, ent_pack(v, a, e_new));
-                        if (lane == j) {
-                            rmin = (rlive == 0 || (int)(e_new - rmin) < 0) ? e_new : rmin;
-                            rlive++;
-                        }
+                        if (lane == L) ring[0] = ent_pack(v, a, e_new);
+                        nrows = max(nrows, 1);
                         ins++;
                     }
                     if (lane == 0) {
                         asg[v] = (uint8_t)b;
-                        grow[a] = (uint8_t)((ba & GM) | TABU);
-                        grow[b] = (uint8_t)(grow[b] | OWN);
+                        grow[pa] = (uint8_t)((ba & GM) | TABU);
+                        const int pb = S::phys(b, gvv);
+                        grow[pb] = (uint8_t)(grow[pb] | OWN);
                         if (nlog < P.log_cap) {
                             const size_t o = (size_t)ind * P.log_cap + nlog;
                             P.log_v[o] = v;
@@ -729,56 +856,50 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                         Cn++;
                     };
                     if constexpr (BITSET) {
-                        uint32_t ch = reinterpret_cast<const CT *>(smem + (size_t)v * 4 * CH)[lane];
+                        // lane L: neighbours L + 32 q, all CH positions unrolled and
+                        // predicated; loads first, then stores (distinct rows)
+                        const uint32_t ch = reinterpret_cast<const CT *>(smem + (size_t)v * 4 * CH)[lane];
                         if (cnt_on) sum_deg += __reduce_add_sync(FULLM, __popc(ch));
-                        uint32_t evE = 0, evL = 0;
-                        uint8_t *ga = gam + a, *gb = gam + b;
-                        const int ubase = lane * CH;
-                        while (ch) {
-                            // up to 4 neighbours per pass: all loads in flight before
-                            // the stores (distinct rows, no aliasing)
-                            int jj[4];
-                            uint8_t *pa[4], *pb[4];
-                            uint32_t oa[4], ob[4];
-#pragma unroll
-                            for (int q = 0; q < 4; q++) {
-                                jj[q] = __ffs(ch) - 1;
-                                ch &= ch - 1;
-                                const int u = ubase + max(jj[q], 0);
-                                pa[q] = ga + (size_t)u * KP;
-                                pb[q] = gb + (size_t)u * KP;
-                            }
-#pragma unroll
-                            for (int q = 0; q < 4; q++)
-                                if (jj[q] >= 0) {
-                                    oa[q] = *pa[q];
-                                    ob[q] = *pb[q];
-                                }
-#pragma unroll
-                            for (int q = 0; q < 4; q++)
-                                if (jj[q] >= 0) {
-                                    *pa[q] = (uint8_t)(oa[q] - 1);
-                                    *pb[q] = (uint8_t)(ob[q] + 1);
-                                    ovf |= (ob[q] & GM) == GM;
-                                    evL |= ((oa[q] & 0xBFu) == 0x81u) ? 1u << jj[q] : 0u;
-                                    evE |= ((ob[q] & 0xBFu) == 0x80u) ? 1u << jj[q] : 0u;
-                                }
-                        }
+                        // rows u = lane + 32 q for every q < CH: rows >= n lie inside
+                        // this warp's region (host-checked) and are written back
+                        // unchanged (never neighbours)
+                        const uint32_t ra = smem_addr(gam) + (uint32_t)(lane * KP + S::phys(a, g_lane));
+                        const uint32_t rb = smem_addr(gam) + (uint32_t)(lane * KP + S::phys(b, g_lane));
+                        constexpr int QS = 32 * KP;
+                        uint32_t oa[CH], ob[CH];
+                        static_for<CH>([&](auto qc) {
+                            constexpr int q = decltype(qc)::value;
+                            oa[q] = lds8<q * QS>(ra);
+                            ob[q] = lds8<q * QS>(rb);
+                        });
+                        uint32_t evE = 0, evL = 0, ovm = 0;
+                        static_for<CH>([&](auto qc) {
+                            constexpr int q = decltype(qc)::value;
+                            const uint32_t nbq = (ch >> q) & 1u;
+                            const uint32_t na = oa[q] - nbq, nb = ob[q] + nbq;
+                            sts8<q * QS>(ra, na);
+                            sts8<q * QS>(rb, nb);
+                            // leave: own colour a, gamma 1 -> 0; enter: own b, 0 -> 1
+                            evL |= ((na & 0xBFu) == 0x80u) ? (nbq << q) : 0u;
+                            evE |= ((nb & 0xBFu) == 0x81u) ? (nbq << q) : 0u;
+                            ovm |= ((nb & GM) == 0u) ? (nbq << q) : 0u;  // 63 -> 64 wrapped
+                        });
+                        ovf = ovm != 0u;
                         __syncwarp();
                         WPH(WS_CY_UPDATE);
-                        unsigned lw = __ballot_sync(FULLM, (evE | evL) != 0u);
-                        while (lw) {
-                            const int L = __ffs(lw) - 1;
-                            lw &= lw - 1;
-                            const uint32_t E = __shfl_sync(FULLM, evE, L);
-                            uint32_t all = E | __shfl_sync(FULLM, evL, L);
-                            while (all) {
-                                const int j = __ffs(all) - 1;
-                                all &= all - 1;
-                                const int u = L * CH + j;
+                        // events in ascending vertex order u = L + 32 q: q-major
+                        uint32_t qs = __reduce_or_sync(FULLM, evE | evL);
+                        while (qs) {
+                            const int q = __ffs(qs) - 1;
+                            qs &= qs - 1;
+                            unsigned lm = __ballot_sync(FULLM, ((evE | evL) >> q) & 1u);
+                            const unsigned lE = __ballot_sync(FULLM, (evE >> q) & 1u);
+                            while (lm) {
+                                const int L = __ffs(lm) - 1;
+                                lm &= lm - 1;
                                 WST(WS_EVENTS, 1);
-                                if ((E >> j) & 1u) cl_append(u);
-                                else cl_remove(u);
+                                if ((lE >> L) & 1u) cl_append(L + 32 * q);
+                                else cl_remove(L + 32 * q);
                             }
                         }
                     } else {
@@ -790,7 +911,9 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             int u = 0;
                             if (j < s1) {
                                 u = P.nbr16[j];
-                                uint8_t *pa = gam + (size_t)u * KP + a, *pb = gam + (size_t)u * KP + b;
+                                const int gu = S::g(u);
+                                uint8_t *pa = gam + (size_t)u * KP + S::phys(a, gu);
+                                uint8_t *pb = gam + (size_t)u * KP + S::phys(b, gu);
                                 const uint32_t oa = *pa, ob = *pb;
                                 *pa = (uint8_t)(oa - 1);
                                 *pb = (uint8_t)(ob + 1);
@@ -877,13 +1000,17 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
     }
 }
 
-__global__ void tw_bitset_kernel(const int64_t *indptr, const int32_t *indices, int n, int row_bytes,
+// lane-interleaved bitset: row v = 32 chunks of CH bits, bit q of chunk L <->
+// vertex L + 32 q (bit index L*CH + q of the row)
+__global__ void tw_bitset_kernel(const int64_t *indptr, const int32_t *indices, int n, int ch,
                                  uint32_t *bits) {
+    const int row_words = ch;  // 32 * ch bits
     for (int v = blockIdx.x; v < n; v += gridDim.x) {
-        uint32_t *row = bits + (size_t)v * (row_bytes / 4);
+        uint32_t *row = bits + (size_t)v * row_words;
         for (int64_t i = indptr[v] + threadIdx.x; i < indptr[v + 1]; i += blockDim.x) {
             const int u = indices[i];
-            atomicOr(row + (u >> 5), 1u << (u & 31));
+            const int bit = (u & 31) * ch + (u >> 5);
+            atomicOr(row + (bit >> 5), 1u << (bit & 31));
         }
     }
 }
@@ -967,10 +1094,24 @@ static bool tw_plan(int n, int k, int64_t p, WarpPlan *pl) {
     }
     if (const char *e = getenv("MCB_WARPS")) w = std::max(1, std::min(w, atoi(e)));
     if (w < 1) return false;
+    if (use_ch) {
+        // the unrolled update touches rows lane + 32 q for all q < CH
+        const size_t need = (size_t)32 * use_ch * kp;
+        if (need > wb) {
+            const size_t wb2 = (need + 15) & ~(size_t)15;
+            const int w2 = (int)std::min<size_t>((cap - bb) / wb2, TW_MAX_WARPS);
+            if (w2 < 1) return false;
+            w = std::min(w, w2);
+            pl->warp_smem = wb2;
+        } else {
+            pl->warp_smem = wb;
+        }
+    } else {
+        pl->warp_smem = wb;
+    }
     pl->kv = kv;
     pl->ch = use_ch;
     pl->warps = w;
-    pl->warp_smem = wb;
     pl->bitset_bytes = use_ch ? bb : 0;
     const int64_t ctas = (p + w - 1) / w;
     pl->grid = (int)std::min<int64_t>(ctas, sms);
@@ -1012,7 +1153,7 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
     if (pl.ch) {
         if (cudaMemsetAsync(gbase, 0, pl.bitset_bytes, st) != cudaSuccess)
             return set_error(MCB_ERR_CUDA, "memset failed");
-        tw_bitset_kernel<<<std::min(n, 4 * num_sms()), 128, 0, st>>>(A.indptr, A.indices, n, 4 * pl.ch,
+        tw_bitset_kernel<<<std::min(n, 4 * num_sms()), 128, 0, st>>>(A.indptr, A.indices, n, pl.ch,
                                                                     reinterpret_cast<uint32_t *>(gbase));
         P.bitset = gbase;
     } else {
