@@ -344,6 +344,7 @@ template <int KV, int CH, bool BITSET>
 __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(WarpTabuParams P) {
     constexpr int KP = 16 * KV, KW = 4 * KV;
     constexpr int RW = 2;  // conflicting rows per lane per scan round
+    constexpr int SW = KW <= 4 ? 4 : KW <= 8 ? 8 : KW <= 16 ? 16 : 32;  // walk segment width
     static_assert(KW <= 32, "k <= 128");
     using S = Swz<KW>;
     using CT = typename ChunkT<BITSET ? CH : 32>::T;
@@ -536,7 +537,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             v[h] = clist[li];
                             uint32_t x[KW];
                             load_row<KV>(gam + (size_t)v[h] * KP, x);
-                            gva[h] = own_gamma<KW>(x);
+                            gva[h] = gam[(size_t)v[h] * KP + S::phys(asg[v[h]], S::g(v[h]))] & GM;
                             A[h] = gva[h] + thr;
                             int m = row_min<KW>(x, 0u);  // non-own, non-tabu (bytes < 0x40)
                             if (A[h] > 0) {
@@ -600,39 +601,33 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
 
                 int mv_v = -1, mv_a = 0, mv_b = 0, Dg = 0;
                 if (D < TW_BIG) {
-                    // ---- phase 2: tie counts of the listed rows.  Rows equal to the
-                    // running minimum contribute all their minimum candidates as tie
-                    // events; rows at D contribute T, the final group.  The first 32
-                    // list entries keep (row, exclusive D-count prefix) in registers.
+                    // ---- phase 2a: tie counts of the listed rows (one lane per entry).
+                    // Rows equal to the running minimum contribute all their minimum
+                    // candidates as tie events; rows at D contribute T, the final
+                    // group.  The first 32 entries keep (row, exclusive D-count
+                    // prefix) in registers for the locate.
                     int T = 0, e_li = 0, e_cD = 0, e_ex = 0;
                     for (int i0 = 0; i0 < ncl; i0 += 32) {
                         const int i = i0 + lane;
-                        int cD = 0, li = 0;
+                        int cD = 0, li = 0, v = 0, gv = 0, pe = 127;
+                        bool lower = false;
                         if (i < ncl) {
                             const uint32_t e = rmc[i];
                             li = (int)(e & 0xFFFFu);
                             const int rmi = (int)((e >> 16) & 0x7Fu) - 64;
-                            const int pe = (int)(e >> 23);
-                            const bool tie = rmi == pe - 64, lower = rmi < pe - 64;
+                            pe = (int)(e >> 23);
+                            const bool tie = rmi == pe - 64;
+                            lower = rmi < pe - 64;
+                            v = clist[li];
+                            const uint8_t *grow = gam + (size_t)v * KP;
+                            gv = grow[S::phys(asg[v], S::g(v))] & GM;
                             int cnt = 0;
-                            if (tie || rmi == D || (lower && !prod)) {
-                                // the row in colour order (logical words)
-                                const int v = clist[li];
-                                const uint8_t *grow = gam + (size_t)v * KP;
-                                const int gvv = S::g(v);
+                            if (tie || rmi == D) {
                                 uint32_t x[KW];
-#pragma unroll
-                                for (int q = 0; q < KW; q++) x[q] = reinterpret_cast<const uint32_t *>(grow)[S::pw(q, gvv)];
-                                const int gv = own_gamma<KW>(x);
-                                const int m = rmi + gv, A = gv + thr;
-                                if (tie || rmi == D) {
-                                    cnt = row_count<KW>(x, (uint32_t)m);
-                                    if (m < A) cnt += row_count<KW>(x, (uint32_t)m | TABU);
-                                }
-                                if (lower && !prod) {
-                                    // rows that lower the running minimum: exact walk
-                                    total += walk_words<KW>(x, A, pe == 127 ? INT_MAX : pe - 64 + gv);
-                                }
+                                load_row<KV>(grow, x);
+                                const int m = rmi + gv;
+                                cnt = row_count<KW>(x, (uint32_t)m);
+                                if (m < gv + thr) cnt += row_count<KW>(x, (uint32_t)m | TABU);
                             }
                             if (tie) total += cnt;
                             if (rmi == D) cD = cnt;
@@ -651,6 +646,42 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             T = __shfl_sync(FULLM, incl, 31);
                         } else {
                             T += __reduce_add_sync(FULLM, cD);
+                        }
+                        // ---- phase 2b: rows that lower the running minimum -- exact
+                        // walks, lanes over the row's words, 32/SW rows per pass
+                        unsigned low = prod ? 0u : __ballot_sync(FULLM, lower);
+                        while (low) {
+                            WST(WS_WALK_PASSES, 1);
+                            const int g = lane / SW, wl = lane % SW;
+                            unsigned tmp = low;
+#pragma unroll
+                            for (int q = 0; q < 32 / SW - 1; q++)
+                                if (q < g) tmp &= tmp - 1;
+                            const int src = tmp ? __ffs(tmp) - 1 : -1;
+                            const int s = max(src, 0);
+                            const int wv = __shfl_sync(FULLM, v, s);
+                            const int wg = __shfl_sync(FULLM, gv, s);
+                            const int wp = __shfl_sync(FULLM, pe, s);
+                            uint32_t y = 0xFFFFFFFFu;
+                            if (src >= 0 && wl < KW)
+                                y = cand_word(reinterpret_cast<const uint32_t *>(gam + (size_t)wv * KP)[S::pw(wl, S::g(wv))],
+                                              wg + thr);
+                            const uint32_t m2 = __vminu2(y & 0x00FF00FFu, __byte_perm(y, 0, 0x4341));
+                            const int um = (int)min(m2 & 0xFFFFu, m2 >> 16);
+                            const int ex = seg_excl_min<SW>(um, wl);
+                            // running minimum entering this word (clamped: never tied
+                            // or lowered by a non-candidate 0xFF), then the exclusive
+                            // prefix minima of its 4 bytes, packed; events = equal bytes
+                            const int c0 = min(min(wp == 127 ? INT_MAX : wp - 64 + wg, ex), 0xFE);
+                            const int c1 = min(c0, (int)(y & 0xFFu));
+                            const int c2 = min(c1, (int)__byte_perm(y, 0, 0x4441));
+                            const int c3 = min(c2, (int)__byte_perm(y, 0, 0x4442));
+                            const uint32_t Cp =
+                                __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+                            const int t = seg_sum<SW>(count_eq(y, Cp));
+                            if (wl == 0 && src >= 0) total += t;
+#pragma unroll
+                            for (int q = 0; q < 32 / SW; q++) low &= low - 1;
                         }
                     }
                     const int tot = prod ? 0 : __reduce_add_sync(FULLM, total);
@@ -676,18 +707,19 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                         }
                     }
                     WPH(WS_CY_DRAW);
-                    // ---- locate the sstar-th D-candidate in scan order: the row, then
-                    // (in the lane that owns it) the colour
-                    int src, need;
+                    // ---- locate the sstar-th D-candidate in scan order: the row ...
+                    int row_li, need;
                     {
-                        unsigned bm = __ballot_sync(FULLM, e_cD > 0 && e_ex < sstar && sstar <= e_ex + e_cD);
+                        const unsigned bm = __ballot_sync(FULLM, e_cD > 0 && e_ex < sstar && sstar <= e_ex + e_cD);
                         if (bm) {
-                            src = __ffs(bm) - 1;
-                            need = sstar - e_ex;  // valid in lane src
+                            const int src = __ffs(bm) - 1;
+                            row_li = __shfl_sync(FULLM, e_li, src);
+                            need = sstar - __shfl_sync(FULLM, e_ex, src);
                         } else {
                             // beyond the first 32 list entries (rare)
                             int cum = 0;
-                            src = -1;
+                            row_li = 0;
+                            need = 1;
                             for (int i0 = 0; i0 < ncl; i0 += 32) {
                                 const int i = i0 + lane;
                                 int cc = 0, li = 0;
@@ -705,9 +737,9 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                                 const int rt = __shfl_sync(FULLM, incl, 31);
                                 if (cum + rt >= sstar) {
                                     const unsigned b2 = __ballot_sync(FULLM, cum + incl >= sstar);
-                                    src = __ffs(b2) - 1;
-                                    e_li = li;
-                                    need = sstar - cum - (incl - cc);
+                                    const int src = __ffs(b2) - 1;
+                                    row_li = __shfl_sync(FULLM, li, src);
+                                    need = sstar - cum - __shfl_sync(FULLM, incl - cc, src);
                                     break;
                                 }
                                 cum += rt;
@@ -715,60 +747,39 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                         }
                     }
                     WPH(WS_CY_LOCROW);
-                    // in lane src: the row, its own colour and the need-th candidate
-                    // equal to D in colour order
-                    int v = 0, a = 0, b = -1, gva = 0;
-                    if (lane == src) {
-                        v = clist[e_li];
-                        const uint8_t *grow = gam + (size_t)v * KP;
-                        const int gvv = S::g(v);
-                        uint32_t w[KW];
-#pragma unroll
-                        for (int i = 0; i < KW; i++) w[i] = reinterpret_cast<const uint32_t *>(grow)[S::pw(i, gvv)];
-                        // own colour: the byte with bit 7
-                        int ow = 0;
-                        uint32_t owv = 0;
-#pragma unroll
-                        for (int i = 0; i < KW; i++) {
-                            const uint32_t hb = w[i] & 0x80808080u;
-                            if (hb) {
-                                ow = i;
-                                owv = hb;
-                            }
-                        }
-                        a = 4 * ow + ((__ffs(owv) - 1) >> 3);
-                        uint32_t wo = w[0];
-#pragma unroll
-                        for (int i = 1; i < KW; i++)
-                            if (i == ow) wo = w[i];
-                        gva = (wo >> (8 * (a & 3))) & GM;
-                        const int Dg_ = D + gva, A_ = gva + thr;
-                        const uint32_t M = (uint32_t)Dg_ * 0x01010101u;
-                        int rr = need;
-#pragma unroll
-                        for (int i = 0; i < KW; i++) {
-                            const uint32_t y = cand_word(w[i], A_);
-                            const uint32_t z = zero_flags(y ^ M);
-                            const int c = __popc(z);
-                            if (b < 0) {
-                                if (rr <= c) {
-                                    uint32_t zz = z;
-                                    for (int q = 1; q < rr; q++) zz &= zz - 1;
-                                    b = 4 * i + ((__ffs(zz) - 1) >> 3);
-                                }
-                                rr -= c;
-                            }
-                        }
-                    }
-                    v = __shfl_sync(FULLM, v, src);
-                    a = __shfl_sync(FULLM, a, src);
-                    b = __shfl_sync(FULLM, b, src);
-                    gva = __shfl_sync(FULLM, gva, src);
+                    // ... then the colour: lanes over the row's words in colour order
+                    const int v = clist[row_li];
                     uint8_t *grow = gam + (size_t)v * KP;
                     const int gvv = S::g(v);
+                    const int a = asg[v];
                     const int pa = S::phys(a, gvv);
                     const uint32_t ba = grow[pa];
+                    const int gva = ba & GM;
                     Dg = D + gva;
+                    int b = -1;
+                    {
+                        uint32_t xw = 0xFFFFFFFFu;
+                        int cc = 0;
+                        if (lane < KW) {
+                            xw = cand_word(reinterpret_cast<const uint32_t *>(grow)[S::pw(lane, gvv)], gva + thr);
+                            cc = count_eq(xw, (uint32_t)Dg * 0x01010101u);
+                        }
+                        int incl = cc;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int t = __shfl_up_sync(FULLM, incl, o);
+                            if (lane >= o) incl += t;
+                        }
+                        const unsigned bm = __ballot_sync(FULLM, incl >= need);
+                        const int src = bm ? __ffs(bm) - 1 : 0;
+                        int col = -1;
+                        if (lane == src && bm) {
+                            uint32_t z = zero_flags(xw ^ ((uint32_t)Dg * 0x01010101u));
+                            for (int r = need - (incl - cc); r > 1; r--) z &= z - 1;
+                            col = 4 * lane + ((__ffs(z) - 1) >> 3);
+                        }
+                        b = __shfl_sync(FULLM, col, src);
+                    }
                     if (b < 0) {
                         bad = true;  // cannot happen; route to the wide kernel
                         break;
