@@ -74,12 +74,19 @@ __global__ void modcheck_kernel(int64_t count, unsigned long long *bad) {
         if (mcb::mod_is_zero(x, s) != (x % s == 0)) atomicAdd(bad, 1ull);
     }
 }
+namespace mcb {
+int tabucol_warp_divcheck(int64_t count, unsigned long long *mismatches);
+}
 extern "C" int mcb_debug_modcheck(int64_t count, unsigned long long *mismatches) {
+    // fp64 path (any 32-bit s) and the small-divisor table path (s < 64)
+    unsigned long long m2 = 0;
+    if (int rc = mcb::tabucol_warp_divcheck(count, &m2)) return rc;
     unsigned long long *d = nullptr;
     if (cudaMalloc(&d, sizeof(*d)) != cudaSuccess) return MCB_ERR_CUDA;
     cudaMemset(d, 0, sizeof(*d));
     modcheck_kernel<<<1184, 256>>>(count, d);
     const cudaError_t e = cudaMemcpy(mismatches, d, sizeof(*d), cudaMemcpyDeviceToHost);
     cudaFree(d);
+    *mismatches += m2;
     return e == cudaSuccess ? MCB_OK : MCB_ERR_CUDA;
 }

@@ -86,6 +86,18 @@ struct WarpTabuParams {
 };
 
 __device__ unsigned long long g_wstats[32];
+// divisibility by s = o * 2^t, odd o < 64: x % s == 0  <=>  low t bits of x are
+// zero and (x >> t) * inv(o) <= floor((2^64 - 1) / o)  (inv = inverse mod 2^64)
+__device__ ulonglong2 g_divtab[32];
+__device__ __forceinline__ bool divisible(uint64_t x, uint32_t s) {
+    if (s < 64u) {
+        const int t = __ffs(s) - 1;
+        const uint32_t o = s >> t;
+        const ulonglong2 e = __ldg(&g_divtab[o >> 1]);
+        return (x & ((1ull << t) - 1ull)) == 0ull && (x >> t) * e.x <= e.y;
+    }
+    return mod_is_zero(x, s);
+}
 // stats slots (MCB_FLAG_WSTATS): event counters, then per-phase cycles
 enum {
     WS_IT,
@@ -578,17 +590,17 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                         carry = cc;
                     }
                     WPH(WS_CY_PREFIX);
-                    // list entry: row | (rm + 64) << 16 | (entering minimum + 64, 127 =
-                    // none) << 23; rm == entering minimum marks a tie row, rm below it a
-                    // row that lowers it (walked in phase 2)
+                    // list entry: v | (rm + 64) << 10 | (entering minimum + 64, 127 =
+                    // none) << 17 | gva << 24; rm == entering minimum marks a tie row,
+                    // rm below it a row that lowers it (walked in phase 2)
 #pragma unroll
                     for (int h = 0; h < RW; h++) {
                         const bool lst = rm[h] < TW_BIG && rm[h] <= Pl[h];
                         const unsigned nb = __ballot_sync(FULLM, lst);
                         if (lst)
-                            rmc[ncl + __popc(nb & lt_mask)] = (uint32_t)(b0 + 32 * h + lane) |
-                                                              ((uint32_t)(rm[h] + 64) << 16) |
-                                                              ((uint32_t)(Pl[h] >= TW_BIG ? 127 : Pl[h] + 64) << 23);
+                            rmc[ncl + __popc(nb & lt_mask)] = (uint32_t)v[h] | ((uint32_t)(rm[h] + 64) << 10) |
+                                                              ((uint32_t)(Pl[h] >= TW_BIG ? 127 : Pl[h] + 64) << 17) |
+                                                              ((uint32_t)gva[h] << 24);
                         ncl += __popc(nb);
                     }
                     WPH(WS_CY_LIST);
@@ -606,21 +618,20 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                     // candidates as tie events; rows at D contribute T, the final
                     // group.  The first 32 entries keep (row, exclusive D-count
                     // prefix) in registers for the locate.
-                    int T = 0, e_li = 0, e_cD = 0, e_ex = 0;
+                    int T = 0, e_v = 0, e_gv = 0, e_cD = 0, e_ex = 0;
                     for (int i0 = 0; i0 < ncl; i0 += 32) {
                         const int i = i0 + lane;
-                        int cD = 0, li = 0, v = 0, gv = 0, pe = 127;
+                        int cD = 0, v = 0, gv = 0, pe = 127;
                         bool lower = false;
                         if (i < ncl) {
                             const uint32_t e = rmc[i];
-                            li = (int)(e & 0xFFFFu);
-                            const int rmi = (int)((e >> 16) & 0x7Fu) - 64;
-                            pe = (int)(e >> 23);
+                            v = (int)(e & 0x3FFu);
+                            const int rmi = (int)((e >> 10) & 0x7Fu) - 64;
+                            pe = (int)((e >> 17) & 0x7Fu);
+                            gv = (int)(e >> 24);
                             const bool tie = rmi == pe - 64;
                             lower = rmi < pe - 64;
-                            v = clist[li];
                             const uint8_t *grow = gam + (size_t)v * KP;
-                            gv = grow[S::phys(asg[v], S::g(v))] & GM;
                             int cnt = 0;
                             if (tie || rmi == D) {
                                 uint32_t x[KW];
@@ -631,7 +642,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             }
                             if (tie) total += cnt;
                             if (rmi == D) cD = cnt;
-                            rmc[i] = (uint32_t)li | ((uint32_t)cD << 16);
+                            rmc[i] = (uint32_t)v | ((uint32_t)gv << 10) | ((uint32_t)cD << 16);
                         }
                         if (i0 == 0) {
                             int incl = cD;
@@ -640,7 +651,8 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                                 const int t = __shfl_up_sync(FULLM, incl, o);
                                 if (lane >= o) incl += t;
                             }
-                            e_li = li;
+                            e_v = v;
+                            e_gv = gv;
                             e_cD = cD;
                             e_ex = incl - cD;
                             T = __shfl_sync(FULLM, incl, 31);
@@ -699,7 +711,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             int smax = 1;
                             WST(WS_DRAW_ROUNDS, (T + 30) / 32);
                             for (int s = 2 + lane; s <= T; s += 32)
-                                if (mod_is_zero(stream_value(key, c0 + (unsigned long long)(s - 2)), (uint32_t)s))
+                                if (divisible(stream_value(key, c0 + (unsigned long long)(s - 2)), (uint32_t)s))
                                     smax = s;
                             sstar = __reduce_max_sync(FULLM, smax);
                         } else {
@@ -708,24 +720,26 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                     }
                     WPH(WS_CY_DRAW);
                     // ---- locate the sstar-th D-candidate in scan order: the row ...
-                    int row_li, need;
+                    int v, gva, need;
                     {
                         const unsigned bm = __ballot_sync(FULLM, e_cD > 0 && e_ex < sstar && sstar <= e_ex + e_cD);
                         if (bm) {
                             const int src = __ffs(bm) - 1;
-                            row_li = __shfl_sync(FULLM, e_li, src);
+                            v = __shfl_sync(FULLM, e_v, src);
+                            gva = __shfl_sync(FULLM, e_gv, src);
                             need = sstar - __shfl_sync(FULLM, e_ex, src);
                         } else {
                             // beyond the first 32 list entries (rare)
                             int cum = 0;
-                            row_li = 0;
+                            v = 0;
+                            gva = 0;
                             need = 1;
                             for (int i0 = 0; i0 < ncl; i0 += 32) {
                                 const int i = i0 + lane;
-                                int cc = 0, li = 0;
+                                int cc = 0;
+                                uint32_t e = 0;
                                 if (i < ncl) {
-                                    const uint32_t e = rmc[i];
-                                    li = (int)(e & 0xFFFFu);
+                                    e = rmc[i];
                                     cc = (int)(e >> 16);
                                 }
                                 int incl = cc;
@@ -738,7 +752,9 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                                 if (cum + rt >= sstar) {
                                     const unsigned b2 = __ballot_sync(FULLM, cum + incl >= sstar);
                                     const int src = __ffs(b2) - 1;
-                                    row_li = __shfl_sync(FULLM, li, src);
+                                    const uint32_t es = __shfl_sync(FULLM, e, src);
+                                    v = (int)(es & 0x3FFu);
+                                    gva = (int)((es >> 10) & 0x3Fu);
                                     need = sstar - cum - __shfl_sync(FULLM, incl - cc, src);
                                     break;
                                 }
@@ -748,13 +764,8 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                     }
                     WPH(WS_CY_LOCROW);
                     // ... then the colour: lanes over the row's words in colour order
-                    const int v = clist[row_li];
                     uint8_t *grow = gam + (size_t)v * KP;
                     const int gvv = S::g(v);
-                    const int a = asg[v];
-                    const int pa = S::phys(a, gvv);
-                    const uint32_t ba = grow[pa];
-                    const int gva = ba & GM;
                     Dg = D + gva;
                     int b = -1;
                     {
@@ -784,6 +795,9 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                         bad = true;  // cannot happen; route to the wide kernel
                         break;
                     }
+                    const int a = asg[v];
+                    const int pa = S::phys(a, gvv);
+                    const uint32_t ba = grow[pa];
                     WPH(WS_CY_SELECT);
                     // ---- move, tenure, tabu entry (:352-366)
                     conflicts = nconf;
@@ -883,17 +897,33 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             oa[q] = lds8<q * QS>(ra);
                             ob[q] = lds8<q * QS>(rb);
                         });
+                        // 4 slots per 32-bit word: SIMD +-1 and SIMD event / overflow
+                        // tests (bytes never borrow: a neighbour's gamma[u,a] >= 1)
                         uint32_t evE = 0, evL = 0, ovm = 0;
-                        static_for<CH>([&](auto qc) {
-                            constexpr int q = decltype(qc)::value;
-                            const uint32_t nbq = (ch >> q) & 1u;
-                            const uint32_t na = oa[q] - nbq, nb = ob[q] + nbq;
-                            sts8<q * QS>(ra, na);
-                            sts8<q * QS>(rb, nb);
-                            // leave: own colour a, gamma 1 -> 0; enter: own b, 0 -> 1
-                            evL |= ((na & 0xBFu) == 0x80u) ? (nbq << q) : 0u;
-                            evE |= ((nb & 0xBFu) == 0x81u) ? (nbq << q) : 0u;
-                            ovm |= ((nb & GM) == 0u) ? (nbq << q) : 0u;  // 63 -> 64 wrapped
+                        static_for<CH / 4>([&](auto gc) {
+                            constexpr int g0 = 4 * decltype(gc)::value;
+                            const uint32_t nbm = (((ch >> g0) & 0xFu) * 0x00204081u) & 0x01010101u;
+                            const uint32_t pa4 = __byte_perm(__byte_perm(oa[g0], oa[g0 + 1], 0x0040),
+                                                             __byte_perm(oa[g0 + 2], oa[g0 + 3], 0x0040), 0x5410);
+                            const uint32_t pb4 = __byte_perm(__byte_perm(ob[g0], ob[g0 + 1], 0x0040),
+                                                             __byte_perm(ob[g0 + 2], ob[g0 + 3], 0x0040), 0x5410);
+                            const uint32_t na4 = pa4 - nbm, nb4 = pb4 + nbm;
+                            sts8<(g0 + 0) * QS>(ra, na4);
+                            sts8<(g0 + 1) * QS>(ra, na4 >> 8);
+                            sts8<(g0 + 2) * QS>(ra, na4 >> 16);
+                            sts8<(g0 + 3) * QS>(ra, na4 >> 24);
+                            sts8<(g0 + 0) * QS>(rb, nb4);
+                            sts8<(g0 + 1) * QS>(rb, nb4 >> 8);
+                            sts8<(g0 + 2) * QS>(rb, nb4 >> 16);
+                            sts8<(g0 + 3) * QS>(rb, nb4 >> 24);
+                            const uint32_t nbh = nbm << 7;
+                            // leave: own colour a, gamma 1 -> 0; enter: own b, 0 -> 1;
+                            // overflow: gamma 63 -> 64 wrapped to 0
+                            const uint32_t zl = zero_flags((na4 & 0xBFBFBFBFu) ^ 0x80808080u) & nbh;
+                            const uint32_t ze = zero_flags((nb4 & 0xBFBFBFBFu) ^ 0x81818181u) & nbh;
+                            ovm |= zero_flags(nb4 & 0x3F3F3F3Fu) & nbh;
+                            evL |= ((((zl >> 7) * 0x00204081u) >> 21) & 0xFu) << g0;
+                            evE |= ((((ze >> 7) * 0x00204081u) >> 21) & 0xFu) << g0;
                         });
                         ovf = ovm != 0u;
                         __syncwarp();
@@ -1138,6 +1168,25 @@ static bool tw_plan(int n, int k, int64_t p, WarpPlan *pl) {
 // Launches the warp kernel; individuals it cannot finish (table overflow) are
 // appended to ovf_list for the wide CTA kernel.  Returns MCB_OK, or -1 when
 // the shape is outside the envelope (caller uses the CTA kernels).
+static int upload_divtab(cudaStream_t st) {
+    static bool done[64] = {false};
+    int d = 0;
+    cudaGetDevice(&d);
+    if (done[d & 63]) return MCB_OK;
+    ulonglong2 tab[32];
+    for (int i = 0; i < 32; i++) {
+        const uint64_t o = 2 * (uint64_t)i + 1;
+        uint64_t x = o;  // Newton: inverse of o modulo 2^64
+        for (int r = 0; r < 6; r++) x *= 2 - o * x;
+        tab[i] = make_ulonglong2(x, ~0ull / o);
+    }
+    if (cudaMemcpyToSymbolAsync(g_divtab, tab, sizeof(tab), 0, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "tabucol_warp: divisor table upload failed");
+    done[d & 63] = true;
+    return MCB_OK;
+}
+
 int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, int32_t *ovf_list,
                         int32_t *ovf_count, int32_t *err_flag) {
     if (A.flags & (MCB_FLAG_FORCE_WIDE | MCB_FLAG_FORCE_GLOBAL | MCB_FLAG_PROFILE)) return -1;
@@ -1150,6 +1199,7 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
     if (!tw_plan((int)A.n, (int)A.k, A.p, &pl)) return -1;
     KernT kern = pick_kernel(pl.kv, pl.ch);
     if (!kern) return -1;
+    if (int rc = upload_divtab(st)) return rc;
     const int n = (int)A.n, kp = 16 * pl.kv;
     const size_t smem = pl.bitset_bytes + (size_t)pl.warps * pl.warp_smem;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -1220,5 +1270,28 @@ int tabucol_warp_stats(unsigned long long *out) {
     if (cudaMemcpyFromSymbol(out, g_wstats, sizeof(unsigned long long) * 32) != cudaSuccess)
         return set_error(MCB_ERR_CUDA, "warp stats unavailable");
     return MCB_OK;
+}
+}  // namespace mcb
+
+namespace mcb {
+// Diagnostics: the table divisibility test against the 64-bit %, s in [1, 63]
+__global__ void divcheck_kernel(int64_t count, unsigned long long *bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t x0 = stream_value(0x5151ull, (uint64_t)i);
+        const uint32_t s = 1 + (uint32_t)(stream_value(0x7777ull, (uint64_t)i) % 63);
+        const uint64_t x = (i & 1) ? x0 : (x0 / s) * s;
+        if (divisible(x, s) != (x % s == 0)) atomicAdd(bad, 1ull);
+    }
+}
+int tabucol_warp_divcheck(int64_t count, unsigned long long *mismatches) {
+    if (int rc = upload_divtab(0)) return rc;
+    unsigned long long *d = nullptr;
+    if (cudaMalloc(&d, sizeof(*d)) != cudaSuccess) return MCB_ERR_CUDA;
+    cudaMemset(d, 0, sizeof(*d));
+    divcheck_kernel<<<1184, 256>>>(count, d);
+    const cudaError_t e = cudaMemcpy(mismatches, d, sizeof(*d), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? MCB_OK : MCB_ERR_CUDA;
 }
 }  // namespace mcb

@@ -18,13 +18,13 @@ def find(pat):
 
 
 marks = [("expire", "// ---- tabu expiry"), ("scan1", "// ---- scan, phase 1"),
-         ("phase2", "// ---- phase 2: tie counts"), ("draws", "// ---- reservoir: the T-1 draws"),
+         ("phase2", "// ---- phase 2a: tie counts"), ("walks", "// ---- phase 2b: rows that lower"), ("draws", "// tenure draw (:363-365)"),
          ("locate", "// ---- locate the sstar-th"), ("move", "// ---- move, tenure, tabu entry"),
          ("update", "// ---- gamma update over N(v)"), ("events", "// events in ascending vertex order"),
          ("best", "// ---- best (:387-390)"), ("tail", "// ---- scratch check every 1024"),
          ("end", "// ---------------- outputs")]
 marks = [(n, find(p)) for n, p in marks]
-hl = [("walk", "walk_row_impl"), ("cand_word", "__device__ __forceinline__ uint32_t cand_word"),
+hl = [("walk_words", "int walk_words("), ("cand_word", "__device__ __forceinline__ uint32_t cand_word"),
       ("row_min", "__device__ __forceinline__ int row_min("), ("row_count", "__device__ __forceinline__ int row_count("),
       ("count_eq", "__device__ __forceinline__ uint32_t zero_flags")]
 hl = sorted([(find(p), n) for n, p in hl])
