@@ -71,6 +71,9 @@ int mcb_debug_warp_stats(unsigned long long *out);
 /* Diagnostics: the exact fp64 divisibility test of the reservoir draws against
  * the 64-bit integer %, on `count` pseudo-random pairs; out: #mismatches. */
 int mcb_debug_modcheck(int64_t count, unsigned long long *mismatches);
+/* Diagnostics: which TabuCol kernel variant a call with (n, k, p) launches on
+ * the current device, as text (no launch). */
+int mcb_tabucol_describe(int64_t n, int64_t k, int64_t p, char *buf, int len);
 
 /* out[i] = stream_value(keys[i], ctrs[i]) (rng.py:56-59); device pointers. */
 int mcb_stream_values(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out, int64_t count,

@@ -28,7 +28,7 @@ EXPORTS = [
     "mcb_tabucol_batch", "mcb_tabucol_batch_host", "mcb_wvcp_batch", "mcb_wvcp_batch_host",
     "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_gpx_rows", "mcb_pairwise", "mcb_pairwise_host",
     "mcb_probe_smem_bandwidth", "mcb_debug_phase_cycles", "mcb_debug_warp_stats",
-    "mcb_debug_modcheck",
+    "mcb_debug_modcheck", "mcb_tabucol_describe",
 ]
 
 _lib = None
@@ -62,6 +62,7 @@ def _declare(L):
     L.mcb_debug_phase_cycles.argtypes = [P, C.c_int]
     L.mcb_debug_warp_stats.argtypes = [P]
     L.mcb_debug_modcheck.argtypes = [I64, P]
+    L.mcb_tabucol_describe.argtypes = [I64, I64, I64, C.c_char_p, C.c_int]
     for name in EXPORTS[3:]:
         getattr(L, name).restype = C.c_int
 

@@ -90,3 +90,10 @@ extern "C" int mcb_debug_modcheck(int64_t count, unsigned long long *mismatches)
     *mismatches += m2;
     return e == cudaSuccess ? MCB_OK : MCB_ERR_CUDA;
 }
+
+namespace mcb {
+int tabucol_warp_describe(int64_t n, int64_t k, int64_t p, char *buf, int len);
+}
+extern "C" int mcb_tabucol_describe(int64_t n, int64_t k, int64_t p, char *buf, int len) {
+    return mcb::tabucol_warp_describe(n, k, p, buf, len);
+}

@@ -1133,6 +1133,24 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     P.sm_ticket = ctl32 + 64;  // 256 per-SM counters
     uint8_t *tables = ws + tables_off;
 
+    // fast path: one individual per warp (tabucol_warp.cu); overflowing
+    // individuals land on the list the wide pass below consumes, and the wide
+    // pass is launched only when that list is not empty
+    bool warp_done = false;
+    if (variant == 0) {
+        rc = tabucol_warp_launch(A, st, ctl32 + 0, ctl32 + 64 + 256, ctl32 + 2, ctl32 + 3);
+        if (rc > 0) return rc;
+        warp_done = rc == MCB_OK;
+    }
+    if (warp_done) {
+        int32_t h[2] = {0, 0};  // [0] = overflowed individuals, [1] = error flag
+        if (cudaMemcpyAsync(h, ctl32 + 2, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return set_error(MCB_ERR_CUDA, "tabucol: kernel failed: %s", cudaGetErrorString(cudaGetLastError()));
+        if (h[1] == 1) return set_error(MCB_ERR_RANGE, "color id out of range [0, k)");
+        if (h[0] == 0) return MCB_OK;
+    }
+
     // CSR row offsets -> __constant__ (u32) when they fit
     P.const_indptr = 0;
     if (n + 1 <= TC_CONST_INDPTR && 2 * A.m < (int64_t)UINT32_MAX) {
@@ -1144,14 +1162,6 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
         P.const_indptr = 1;
     }
 
-    // fast path: one individual per warp (tabucol_warp.cu); overflowing
-    // individuals land on the same list the wide pass below consumes
-    bool warp_done = false;
-    if (variant == 0) {
-        rc = tabucol_warp_launch(A, st, ctl32 + 0, ctl32 + 64 + 256, ctl32 + 2, ctl32 + 3);
-        if (rc > 0) return rc;
-        warp_done = rc == MCB_OK;
-    }
     if (variant != 2 && !warp_done) {
         P.work_counter = ctl32 + 0;
         P.ovf_count = ctl32 + 2;

@@ -1295,3 +1295,18 @@ int tabucol_warp_divcheck(int64_t count, unsigned long long *mismatches) {
     return e == cudaSuccess ? MCB_OK : MCB_ERR_CUDA;
 }
 }  // namespace mcb
+
+namespace mcb {
+// The kernel variant tabucol_run would launch for (n, k, p), as text.
+int tabucol_warp_describe(int64_t n, int64_t k, int64_t p, char *buf, int len) {
+    WarpPlan pl;
+    if (!tw_plan((int)n, (int)k, p, &pl)) {
+        snprintf(buf, len, "tabucol_kernel (CTA per individual; shape outside the warp kernel)");
+        return MCB_OK;
+    }
+    snprintf(buf, len, "tabucol_warp_kernel<KV=%d,%s> %d warps/CTA x %d CTAs, %zu B smem/individual", pl.kv,
+             pl.ch ? (pl.ch == 8 ? "bitset CH=8" : pl.ch == 16 ? "bitset CH=16" : "bitset CH=32") : "csr",
+             pl.warps, pl.grid, pl.warp_smem);
+    return MCB_OK;
+}
+}  // namespace mcb
