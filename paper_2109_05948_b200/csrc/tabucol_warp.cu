@@ -303,6 +303,25 @@ __device__ __forceinline__ int walk_words(const uint32_t (&w)[KW], int A, int Pg
     return t[0];
 }
 
+// exclusive prefix sum over lanes of small values v in [0, 2^BITS): one
+// ballot per bit plane, then popcounts (one VOTE + POPC level instead of a
+// log-step shuffle scan)
+template <int BITS>
+__device__ __forceinline__ int excl_sum_small(int v, unsigned lt) {
+    int s = 0;
+#pragma unroll
+    for (int b = 0; b < BITS; b++) s += __popc(__ballot_sync(0xffffffffu, (v >> b) & 1) & lt) << b;
+    return s;
+}
+// sum over the lanes of a mask, values in [0, 2^BITS)
+template <int BITS>
+__device__ __forceinline__ int masked_sum_small(int v, unsigned m) {
+    int s = 0;
+#pragma unroll
+    for (int b = 0; b < BITS; b++) s += __popc(__ballot_sync(0xffffffffu, (v >> b) & 1) & m) << b;
+    return s;
+}
+
 template <int W>
 __device__ __forceinline__ int seg_excl_min(int v, int li) {
     int incl = v;
@@ -619,81 +638,121 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                     // group.  The first 32 entries keep (row, exclusive D-count
                     // prefix) in registers for the locate.
                     int T = 0, e_v = 0, e_gv = 0, e_cD = 0, e_ex = 0;
-                    for (int i0 = 0; i0 < ncl; i0 += 32) {
-                        const int i = i0 + lane;
-                        int cD = 0, v = 0, gv = 0, pe = 127;
-                        bool lower = false;
-                        if (i < ncl) {
-                            const uint32_t e = rmc[i];
-                            v = (int)(e & 0x3FFu);
-                            const int rmi = (int)((e >> 10) & 0x7Fu) - 64;
-                            pe = (int)((e >> 17) & 0x7Fu);
-                            gv = (int)(e >> 24);
-                            const bool tie = rmi == pe - 64;
-                            lower = rmi < pe - 64;
-                            const uint8_t *grow = gam + (size_t)v * KP;
-                            int cnt = 0;
-                            if (tie || rmi == D) {
-                                uint32_t x[KW];
-                                load_row<KV>(grow, x);
-                                const int m = rmi + gv;
-                                cnt = row_count<KW>(x, (uint32_t)m);
-                                if (m < gv + thr) cnt += row_count<KW>(x, (uint32_t)m | TABU);
-                            }
-                            if (tie) total += cnt;
-                            if (rmi == D) cD = cnt;
-                            rmc[i] = (uint32_t)v | ((uint32_t)gv << 10) | ((uint32_t)cD << 16);
-                        }
-                        if (i0 == 0) {
-                            int incl = cD;
+                    // one walk pass over up to 32/SW lowering rows (bit mask `low` of
+                    // list lanes); returns this lane's share of the tie events
+                    auto walk_pass = [&](unsigned low, int v, int gv, int pe) -> int {
+                        const int g = lane / SW, wl = lane % SW;
+                        unsigned tmp = low;
 #pragma unroll
-                            for (int o = 1; o < 32; o <<= 1) {
-                                const int t = __shfl_up_sync(FULLM, incl, o);
-                                if (lane >= o) incl += t;
-                            }
-                            e_v = v;
-                            e_gv = gv;
-                            e_cD = cD;
-                            e_ex = incl - cD;
-                            T = __shfl_sync(FULLM, incl, 31);
-                        } else {
-                            T += __reduce_add_sync(FULLM, cD);
-                        }
-                        // ---- phase 2b: rows that lower the running minimum -- exact
-                        // walks, lanes over the row's words, 32/SW rows per pass
+                        for (int q = 0; q < 32 / SW - 1; q++)
+                            if (q < g) tmp &= tmp - 1;
+                        const int src = tmp ? __ffs(tmp) - 1 : -1;
+                        const int s = max(src, 0);
+                        const int wv = __shfl_sync(FULLM, v, s);
+                        const int wg = __shfl_sync(FULLM, gv, s);
+                        const int wp = __shfl_sync(FULLM, pe, s);
+                        uint32_t y = 0xFFFFFFFFu;
+                        if (src >= 0 && wl < KW)
+                            y = cand_word(reinterpret_cast<const uint32_t *>(gam + (size_t)wv * KP)[S::pw(wl, S::g(wv))],
+                                          wg + thr);
+                        const uint32_t m2 = __vminu2(y & 0x00FF00FFu, __byte_perm(y, 0, 0x4341));
+                        const int um = (int)min(m2 & 0xFFFFu, m2 >> 16);
+                        const int ex = seg_excl_min<SW>(um, wl);
+                        // running minimum entering this word (clamped: never tied or
+                        // lowered by a non-candidate 0xFF), then the exclusive prefix
+                        // minima of its 4 bytes, packed; events = equal bytes
+                        const int c0 = min(min(wp == 127 ? INT_MAX : wp - 64 + wg, ex), 0xFE);
+                        const int c1 = min(c0, (int)(y & 0xFFu));
+                        const int c2 = min(c1, (int)__byte_perm(y, 0, 0x4441));
+                        const int c3 = min(c2, (int)__byte_perm(y, 0, 0x4442));
+                        const uint32_t Cp = __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+                        const unsigned segm = (SW == 32 ? 0xffffffffu : ((1u << SW) - 1u)) << (lane & ~(SW - 1));
+                        const int t = masked_sum_small<3>(count_eq(y, Cp), segm);
+                        return (wl == 0 && src >= 0) ? t : 0;
+                    };
+                    if (ncl <= 32) {
+                        // common case, straight-line: the tie counts (lane = entry) and
+                        // the first walk pass are independent and interleave
+                        const bool val = lane < ncl;
+                        const uint32_t e = rmc[val ? lane : 0];
+                        const int v = (int)(e & 0x3FFu);
+                        const int rmi = (int)((e >> 10) & 0x7Fu) - 64;
+                        const int pe = (int)((e >> 17) & 0x7Fu);
+                        const int gv = (int)(e >> 24);
+                        const bool tie = val && rmi == pe - 64, lower = val && rmi < pe - 64;
+                        const bool atD = val && rmi == D;
+                        uint32_t x[KW];
+                        load_row<KV>(gam + (size_t)v * KP, x);
+                        const int m = rmi + gv;
+                        int cnt = row_count<KW>(x, (uint32_t)m);
+                        if (m < gv + thr) cnt += row_count<KW>(x, (uint32_t)m | TABU);
                         unsigned low = prod ? 0u : __ballot_sync(FULLM, lower);
-                        while (low) {
+                        if (low) {
                             WST(WS_WALK_PASSES, 1);
-                            const int g = lane / SW, wl = lane % SW;
-                            unsigned tmp = low;
-#pragma unroll
-                            for (int q = 0; q < 32 / SW - 1; q++)
-                                if (q < g) tmp &= tmp - 1;
-                            const int src = tmp ? __ffs(tmp) - 1 : -1;
-                            const int s = max(src, 0);
-                            const int wv = __shfl_sync(FULLM, v, s);
-                            const int wg = __shfl_sync(FULLM, gv, s);
-                            const int wp = __shfl_sync(FULLM, pe, s);
-                            uint32_t y = 0xFFFFFFFFu;
-                            if (src >= 0 && wl < KW)
-                                y = cand_word(reinterpret_cast<const uint32_t *>(gam + (size_t)wv * KP)[S::pw(wl, S::g(wv))],
-                                              wg + thr);
-                            const uint32_t m2 = __vminu2(y & 0x00FF00FFu, __byte_perm(y, 0, 0x4341));
-                            const int um = (int)min(m2 & 0xFFFFu, m2 >> 16);
-                            const int ex = seg_excl_min<SW>(um, wl);
-                            // running minimum entering this word (clamped: never tied
-                            // or lowered by a non-candidate 0xFF), then the exclusive
-                            // prefix minima of its 4 bytes, packed; events = equal bytes
-                            const int c0 = min(min(wp == 127 ? INT_MAX : wp - 64 + wg, ex), 0xFE);
-                            const int c1 = min(c0, (int)(y & 0xFFu));
-                            const int c2 = min(c1, (int)__byte_perm(y, 0, 0x4441));
-                            const int c3 = min(c2, (int)__byte_perm(y, 0, 0x4442));
-                            const uint32_t Cp =
-                                __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
-                            const int t = seg_sum<SW>(count_eq(y, Cp));
-                            if (wl == 0 && src >= 0) total += t;
+                            total += walk_pass(low, v, gv, pe);
 #pragma unroll
                             for (int q = 0; q < 32 / SW; q++) low &= low - 1;
+                        }
+                        if (tie) total += cnt;
+                        const int cD = atD ? cnt : 0;
+                        e_v = v;
+                        e_gv = gv;
+                        e_cD = cD;
+                        e_ex = excl_sum_small<8>(cD, lt_mask);
+                        T = __reduce_add_sync(FULLM, cD);
+                        while (low) {
+                            WST(WS_WALK_PASSES, 1);
+                            total += walk_pass(low, v, gv, pe);
+#pragma unroll
+                            for (int q = 0; q < 32 / SW; q++) low &= low - 1;
+                        }
+                    } else {
+                        for (int i0 = 0; i0 < ncl; i0 += 32) {
+                            const int i = i0 + lane;
+                            int cD = 0, v = 0, gv = 0, pe = 127;
+                            bool lower = false;
+                            if (i < ncl) {
+                                const uint32_t e = rmc[i];
+                                v = (int)(e & 0x3FFu);
+                                const int rmi = (int)((e >> 10) & 0x7Fu) - 64;
+                                pe = (int)((e >> 17) & 0x7Fu);
+                                gv = (int)(e >> 24);
+                                const bool tie = rmi == pe - 64;
+                                lower = rmi < pe - 64;
+                                int cnt = 0;
+                                if (tie || rmi == D) {
+                                    uint32_t x[KW];
+                                    load_row<KV>(gam + (size_t)v * KP, x);
+                                    const int m = rmi + gv;
+                                    cnt = row_count<KW>(x, (uint32_t)m);
+                                    if (m < gv + thr) cnt += row_count<KW>(x, (uint32_t)m | TABU);
+                                }
+                                if (tie) total += cnt;
+                                if (rmi == D) cD = cnt;
+                                rmc[i] = (uint32_t)v | ((uint32_t)gv << 10) | ((uint32_t)cD << 16);
+                            }
+                            if (i0 == 0) {
+                                int incl = cD;
+#pragma unroll
+                                for (int o = 1; o < 32; o <<= 1) {
+                                    const int t = __shfl_up_sync(FULLM, incl, o);
+                                    if (lane >= o) incl += t;
+                                }
+                                e_v = v;
+                                e_gv = gv;
+                                e_cD = cD;
+                                e_ex = incl - cD;
+                                T = __shfl_sync(FULLM, incl, 31);
+                            } else {
+                                T += __reduce_add_sync(FULLM, cD);
+                            }
+                            unsigned low = prod ? 0u : __ballot_sync(FULLM, lower);
+                            while (low) {
+                                WST(WS_WALK_PASSES, 1);
+                                total += walk_pass(low, v, gv, pe);
+#pragma unroll
+                                for (int q = 0; q < 32 / SW; q++) low &= low - 1;
+                            }
                         }
                     }
                     const int tot = prod ? 0 : __reduce_add_sync(FULLM, total);
@@ -775,12 +834,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             xw = cand_word(reinterpret_cast<const uint32_t *>(grow)[S::pw(lane, gvv)], gva + thr);
                             cc = count_eq(xw, (uint32_t)Dg * 0x01010101u);
                         }
-                        int incl = cc;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int t = __shfl_up_sync(FULLM, incl, o);
-                            if (lane >= o) incl += t;
-                        }
+                        const int incl = excl_sum_small<3>(cc, lt_mask) + cc;
                         const unsigned bm = __ballot_sync(FULLM, incl >= need);
                         const int src = bm ? __ffs(bm) - 1 : 0;
                         int col = -1;
