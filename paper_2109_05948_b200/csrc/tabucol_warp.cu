@@ -82,7 +82,7 @@ struct WarpTabuParams {
     int32_t *ovf_list, *ovf_count, *err_flag;
     uint32_t flags;
     int warp_smem;     // bytes per warp region
-    int bitset_bytes;  // bytes of the CTA-shared bitset (0 for CSR)
+    int bitset_bytes;  // bytes of the CTA-shared bitset copy (0: rows read from L2)
 };
 
 __device__ unsigned long long g_wstats[32];
@@ -386,7 +386,10 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
     const unsigned lt_mask = (1u << lane) - 1u;
 
     // CTA-shared adjacency bitset (read-only afterwards; warps never sync again)
-    if constexpr (BITSET) {
+    // bitset rows: a CTA-shared copy, or straight from L2 (the update's row is
+    // loaded as soon as the moving vertex is known, ~600 cycles before use)
+    const uint8_t *brows = P.bitset_bytes ? smem : P.bitset;
+    if (BITSET && P.bitset_bytes) {
         const uint4 *src = reinterpret_cast<const uint4 *>(P.bitset);
         uint4 *dst = reinterpret_cast<uint4 *>(smem);
         for (int i = threadIdx.x; i < P.bitset_bytes / 16; i += blockDim.x) dst[i] = src[i];
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
             uint8_t *row = gam + (size_t)u * KP;
             const int gu = S::g(u);
             if constexpr (BITSET) {
-                const CT *br = reinterpret_cast<const CT *>(smem + (size_t)u * 4 * CH);
+                const CT *br = reinterpret_cast<const CT *>(brows + (size_t)u * 4 * CH);
                 for (int L = 0; L < 32; L++) {
                     uint32_t ch = br[L];
                     while (ch) {
@@ -631,6 +634,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                 if (cnt_on) sum_c += C;
 
                 int mv_v = -1, mv_a = 0, mv_b = 0, Dg = 0;
+                uint32_t ch_pref = 0;
                 if (D < TW_BIG) {
                     // ---- phase 2a: tie counts of the listed rows (one lane per entry).
                     // Rows equal to the running minimum contribute all their minimum
@@ -822,6 +826,11 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                         }
                     }
                     WPH(WS_CY_LOCROW);
+                    // the moving vertex is known: fetch its adjacency chunk now
+                    if constexpr (BITSET) {
+                        const CT *br = reinterpret_cast<const CT *>(brows + (size_t)v * 4 * CH) + lane;
+                        ch_pref = P.bitset_bytes ? (uint32_t)*br : (uint32_t)__ldg(br);
+                    }
                     // ... then the colour: lanes over the row's words in colour order
                     uint8_t *grow = gam + (size_t)v * KP;
                     const int gvv = S::g(v);
@@ -937,7 +946,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                     if constexpr (BITSET) {
                         // lane L: neighbours L + 32 q, all CH positions unrolled and
                         // predicated; loads first, then stores (distinct rows)
-                        const uint32_t ch = reinterpret_cast<const CT *>(smem + (size_t)v * 4 * CH)[lane];
+                        const uint32_t ch = ch_pref;
                         if (cnt_on) sum_deg += __reduce_add_sync(FULLM, __popc(ch));
                         // rows u = lane + 32 q for every q < CH: rows >= n lie inside
                         // this warp's region (host-checked) and are written back
@@ -1145,7 +1154,7 @@ static KernT pick_kernel(int kv, int ch) {
 struct WarpPlan {
     int kv, ch;  // ch = 0: CSR
     int warps, grid;
-    size_t warp_smem, bitset_bytes;
+    size_t warp_smem, bitset_bytes, bitset_global;
 };
 
 static size_t tw_warp_bytes(int n, int kp) {
@@ -1175,7 +1184,11 @@ static bool tw_plan(int n, int k, int64_t p, WarpPlan *pl) {
     const size_t bb = ((size_t)n * 4 * ch + 15) & ~(size_t)15;
     // warps wanted per SM: enough to cover p, at most TW_MAX_WARPS
     const int want = (int)std::min<int64_t>(TW_MAX_WARPS, (p + sms - 1) / sms);
-    int w_bits = cap > bb ? (int)std::min<size_t>((cap - bb) / wb, TW_MAX_WARPS) : 0;
+    // bitset rows from L2 by default (all of shared memory for individuals);
+    // MCB_WARP_BITSET_SMEM=1 keeps a CTA-shared copy (A/B)
+    const bool bsm = getenv("MCB_WARP_BITSET_SMEM") != nullptr;
+    const size_t bb_smem = bsm ? bb : 0;
+    int w_bits = cap > bb_smem ? (int)std::min<size_t>((cap - bb_smem) / wb, TW_MAX_WARPS) : 0;
     int w_csr = (int)std::min<size_t>(cap / wb, TW_MAX_WARPS);
     if (getenv("MCB_WARP_CSR")) w_bits = 0;
     const char *mode = getenv("MCB_WARP_MODE");  // A/B: force "bits" or "csr"
@@ -1200,7 +1213,7 @@ static bool tw_plan(int n, int k, int64_t p, WarpPlan *pl) {
         const size_t need = (size_t)32 * use_ch * kp;
         if (need > wb) {
             const size_t wb2 = (need + 15) & ~(size_t)15;
-            const int w2 = (int)std::min<size_t>((cap - bb) / wb2, TW_MAX_WARPS);
+            const int w2 = (int)std::min<size_t>((cap - bb_smem) / wb2, TW_MAX_WARPS);
             if (w2 < 1) return false;
             w = std::min(w, w2);
             pl->warp_smem = wb2;
@@ -1213,7 +1226,8 @@ static bool tw_plan(int n, int k, int64_t p, WarpPlan *pl) {
     pl->kv = kv;
     pl->ch = use_ch;
     pl->warps = w;
-    pl->bitset_bytes = use_ch ? bb : 0;
+    pl->bitset_bytes = use_ch ? bb_smem : 0;
+    pl->bitset_global = use_ch ? bb : 0;
     const int64_t ctas = (p + w - 1) / w;
     pl->grid = (int)std::min<int64_t>(ctas, sms);
     return true;
@@ -1264,7 +1278,7 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
     if (cudaMemcpyAsync(&nnz_h, A.indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
         return set_error(MCB_ERR_CUDA, "tabucol_warp: indptr read failed");
-    const size_t graph_bytes = pl.ch ? pl.bitset_bytes : (4 * (size_t)(n + 1) + 2 * (size_t)nnz_h + 256);
+    const size_t graph_bytes = pl.ch ? pl.bitset_global : (4 * (size_t)(n + 1) + 2 * (size_t)nnz_h + 256);
     uint8_t *ws = (uint8_t *)workspace2(spill_bytes + graph_bytes + 512);
     if (!ws) return set_error(MCB_ERR_CUDA, "tabucol_warp: workspace allocation failed");
     WarpTabuParams P{};
@@ -1272,7 +1286,7 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
     P.best_assigns = A.best_assigns;
     uint8_t *gbase = ws + ((spill_bytes + 255) & ~(size_t)255);
     if (pl.ch) {
-        if (cudaMemsetAsync(gbase, 0, pl.bitset_bytes, st) != cudaSuccess)
+        if (cudaMemsetAsync(gbase, 0, pl.bitset_global, st) != cudaSuccess)
             return set_error(MCB_ERR_CUDA, "memset failed");
         tw_bitset_kernel<<<std::min(n, 4 * num_sms()), 128, 0, st>>>(A.indptr, A.indices, n, pl.ch,
                                                                     reinterpret_cast<uint32_t *>(gbase));
