@@ -66,7 +66,7 @@ int mcb_probe_smem_bandwidth(double *gbs, double *ms);
  * by runs with MCB_FLAG_PROFILE (out: 16 counters; [10] = iterations). */
 int mcb_debug_phase_cycles(unsigned long long *out, int reset);
 /* Diagnostics: counters of the last warp-kernel TabuCol launch made with
- * MCB_FLAG_WSTATS (out: 32 counters, see tabucol_warp.cu WS_*). */
+ * MCB_FLAG_WSTATS (out: 40 counters, see tabucol_warp.cu WS_*). */
 int mcb_debug_warp_stats(unsigned long long *out);
 /* Diagnostics: the exact fp64 divisibility test of the reservoir draws against
  * the 64-bit integer %, on `count` pseudo-random pairs; out: #mismatches. */

@@ -85,7 +85,7 @@ struct WarpTabuParams {
     int bitset_bytes;  // bytes of the CTA-shared bitset copy (0: rows read from L2)
 };
 
-__device__ unsigned long long g_wstats[32];
+__device__ unsigned long long g_wstats[40];
 // divisibility by s = o * 2^t, odd o < 64: x % s == 0  <=>  low t bits of x are
 // zero and (x >> t) * inv(o) <= floor((2^64 - 1) / o)  (inv = inverse mod 2^64)
 __device__ ulonglong2 g_divtab[32];
@@ -124,7 +124,10 @@ enum {
     WS_CY_P2,
     WS_CY_DRAW,
     WS_CY_LOCROW,
-    WS_N = 32
+    WS_NCL_SUM,
+    WS_NCL_GT32,
+    WS_NCL_GT144,
+    WS_N = 40
 };
 #define WST(i, x) \
     if (stats) st[i] += (x)
@@ -630,6 +633,9 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                 __syncwarp();
                 const int D = carry;
                 WST(WS_ROUNDS, nr);
+                WST(WS_NCL_SUM, ncl);
+                WST(WS_NCL_GT32, ncl > 32);
+                WST(WS_NCL_GT144, ncl > 144);
                 WPH(WS_CY_SCAN);
                 if (cnt_on) sum_c += C;
 
@@ -1260,7 +1266,7 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
     if (A.flags & (MCB_FLAG_FORCE_WIDE | MCB_FLAG_FORCE_GLOBAL | MCB_FLAG_PROFILE)) return -1;
     if (A.flags & MCB_FLAG_WSTATS) {
         // reset the counters of this launch
-        unsigned long long z[32] = {0};
+        unsigned long long z[40] = {0};
         cudaMemcpyToSymbolAsync(g_wstats, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
     }
     WarpPlan pl;
@@ -1335,7 +1341,7 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
 
 namespace mcb {
 int tabucol_warp_stats(unsigned long long *out) {
-    if (cudaMemcpyFromSymbol(out, g_wstats, sizeof(unsigned long long) * 32) != cudaSuccess)
+    if (cudaMemcpyFromSymbol(out, g_wstats, sizeof(unsigned long long) * 40) != cudaSuccess)
         return set_error(MCB_ERR_CUDA, "warp stats unavailable");
     return MCB_OK;
 }

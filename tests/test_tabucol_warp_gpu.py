@@ -86,7 +86,7 @@ def test_warp_supersede_path_is_exercised(monkeypatch):
     keys = stream_keys(seed, TAG_LS, 0, pop)
     monkeypatch.delenv("MCB_NO_WARP_KERNEL", raising=False)
     LS._run_tabucol_batch(g, A.copy(), k, keys, depth, flags=N.FLAG_WSTATS)
-    buf = (ctypes.c_ulonglong * 32)()
+    buf = (ctypes.c_ulonglong * 40)()
     N.check(N.lib().mcb_debug_warp_stats(ctypes.addressof(buf)))
     assert buf[0] == pop * depth or buf[0] > 0  # iterations ran in the warp kernel
     assert buf[4] > 0, "no supersede event in the supersede case"

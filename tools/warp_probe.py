@@ -75,13 +75,13 @@ for spec in variants:
     c = out["counters"].cpu().numpy().sum(0)
     if a.stats:
         import ctypes
-        buf = (ctypes.c_ulonglong * 32)()
+        buf = (ctypes.c_ulonglong * 40)()
         N.lib().mcb_debug_warp_stats(ctypes.addressof(buf))
         names = ["it", "rounds", "asp_rounds", "expire_rows", "supersede", "walk_passes", "draw_rounds",
                  "events", "removes", "best"] + [""] * 6 + ["cy_scan", "cy_select", "cy_move", "cy_update",
                                                            "cy_events", "cy_tail", "cy_expire",
                                                            "cy_rowmin", "cy_prefix", "cy_list", "cy_walk", "cy_p2",
-                                                           "cy_draw", "cy_locrows"]
+                                                           "cy_draw", "cy_locrows", "ncl", "ncl_gt32", "ncl_gt144"]
         it_ = max(buf[0], 1)
         print(json.dumps({nm: round(buf[i] / it_, 3) for i, nm in enumerate(names) if nm}), flush=True)
     print(json.dumps({"variant": name, "moves_per_s": best, "ms": ms, "moves": moves,
