@@ -2,7 +2,9 @@
 // host-side runtime shared by the kernel launchers: error state, device
 // properties, grow-only scratch, and the host-pointer (`*_host`) variants
 // that own the host<->device copies.
+#include <chrono>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -47,6 +49,14 @@ int max_smem_optin() {
 static void *grow_buffer(void **buf, size_t *cap, size_t bytes);
 
 void *workspace(size_t bytes) {
+    static void *buf[64] = {nullptr};
+    static size_t cap[64] = {0};
+    const int d = cur_dev();
+    return grow_buffer(&buf[d], &cap[d], bytes);
+}
+
+// third: the device arena of the host-pointer entry points
+void *workspace3(size_t bytes) {
     static void *buf[64] = {nullptr};
     static size_t cap[64] = {0};
     const int d = cur_dev();
@@ -127,8 +137,10 @@ struct Arena {
         size_t total = 0;
         for (auto &it : items) total += (it.bytes + 255) & ~(size_t)255;
         if (total == 0) return MCB_OK;
-        if (cudaMallocAsync((void **)&base, total, st) != cudaSuccess)
-            return set_error(MCB_ERR_CUDA, "cudaMallocAsync(%zu) failed", total);
+        // persistent grow-only buffer (entry points are serialised by g_mu): no
+        // per-call pool allocation / release on the host path
+        base = (uint8_t *)workspace3(total);
+        if (!base) return set_error(MCB_ERR_CUDA, "host-path arena allocation (%zu) failed", total);
         size_t off = 0;
         for (auto &it : items) {
             *it.dev = base + off;
@@ -147,12 +159,7 @@ struct Arena {
         if (cudaStreamSynchronize(st) != cudaSuccess) return set_error(MCB_ERR_CUDA, "sync failed");
         return MCB_OK;
     }
-    ~Arena() {
-        if (base) {
-            cudaFreeAsync(base, st);
-            cudaStreamSynchronize(st);
-        }
-    }
+    ~Arena() {}
 };
 
 }  // namespace mcb
@@ -219,11 +226,16 @@ int mcb_tabucol_batch_host(int32_t *assigns, int64_t p, int64_t n, int64_t k,
     ar.add(end_conflicts, &a.end_conflicts, (size_t)p, false, true);
     ar.add(iters_used, &a.iters_used, (size_t)p, false, true);
     ar.add(diag, &a.diag, (size_t)p, true, true);
-    ar.add(log_v, &a.log_v, pc, false, true);
-    ar.add(log_iter, &a.log_iter, pc, false, true);
-    ar.add(log_tt, &a.log_tt, pc, false, true);
+    // the kernels write only the first log_cnt[i] entries of a row: the rest
+    // keeps the caller's content (as the numba kernel leaves it), so upload too
+    ar.add(log_v, &a.log_v, pc, true, true);
+    ar.add(log_iter, &a.log_iter, pc, true, true);
+    ar.add(log_tt, &a.log_tt, pc, true, true);
     ar.add(log_cnt, &a.log_cnt, (size_t)p, false, true);
     ar.add(counters, &a.counters, 2 * (size_t)p, false, true);
+    const bool timing = getenv("MCB_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t0 = now();
     int rc = ar.upload();
     if (rc) return rc;
     a.p = p;
@@ -233,9 +245,19 @@ int mcb_tabucol_batch_host(int32_t *assigns, int64_t p, int64_t n, int64_t k,
     a.depth = depth;
     a.log_cap = (log_cap > 0 && a.log_v) ? log_cap : 0;
     a.flags = flags;
+    if (timing) cudaStreamSynchronize(st);
+    const auto t1 = now();
     rc = tabucol_run(a, st);
     if (rc) return rc;
-    return ar.download();
+    const auto t2 = now();
+    rc = ar.download();
+    if (timing) {
+        const auto t3 = now();
+        auto ms = [](auto x, auto y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
+        fprintf(stderr, "[mcb] tabucol_host: upload %.1f ms, run %.1f ms, download %.1f ms\n", ms(t0, t1),
+                ms(t1, t2), ms(t2, t3));
+    }
+    return rc;
 }
 
 int mcb_wvcp_batch(int32_t *assigns, int64_t p, int64_t n, int64_t k, const int64_t *adj_indptr,
@@ -290,10 +312,12 @@ int mcb_wvcp_batch_host(int32_t *assigns, int64_t p, int64_t n, int64_t k,
     ar.add(end_conflicts, &a.end_conflicts, (size_t)p, false, true);
     ar.add(phi_used, &a.phi_used, (size_t)p * (rounds + 1), true, true);
     ar.add(diag, &a.diag, (size_t)p, true, true);
-    ar.add(log_v, &a.log_v, pc, false, true);
-    ar.add(log_iter, &a.log_iter, pc, false, true);
-    ar.add(log_tt, &a.log_tt, pc, false, true);
-    ar.add(log_asp, &a.log_asp, pc, false, true);
+    // the kernels write only the first log_cnt[i] entries of a row: the rest
+    // keeps the caller's content (as the numba kernel leaves it), so upload too
+    ar.add(log_v, &a.log_v, pc, true, true);
+    ar.add(log_iter, &a.log_iter, pc, true, true);
+    ar.add(log_tt, &a.log_tt, pc, true, true);
+    ar.add(log_asp, &a.log_asp, pc, true, true);
     ar.add(log_cnt, &a.log_cnt, (size_t)p, false, true);
     int rc = ar.upload();
     if (rc) return rc;

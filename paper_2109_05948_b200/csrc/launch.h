@@ -14,6 +14,7 @@ int max_smem_optin();
 // the previous contents; every entry point synchronises before returning).
 void *workspace(size_t bytes);
 void *workspace2(size_t bytes);
+void *workspace3(size_t bytes);
 
 struct TabucolArgs {
     int32_t *assigns;

@@ -120,3 +120,37 @@ def test_device_path_matches_host_path():
     torch.cuda.synchronize()
     for key in ("end_assigns", "best_assigns", "best_conflicts", "iters_used"):
         np.testing.assert_array_equal(dev[key].cpu().numpy(), host[key])
+
+
+def test_host_path_leaves_unwritten_log_entries_alone():
+    """The kernels write the first log_cnt[i] entries of each log row; the rest
+    keeps the caller's content, as the numba kernel leaves it -- also when the
+    device arena still holds a longer previous call's logs."""
+    g = rand_graph(1, 125, 0.5)
+    A = random_col_assigns(125, 18, 16, 1)
+    keys = stream_keys(1, TAG_LS, 0, 16)
+    LS._run_tabucol_batch(g, A.copy(), 18, keys, 3000, log_moves=True)  # long logs in the arena
+    out = LS._run_tabucol_batch(g, A.copy(), 18, keys, 3000, log_moves=True)
+    lv, li, lt, lc = out["log"]
+    short = LS._run_tabucol_batch(g, A.copy(), 18, keys, 40, log_moves=True)
+    sv, si, st, sc = short["log"]
+    assert (sc == 40).all()
+    np.testing.assert_array_equal(sv[:, :40], lv[:, :40])
+    assert lv.shape[1] == 3000 and sv.shape[1] == 40
+    # a caller-provided tail is preserved
+    p, cap = 16, 200
+    keep = np.full((p, cap), -7, np.int32)
+    from paper_2109_05948_b200 import _native as NN
+    Ac = A.copy()
+    from paper_2109_05948_b200.graph import graph_arrays
+    ip, ix, eu, ev = graph_arrays(g)
+    best = A.copy()
+    bc, ec, it, dg = (np.zeros(p, np.int64) for _ in range(4))
+    li2, lt2, lcnt = np.zeros((p, cap), np.int64), np.zeros((p, cap), np.int64), np.zeros(p, np.int64)
+    NN.check(NN.lib().mcb_tabucol_batch_host(
+        Ac.ctypes.data, p, 125, 18, ip.ctypes.data, ix.ctypes.data, eu.ctypes.data, ev.ctypes.data, g.m, 50,
+        keys.ctypes.data, best.ctypes.data, bc.ctypes.data, ec.ctypes.data, it.ctypes.data,
+        dg.ctypes.data, cap, keep.ctypes.data, li2.ctypes.data, lt2.ctypes.data, lcnt.ctypes.data,
+        None, 0, None))
+    assert (lcnt == 50).all()
+    assert (keep[:, 50:] == -7).all()
