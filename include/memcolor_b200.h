@@ -160,6 +160,38 @@ int mcb_pairwise_host(const int32_t *pop, int64_t p, const int32_t *off, int64_t
                       int64_t k, int32_t *cross, int32_t *within, int64_t job_begin,
                       int64_t job_end, uint32_t flags, void *stream);
 
+/*
+ * Population update (mc/population.py:59-127): merge p incumbents (pdist
+ * p x p, fitness fit_pop) and q newcomers (cross p x q, within q x q,
+ * fitness fit_new); admit candidates in (fitness, origin, index) order when
+ * their distance to every admitted candidate exceeds ms; fill with the best
+ * rejected ones.  out_adm int32[p] = admitted candidate ids in slot order
+ * (0..p-1 incumbents, p.. newcomers), out_rule uint8[p] = admitted by the
+ * spacing rule.  Optional (NULL to skip): out_dist int32[p,p] (the new
+ * population's distance matrix), out_assigns int32[p,n] + out_fit int64[p]
+ * (gathered from pop_assigns int32[p,n] / new_assigns int32[q,n]).  Device
+ * pointers, asynchronous on `stream`.
+ */
+int mcb_update_population(const int32_t *pdist, const int32_t *cross, const int32_t *within,
+                          const int64_t *fit_pop, const int64_t *fit_new, int64_t p, int64_t q, int64_t ms,
+                          const int32_t *pop_assigns, const int32_t *new_assigns, int64_t n,
+                          int32_t *out_adm, uint8_t *out_rule, int32_t *out_dist, int32_t *out_assigns,
+                          int64_t *out_fit, void *stream);
+int mcb_update_population_host(const int32_t *pdist, const int32_t *cross, const int32_t *within,
+                               const int64_t *fit_pop, const int64_t *fit_new, int64_t p, int64_t q,
+                               int64_t ms, const int32_t *pop_assigns, const int32_t *new_assigns, int64_t n,
+                               int32_t *out_adm, uint8_t *out_rule, int32_t *out_dist, int32_t *out_assigns,
+                               int64_t *out_fit, void *stream);
+/*
+ * K nearest neighbours of every individual by (distance, index), excluding
+ * itself (mc/population.py:130-141): dist int32[p,p] with values in
+ * [0, max_dist]; matches int64[p,K] in (distance, index) order.
+ */
+int mcb_match_parents(const int32_t *dist, int64_t p, int64_t K, int64_t max_dist, int64_t *matches,
+                      void *stream);
+int mcb_match_parents_host(const int32_t *dist, int64_t p, int64_t K, int64_t max_dist, int64_t *matches,
+                           void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,6 +29,7 @@ EXPORTS = [
     "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_gpx_rows", "mcb_pairwise", "mcb_pairwise_host",
     "mcb_probe_smem_bandwidth", "mcb_debug_phase_cycles", "mcb_debug_warp_stats",
     "mcb_debug_modcheck", "mcb_tabucol_describe",
+    "mcb_update_population", "mcb_update_population_host", "mcb_match_parents", "mcb_match_parents_host",
 ]
 
 _lib = None
@@ -63,6 +64,11 @@ def _declare(L):
     L.mcb_debug_warp_stats.argtypes = [P]
     L.mcb_debug_modcheck.argtypes = [I64, P]
     L.mcb_tabucol_describe.argtypes = [I64, I64, I64, C.c_char_p, C.c_int]
+    up = [P, P, P, P, P, I64, I64, I64, P, P, I64, P, P, P, P, P, P]
+    L.mcb_update_population.argtypes = up
+    L.mcb_update_population_host.argtypes = up
+    L.mcb_match_parents.argtypes = [P, I64, I64, I64, P, P]
+    L.mcb_match_parents_host.argtypes = [P, I64, I64, I64, P, P]
     for name in EXPORTS[3:]:
         getattr(L, name).restype = C.c_int
 

@@ -402,3 +402,79 @@ int mcb_pairwise_host(const int32_t *pop, int64_t p, const int32_t *off, int64_t
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int mcb_update_population(const int32_t *pdist, const int32_t *cross, const int32_t *within,
+                          const int64_t *fit_pop, const int64_t *fit_new, int64_t p, int64_t q, int64_t ms,
+                          const int32_t *pop_assigns, const int32_t *new_assigns, int64_t n,
+                          int32_t *out_adm, uint8_t *out_rule, int32_t *out_dist, int32_t *out_assigns,
+                          int64_t *out_fit, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int rc = update_population_run(pdist, cross, within, fit_pop, fit_new, p, q, ms, pop_assigns,
+                                         new_assigns, n, out_adm, out_rule, out_dist, out_assigns, out_fit,
+                                         (cudaStream_t)stream);
+    if (rc) return rc;
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "update_population failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return MCB_OK;
+}
+
+int mcb_update_population_host(const int32_t *pdist, const int32_t *cross, const int32_t *within,
+                               const int64_t *fit_pop, const int64_t *fit_new, int64_t p, int64_t q,
+                               int64_t ms, const int32_t *pop_assigns, const int32_t *new_assigns, int64_t n,
+                               int32_t *out_adm, uint8_t *out_rule, int32_t *out_dist, int32_t *out_assigns,
+                               int64_t *out_fit, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p < 1 || q < 0) return set_error(MCB_ERR_VALUE, "bad shape");
+    Arena ar(st);
+    const int32_t *dpd, *dcr, *dwi, *dpa, *dna;
+    const int64_t *dfp, *dfn;
+    int32_t *dadm, *ddist, *das;
+    uint8_t *drule;
+    int64_t *dfit;
+    ar.add(pdist, &dpd, (size_t)p * p);
+    ar.add(cross, &dcr, (size_t)p * q);
+    ar.add(within, &dwi, (size_t)q * q);
+    ar.add(fit_pop, &dfp, (size_t)p);
+    ar.add(fit_new, &dfn, (size_t)q);
+    ar.add(pop_assigns, &dpa, out_assigns ? (size_t)p * n : 0);
+    ar.add(new_assigns, &dna, out_assigns ? (size_t)q * n : 0);
+    ar.add(out_adm, &dadm, (size_t)p, false, true);
+    ar.add(out_rule, &drule, (size_t)p, false, true);
+    ar.add(out_dist, &ddist, (size_t)p * p, false, true);
+    ar.add(out_assigns, &das, (size_t)p * n, false, true);
+    ar.add(out_fit, &dfit, (size_t)p, false, true);
+    int rc = ar.upload();
+    if (rc) return rc;
+    rc = update_population_run(dpd, dcr, dwi, dfp, dfn, p, q, ms, dpa, dna, n, dadm, drule, ddist,
+                               out_assigns ? das : nullptr, out_assigns ? dfit : nullptr, st);
+    if (rc) return rc;
+    return ar.download();
+}
+
+int mcb_match_parents(const int32_t *dist, int64_t p, int64_t K, int64_t max_dist, int64_t *matches,
+                      void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return match_parents_run(dist, p, K, max_dist, matches, (cudaStream_t)stream);
+}
+
+int mcb_match_parents_host(const int32_t *dist, int64_t p, int64_t K, int64_t max_dist, int64_t *matches,
+                           void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p < 1) return set_error(MCB_ERR_VALUE, "bad shape");
+    Arena ar(st);
+    const int32_t *dd;
+    int64_t *dm;
+    ar.add(dist, &dd, (size_t)p * p);
+    ar.add(matches, &dm, (size_t)p * (K > 0 ? K : 0), false, true);
+    int rc = ar.upload();
+    if (rc) return rc;
+    rc = match_parents_run(dd, p, K, max_dist, dm, st);
+    if (rc) return rc;
+    return ar.download();
+}
+
+}  // extern "C"

@@ -76,6 +76,13 @@ int gpx_rows_run(const int32_t *pop, int64_t p, int64_t n, const int64_t *matche
 int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n, int64_t k,
                  int32_t *cross, int32_t *within, int64_t job_begin, int64_t job_end,
                  uint32_t flags, cudaStream_t st);
+int update_population_run(const int32_t *pdist, const int32_t *cross, const int32_t *within,
+                          const int64_t *fit_pop, const int64_t *fit_new, int64_t p, int64_t q, int64_t ms,
+                          const int32_t *pop_assigns, const int32_t *new_assigns, int64_t n,
+                          int32_t *out_adm, uint8_t *out_rule, int32_t *out_dist, int32_t *out_assigns,
+                          int64_t *out_fit, cudaStream_t st);
+int match_parents_run(const int32_t *dist, int64_t p, int64_t K, int64_t max_dist, int64_t *matches,
+                      cudaStream_t st);
 int stream_values_run(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out, int64_t count,
                       cudaStream_t st);
 

@@ -15,6 +15,7 @@ inputs, the outputs of the reference's own hot-path kernels:
 * wvcp.npz      _run_wvcp_batch outputs + move logs (`localsearch.py:427`)
 * gpx.npz       build_offspring_batch / gpx (`crossover.py:69-93`)
 * distance.npz  pairwise_distances / approx_partition_distance (`distance.py:75-155`)
+* population.npz  update_population / match_parents (`population.py:59-141`)
 
 Inputs are regenerated in the tests from the recorded parameters with the
 package's own generators (which are themselves pinned by graphs.npz and the
@@ -40,6 +41,7 @@ import numpy as np  # noqa: E402
 from memcolor import crossover as RCX  # noqa: E402
 from memcolor import distance as RDI  # noqa: E402
 from memcolor import localsearch as RLS  # noqa: E402
+from memcolor import population as RPOP  # noqa: E402
 from memcolor import rng as RRNG  # noqa: E402
 from memcolor.coloring import Coloring as RColoring  # noqa: E402
 from oracles import rand_graph as ref_rand_graph  # noqa: E402
@@ -227,6 +229,68 @@ def gen_distance(out):
     print("distance", len(meta), out["hand_values"])
 
 
+# --------------------------------------------------------------------------
+# population update / matching: (name, seed, n, k, p, q, n_close, fit_range, K)
+#   n_close newcomers are perturbed copies of incumbents (distance <= ms), so
+#   the spacing rule rejects and the fallback fill runs; fit_range small gives
+#   fitness ties (origin / index tie-breaks)
+# --------------------------------------------------------------------------
+POP_CASES = [
+    ("small", 3, 60, 6, 12, 12, 4, 5, 3),
+    ("ties", 4, 80, 8, 20, 24, 10, 3, 5),
+    ("crowded", 5, 50, 5, 16, 16, 16, 2, 4),   # many within ms: fill path
+    ("wide", 6, 120, 10, 32, 32, 8, 40, 7),
+    ("q0", 7, 40, 4, 10, 0, 0, 4, 2),          # no newcomers
+    ("clones", 8, 50, 5, 12, 12, -1, 3, 3),    # all candidates near one colouring: fallback fill
+    ("half", 9, 60, 6, 16, 16, -2, 4, 5),      # two clusters: 2 by the rule, the rest filled
+]
+
+
+def gen_population(out):
+    from memcolor.distance import pairwise_distances as rpd
+
+    for name, seed, n, k, p, q, n_close, fr, K in POP_CASES:
+        rs = np.random.default_rng(seed)
+        pop_a = rs.integers(0, k, size=(p, n)).astype(np.int32)
+        new_a = rs.integers(0, k, size=(q, n)).astype(np.int32)
+        ms = RPOP.min_spacing(n)
+        if n_close < 0:
+            # -1: every candidate a perturbation of one base colouring; -2: of two bases
+            bases = rs.integers(0, k, size=(-n_close, n)).astype(np.int32)
+            for arr in (pop_a, new_a):
+                for t in range(arr.shape[0]):
+                    arr[t] = bases[t % bases.shape[0]]
+                    flip = rs.choice(n, size=1, replace=False)
+                    arr[t, flip] = rs.integers(0, k, size=1)
+        for t in range(max(0, min(n_close, q))):
+            src = pop_a[rs.integers(0, p)] if t % 2 == 0 else new_a[rs.integers(0, max(t, 1))]
+            new_a[t] = src
+            flip = rs.choice(n, size=max(1, ms // 3), replace=False)
+            new_a[t, flip] = rs.integers(0, k, size=flip.size)
+        pop_f = rs.integers(0, fr, size=p).astype(np.int64)
+        new_f = rs.integers(0, fr, size=q).astype(np.int64)
+        cols = [RColoring(pop_a[i], k) for i in range(p)]
+        pop = RPOP.Population.from_colorings(cols, pop_f)
+        cross, within = rpd(pop_a, new_a, k=k)
+        res = RPOP.update_population(pop, new_a, new_f, cross, within, ms)
+        m = RPOP.match_parents(res, K)
+        pre = name + "__"
+        out[pre + "params"] = np.array([seed, n, k, p, q, ms, K], dtype=np.int64)
+        out[pre + "pop_assigns"] = pop_a
+        out[pre + "new_assigns"] = new_a
+        out[pre + "pop_fit"] = pop_f
+        out[pre + "new_fit"] = new_f
+        out[pre + "pop_dist"] = pop.dist.astype(np.int32)
+        out[pre + "cross"] = np.asarray(cross, dtype=np.int32)
+        out[pre + "within"] = np.asarray(within, dtype=np.int32)
+        out[pre + "res_assigns"] = res.assigns.astype(np.int32)
+        out[pre + "res_fit"] = res.fitness.astype(np.int64)
+        out[pre + "res_dist"] = res.dist.astype(np.int32)
+        out[pre + "res_rule"] = res.admitted_by_rule.astype(np.uint8)
+        out[pre + "matches"] = m.astype(np.int64)
+    out["cases"] = np.array([c[0] for c in POP_CASES])
+
+
 def gen_rng(out):
     rows = []
     for seed, tag, idx in [(1, 2, (0, 0)), (1, 1, (0,)), (2024, 2, (5, 11)), (7, 1, ()),
@@ -252,9 +316,14 @@ def gen_graphs(out):
 
 
 def main():
+    """python make_golden.py [name ...]  (default: every fixture)"""
     os.makedirs(HERE, exist_ok=True)
+    only = set(sys.argv[1:])
     for fn, name in [(gen_rng, "rng"), (gen_graphs, "graphs"), (gen_tabucol, "tabucol"),
-                     (gen_wvcp, "wvcp"), (gen_gpx, "gpx"), (gen_distance, "distance")]:
+                     (gen_wvcp, "wvcp"), (gen_gpx, "gpx"), (gen_distance, "distance"),
+                     (gen_population, "population")]:
+        if only and name not in only:
+            continue
         out = {}
         fn(out)
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)

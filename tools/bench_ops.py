@@ -4,6 +4,8 @@ restatement of the reference on this host (oracle/, OpenMP, all cores).
 * WVCP moves/s      config 3 shape: G(500,.5) w in [1,100], k=60 (D, depth reduced)
 * GPX offspring/s   config 2 shape: n=1000, k=83, parents (i, uniform j != i)
 * distance pairs/s  config 2 shape: n=1000, k=83 pairwise_distances(P, P')
+* update_population generations/s, config 2 size p = q = 16384 (n = 1000)
+* match_parents     rows/s, p = 16384, K = 16
 
 Each line: {"op", "gpu": units/s, "cpu": units/s, "cores", "sample", ...}.
 Synthetic inputs; device-resident inputs, CUDA-event timing.
@@ -103,6 +105,78 @@ def bench_distance(a):
             "gpu_ms": 1e3 * t, "alg_bytes_per_pair": 6 * n}
 
 
+def _pop_case(p, q, n, seed=3):
+    """Distance matrices with cluster structure (symmetric, zero diagonal)."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    cen = torch.randint(0, max(2, (p + q) // 8), (p + q,), device="cuda", generator=g)
+    D = torch.randint(n // 2, n + 1, (p + q, p + q), device="cuda", generator=g, dtype=torch.int32)
+    D = torch.minimum(D, D.T)
+    same = cen[:, None] == cen[None, :]
+    D = torch.where(same, torch.randint(0, n // 10 + 3, (p + q, p + q), device="cuda", generator=g,
+                                        dtype=torch.int32), D)
+    D = torch.minimum(D, D.T)
+    D.fill_diagonal_(0)
+    fit = torch.randint(0, 40, (p + q,), device="cuda", generator=g, dtype=torch.int64)
+    return (D[:p, :p].contiguous(), D[:p, p:].contiguous(), D[p:, p:].contiguous(), fit[:p].contiguous(),
+            fit[p:].contiguous())
+
+
+def bench_update_population(a):
+    from oracle import population_oracle as PO
+
+    p = q = a.pop_p
+    n = 1000
+    pd, cr, wi, fp, fq = _pop_case(p, q, n)
+    ms = n // 10
+    adm = torch.empty(p, dtype=torch.int32, device="cuda")
+    rule = torch.empty(p, dtype=torch.uint8, device="cuda")
+    nd = torch.empty((p, p), dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    P = N.ptr
+
+    def run():
+        N.check(N.lib().mcb_update_population(P(pd), P(cr), P(wi), P(fp), P(fq), p, q, ms, None, None, n,
+                                             P(adm), P(rule), P(nd), None, None, stream))
+
+    t, _ = timed(run, reps=2)
+    pc = 384  # the reference loop is O(p^2) Python: bounded CPU sample
+    pdc, crc, wic = pd[:pc, :pc].cpu().numpy(), cr[:pc, :pc].cpu().numpy(), wi[:pc, :pc].cpu().numpy()
+    t0 = time.perf_counter()
+    PO.update_population(pdc, fp[:pc].cpu().numpy(), np.zeros((pc, 1), np.int32), np.zeros((pc, 1), np.int32),
+                         fq[:pc].cpu().numpy(), crc, wic, ms)
+    tc = time.perf_counter() - t0
+    return {"op": "update_population", "unit": "generations/s", "gpu": 1.0 / t,
+            "cpu": 1.0 / (tc * (p / pc) ** 2), "cores": 1,
+            "config": f"p=q={p}, n={n}, ms={ms} (clustered synthetic distances)",
+            "cpu_sample": f"p=q={pc} with the restated reference loop, scaled by (p/{pc})^2 (O(p^2) loop)",
+            "gpu_ms": 1e3 * t, "by_rule": int(rule.sum().item())}
+
+
+def bench_match_parents(a):
+    from oracle import population_oracle as PO
+
+    p, K, n = a.pop_p, 16, 1000
+    pd, _, _, _, _ = _pop_case(p, 1, n)
+    m = torch.empty((p, K), dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        N.check(N.lib().mcb_match_parents(N.ptr(pd), p, K, n, N.ptr(m), stream))
+
+    t, _ = timed(run, reps=3)
+    rows = 256
+    dc = pd.cpu().numpy()
+    t0 = time.perf_counter()
+    idx = np.arange(p)
+    for i in range(rows):  # the reference row loop (population.py:137-140)
+        order = np.lexsort((idx, dc[i]))
+        order[order != i][:K]
+    tc = time.perf_counter() - t0
+    return {"op": "match_parents", "unit": "rows/s", "gpu": p / t, "cpu": rows / tc, "cores": 1,
+            "config": f"p={p}, K={K}", "cpu_sample": f"{rows} rows of the reference loop", "gpu_ms": 1e3 * t,
+            "alg_bytes_per_row": 4 * p}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ops", default="wvcp,gpx,distance")
@@ -110,11 +184,13 @@ def main():
     ap.add_argument("--wvcp-depth", type=int, default=500)
     ap.add_argument("--gpx-pop", type=int, default=16384)
     ap.add_argument("--dist-pop", type=int, default=4096)
+    ap.add_argument("--pop-p", type=int, default=16384)
     a = ap.parse_args()
     N.lib()
     oracle.build()
     for op in a.ops.split(","):
-        r = {"wvcp": bench_wvcp, "gpx": bench_gpx, "distance": bench_distance}[op](a)
+        r = {"wvcp": bench_wvcp, "gpx": bench_gpx, "distance": bench_distance,
+             "update_population": bench_update_population, "match_parents": bench_match_parents}[op](a)
         r["speedup_vs_cpu"] = r["gpu"] / r["cpu"]
         print(json.dumps(r), flush=True)
 
