@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
         for (int j = 0; j < KE; j++) ring[j] = 0u;
         int nrows = 0;
         uint32_t ins = 0;
+        uint32_t next_exp = 0;  // lower bound of the earliest live expiry (valid if nrows)
 
         // ---------------- iterations (:320-405) ----------------
         if (k >= 2 && !bad) {
@@ -532,22 +533,28 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                 const int thr = (int)max(best - conflicts, (long long)-TW_BIG);
 
                 // ---- tabu expiry: it < tabu[v,c] fails from it == expiry on
-                {
+                if (nrows > 0 && (int)(next_exp - it32) <= 0) {
+                    // some entry may expire now (next_exp is a lower bound)
                     int last = -1;
+                    uint32_t dmin = 0x4000u;
 #pragma unroll
                     for (int j = 0; j < KE; j++) {
                         if (j >= nrows) break;
                         const uint32_t e = ring[j];
-                        const bool hit = (e >> 31) != 0u && ent_dist(e, it32) == 0u;
+                        const uint32_t dist = ent_dist(e, it32);
+                        const bool hit = (e >> 31) != 0u && dist == 0u;
                         if (hit) {
                             const int v = (e >> 21) & 0x3FF, c = (e >> 14) & 0x7F;
                             gam[(size_t)v * KP + S::phys(c, S::g(v))] &= (uint8_t)~TABU;
                         }
                         ring[j] = hit ? 0u : e;
-                        if (__any_sync(FULLM, (ring[j] >> 31) != 0u)) last = j;
+                        const bool live = (ring[j] >> 31) != 0u;
+                        if (live) dmin = min(dmin, dist);
+                        if (__any_sync(FULLM, live)) last = j;
                     }
                     WST(WS_EXPIRE_ROWS, nrows);
                     nrows = last + 1;
+                    next_exp = it32 + __reduce_min_sync(FULLM, dmin);
                     __syncwarp();
                 }
                 WPH(WS_CY_EXPIRE);
@@ -903,6 +910,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             nrows = min(nrows + 1, KE);
                         }
                         if (lane == L) ring[0] = ent_pack(v, a, e_new);
+                        if (nrows == 0 || (int)(e_new - next_exp) < 0) next_exp = e_new;
                         nrows = max(nrows, 1);
                         ins++;
                     }
