@@ -14,20 +14,21 @@ def find(pat):
     for i, l in enumerate(src):
         if pat in l:
             return i + 1
-    raise KeyError(pat)
+    return None
 
 
 marks = [("expire", "// ---- tabu expiry"), ("scan1", "// ---- scan, phase 1"),
-         ("phase2", "// ---- phase 2a: tie counts"), ("walks", "// ---- phase 2b: rows that lower"), ("draws", "// tenure draw (:363-365)"),
+         ("phase2", "// ---- phase 2a: tie counts"), ("walks", "one walk pass over up to"), ("walks", "// ---- phase 2b: rows that lower"), ("draws", "// tenure draw (:363-365)"),
          ("locate", "// ---- locate the sstar-th"), ("move", "// ---- move, tenure, tabu entry"),
          ("update", "// ---- gamma update over N(v)"), ("events", "// events in ascending vertex order"),
          ("best", "// ---- best (:387-390)"), ("tail", "// ---- scratch check every 1024"),
          ("end", "// ---------------- outputs")]
 marks = [(n, find(p)) for n, p in marks]
+marks = [(n, l) for n, l in marks if l is not None]
 hl = [("walk_words", "int walk_words("), ("cand_word", "__device__ __forceinline__ uint32_t cand_word"),
       ("row_min", "__device__ __forceinline__ int row_min("), ("row_count", "__device__ __forceinline__ int row_count("),
       ("count_eq", "__device__ __forceinline__ uint32_t zero_flags")]
-hl = sorted([(find(p), n) for n, p in hl])
+hl = sorted([(find(p), n) for n, p in hl if find(p) is not None])
 kern = find("template <int KV, int CH, bool BITSET>")
 
 
