@@ -89,6 +89,39 @@ __device__ __forceinline__ double gval_of(long long ds, long long dc, double phi
     return __dadd_rn((double)ds, __dmul_rn(phi, (double)dc));  // no FMA (:193)
 }
 
+// Exact integer evaluation of the objective.  When phi = t * 2^-s with small
+// t and s (the reference's schedule phi0 * 2^j, e.g. 6 * 2^j at config 4), and
+// |ds| < 2^31, |dc| < 2^16, every fp64 operation of gval_of is exact, so the
+// fp64 values are the rationals (ds * 2^s + t * dc) * 2^-s: comparing the
+// integer numerators G gives exactly the same order and the same ties.  The
+// scan then keeps G (as an exact double where a double is stored).
+struct GvMode {
+    int fast, s;
+    long long t;
+    double phi;
+};
+__device__ __forceinline__ GvMode gv_mode(double phi, int n) {
+    GvMode m{0, 0, 0, phi};
+    if (n < (1 << 16)) {
+        double f = phi;
+        for (int s = 0; s <= 16; s++, f *= 2.0) {  // f = phi * 2^s exactly
+            if (f == trunc(f) && fabs(f) < 1048576.0) {
+                m.fast = 1;
+                m.s = s;
+                m.t = (long long)f;
+                break;
+            }
+        }
+    }
+    return m;
+}
+__device__ __forceinline__ long long gnum(const GvMode &m, long long ds, long long dc) {
+    return (ds << m.s) + m.t * dc;
+}
+__device__ __forceinline__ double gval(const GvMode &m, long long ds, long long dc) {
+    return m.fast ? (double)gnum(m, ds, dc) : gval_of(ds, dc, m.phi);
+}
+
 __device__ __forceinline__ double shfl_up_d(double x, int o) {
     return __longlong_as_double(__shfl_up_sync(0xffffffffu, __double_as_longlong(x), o));
 }
@@ -130,9 +163,17 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
     const bool diagf = (P.flags & MCB_FLAG_DIAG) != 0;
     const bool prod = (P.flags & MCB_FLAG_PRODUCTION) != 0;
 
-    for (int v = tid; v < n; v += NT) {
-        wgt[v] = (int32_t)P.weights[v];
-        wrk[v] = (uint16_t)P.wranks[v];
+    __shared__ int s_maxw;
+    if (tid == 0) s_maxw = 0;
+    __syncthreads();
+    {
+        int mw = 0;
+        for (int v = tid; v < n; v += NT) {
+            wgt[v] = (int32_t)P.weights[v];
+            wrk[v] = (uint16_t)P.wranks[v];
+            mw = max(mw, abs((int)P.weights[v]));
+        }
+        atomicMax(&s_maxw, mw);
     }
 
     // refresh_class (:46-67) by one warp: highest rank with a member, and the
@@ -253,7 +294,70 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                 const long long it = ctl.it, score = ctl.score, conflicts = ctl.conflicts,
                                 best = ctl.best;
                 const double phi = ctl.phi;
+                const GvMode gm = gv_mode(phi, n);
+                // 32-bit numerators when |t| n + maxw 2^s < 2^30 (|dc| <= n, |ds| <= maxw)
+                const bool fast32 =
+                    gm.fast && (long long)(gm.t < 0 ? -gm.t : gm.t) * n + ((long long)s_maxw << gm.s) < (1ll << 30);
                 // pass 1: (min g, count) per vertex row over admissible candidates
+                if (fast32) {
+                    const int S = gm.s, Tt = (int)gm.t;
+                    for (int v = tid; v < n; v += NT) {
+                        const int a = assign[v];
+                        const int rem = (wrk[v] == max_rank[a]) ? (int)uniq_drop[a] : 0;
+                        const uint16_t *row = gamma + (size_t)v * k;
+                        const int gva = row[a];
+                        const bool frozen = (uint64_t)it < tabu_until[v];
+                        const int wv = wgt[v];
+                        int m = INT_MAX, cnt = 0;
+                        if (!frozen) {
+                            // branch-free: the own colour gets INT_MAX (never below a
+                            // real candidate; k >= 2 leaves one)
+                            for (int c = 0; c < k; c++) {
+                                const int dc = (int)row[c] - gva;
+                                const int ds = max(0, wv - (int)max_val[c]) - rem;
+                                const int G = (c == a) ? INT_MAX : (ds << S) + Tt * dc;
+                                cnt = (G < m) ? 1 : cnt + (G == m);
+                                m = min(m, G);
+                            }
+                        } else {
+                            // frozen vertex: only legal moves that beat the best legal score
+                            for (int c = 0; c < k; c++) {
+                                const int dc = (int)row[c] - gva;
+                                const int ds = max(0, wv - (int)max_val[c]) - rem;
+                                const bool ok = c != a && conflicts + dc == 0 && score + ds < best;
+                                const int G = ok ? (ds << S) + Tt * dc : INT_MAX;
+                                cnt = (G < m) ? 1 : cnt + (G == m && ok);
+                                m = min(m, G);
+                            }
+                        }
+                        rmin[v] = (m == INT_MAX) ? INF : (double)m;
+                        rcnt[v] = (uint16_t)(m == INT_MAX ? 0 : cnt);
+                    }
+                } else if (gm.fast) {
+                    // exact integer numerators (see gv_mode)
+                    for (int v = tid; v < n; v += NT) {
+                        const int a = assign[v];
+                        const long long rem = (wrk[v] == max_rank[a]) ? uniq_drop[a] : 0;
+                        const uint16_t *row = gamma + (size_t)v * k;
+                        const int gva = row[a];
+                        const bool frozen = (uint64_t)it < tabu_until[v];
+                        const long long wv = wgt[v];
+                        long long m = LLONG_MAX;
+                        int cnt = 0;
+                        for (int c = 0; c < k; c++) {
+                            const long long dc = (long long)row[c] - gva;
+                            long long dadd = wv - max_val[c];
+                            if (dadd < 0) dadd = 0;
+                            const long long ds = dadd - rem;
+                            const bool skip = (c == a) || (frozen && (conflicts + dc != 0 || score + ds >= best));
+                            const long long G = skip ? LLONG_MAX : gnum(gm, ds, dc);
+                            cnt = (G < m) ? 1 : cnt + (G == m && G != LLONG_MAX);
+                            m = min(m, G);
+                        }
+                        rmin[v] = (m == LLONG_MAX) ? INF : (double)m;
+                        rcnt[v] = (uint16_t)cnt;
+                    }
+                } else
                 for (int v = tid; v < n; v += NT) {
                     const int a = assign[v];
                     const long long rem = (wrk[v] == max_rank[a]) ? uniq_drop[a] : 0;
@@ -341,7 +445,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                                 if (dadd < 0) dadd = 0;
                                 const long long ds = dadd - rem;
                                 if (!(frozen && (conflicts + dc != 0 || score + ds >= best)))
-                                    gv = gval_of(ds, dc, phi);
+                                    gv = gval(gm, ds, dc);
                             }
                             double incl = gv;
                             for (int o = 1; o < 32; o <<= 1) {
@@ -417,7 +521,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                                 if (dadd < 0) dadd = 0;
                                 ds = dadd - rem;
                                 if (!(frozen && (conflicts + dc != 0 || score + ds >= best)))
-                                    hit = gval_of(ds, dc, phi) == D;
+                                    hit = gval(gm, ds, dc) == D;
                             }
                             const unsigned hm = __ballot_sync(FULL, hit);
                             const int hc = __popc(hm);
