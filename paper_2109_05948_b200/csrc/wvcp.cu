@@ -319,12 +319,16 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                                 cnt = (G < m) ? 1 : cnt + (G == m);
                                 m = min(m, G);
                             }
-                        } else {
-                            // frozen vertex: only legal moves that beat the best legal score
+                        } else if (conflicts <= gva) {
+                            // frozen vertex: only legal moves (dc == -conflicts, reachable
+                            // only if conflicts <= gva) that beat the best legal score
+                            const int need_dc = -(int)conflicts;
+                            const long long room = best - score;  // ds < room
+                            const int dsmax = room > INT_MAX ? INT_MAX : (room < INT_MIN ? INT_MIN : (int)room);
                             for (int c = 0; c < k; c++) {
                                 const int dc = (int)row[c] - gva;
                                 const int ds = max(0, wv - (int)max_val[c]) - rem;
-                                const bool ok = c != a && conflicts + dc == 0 && score + ds < best;
+                                const bool ok = c != a && dc == need_dc && ds < dsmax;
                                 const int G = ok ? (ds << S) + Tt * dc : INT_MAX;
                                 cnt = (G < m) ? 1 : cnt + (G == m && ok);
                                 m = min(m, G);
