@@ -390,12 +390,33 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     rcnt[v] = (uint16_t)cnt;
                 }
                 __syncthreads();
-                if (warp == 0) {
-                    // prefix-min over rows in vertex order (chunks of 32 rows)
-                    double carry = INF, lmin = INF;
-                    int lT = 0, lfirst = INT_MAX, tsum = 0, nlow = 0;
-                    for (int base = 0; base < n; base += 32) {
-                        const int v = base + lane;
+                // prefix-min over the rows in vertex order, parallel over the warps:
+                // chunks of 32 rows (warp w: chunks w, w + NW, ...); (1) chunk
+                // minima; (2) each warp enters its chunks with the minimum of the
+                // chunks before, counts the tie events of rows equal to the running
+                // minimum and walks the rows that lower it; (3) warp 0 combines.
+                double *s_cmin = lowR;  // chunk minima (n >= #chunks)
+                __shared__ double s_wmin[NW];
+                __shared__ int s_wT[NW], s_wfirst[NW], s_wtsum[NW];
+                const int nch = (n + 31) >> 5;
+                for (int cb = warp; cb < nch; cb += NW) {
+                    const int v = cb * 32 + lane;
+                    double x = v < n ? rmin[v] : INF;
+                    for (int o = 16; o > 0; o >>= 1) x = fmin(x, __longlong_as_double(__shfl_xor_sync(
+                                                                     FULL, __double_as_longlong(x), o)));
+                    if (lane == 0) s_cmin[cb] = x;
+                }
+                __syncthreads();
+                {
+                    double lmin = INF;
+                    int lT = 0, lfirst = INT_MAX, tsum = 0;
+                    for (int cb = warp; cb < nch; cb += NW) {
+                        // running minimum entering this chunk
+                        double cin = INF;
+                        for (int j = lane; j < cb; j += 32) cin = fmin(cin, s_cmin[j]);
+                        for (int o = 16; o > 0; o >>= 1) cin = fmin(cin, __longlong_as_double(__shfl_xor_sync(
+                                                                           FULL, __double_as_longlong(cin), o)));
+                        const int v = cb * 32 + lane;
                         const double x = v < n ? rmin[v] : INF;
                         const int nq = v < n ? rcnt[v] : 0;
                         double incl = x;
@@ -405,7 +426,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                         }
                         double excl = shfl_up_d(incl, 1);
                         if (lane == 0) excl = INF;
-                        const double RM = fmin(carry, excl);
+                        const double RM = fmin(cin, excl);
                         if (x < lmin) {
                             lmin = x;
                             lT = nq;
@@ -418,52 +439,70 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                             if (x == RM) tsum += nq;
                             else if (x < RM) low = true;
                         }
-                        const unsigned lb = __ballot_sync(FULL, low);
-                        if (low) {
-                            const int pos = nlow + __popc(lb & ((1u << lane) - 1u));
-                            lowq[pos] = v;
-                            lowR[pos] = RM;
-                        }
-                        nlow += __popc(lb);
-                        carry = fmin(carry, shfl_d(incl, 31));
-                    }
-                    __syncwarp();
-                    // walk the rows that lower the running minimum (lanes over colours)
-                    for (int j = 0; j < nlow; j++) {
-                        const int v = lowq[j];
-                        const double R = lowR[j];
-                        const int a = assign[v];
-                        const long long rem = (wrk[v] == max_rank[a]) ? uniq_drop[a] : 0;
-                        const uint16_t *row = gamma + (size_t)v * k;
-                        const int gva = row[a];
-                        const bool frozen = (uint64_t)it < tabu_until[v];
-                        const long long wv = wgt[v];
-                        double cr = R;
-                        int t = 0;
-                        for (int c0 = 0; c0 < k; c0 += 32) {
-                            const int c = c0 + lane;
-                            double gv = INF;
-                            if (c < k && c != a) {
-                                const long long dc = (long long)row[c] - gva;
-                                long long dadd = wv - max_val[c];
-                                if (dadd < 0) dadd = 0;
-                                const long long ds = dadd - rem;
-                                if (!(frozen && (conflicts + dc != 0 || score + ds >= best)))
-                                    gv = gval(gm, ds, dc);
+                        // walk the rows that lower the running minimum (lanes over colours)
+                        unsigned lb = __ballot_sync(FULL, low);
+                        while (lb) {
+                            const int src = __ffs(lb) - 1;
+                            lb &= lb - 1;
+                            const int wvx = cb * 32 + src;
+                            const double R = shfl_d(RM, src);
+                            const int a = assign[wvx];
+                            const long long rem = (wrk[wvx] == max_rank[a]) ? uniq_drop[a] : 0;
+                            const uint16_t *row = gamma + (size_t)wvx * k;
+                            const int gva = row[a];
+                            const bool frozen = (uint64_t)it < tabu_until[wvx];
+                            const long long wv = wgt[wvx];
+                            double cr = R;
+                            int t = 0;
+                            for (int c0 = 0; c0 < k; c0 += 32) {
+                                const int c = c0 + lane;
+                                double gv = INF;
+                                if (c < k && c != a) {
+                                    const long long dc = (long long)row[c] - gva;
+                                    long long dadd = wv - max_val[c];
+                                    if (dadd < 0) dadd = 0;
+                                    const long long ds = dadd - rem;
+                                    if (!(frozen && (conflicts + dc != 0 || score + ds >= best)))
+                                        gv = gval(gm, ds, dc);
+                                }
+                                double inc2 = gv;
+                                for (int o = 1; o < 32; o <<= 1) {
+                                    const double tt = shfl_up_d(inc2, o);
+                                    if (lane >= o) inc2 = fmin(inc2, tt);
+                                }
+                                double ex2 = shfl_up_d(inc2, 1);
+                                if (lane == 0) ex2 = INF;
+                                const double cur = fmin(cr, ex2);
+                                if (gv != INF && gv == cur) t++;
+                                cr = fmin(cr, shfl_d(inc2, 31));
                             }
-                            double incl = gv;
-                            for (int o = 1; o < 32; o <<= 1) {
-                                const double tt = shfl_up_d(incl, o);
-                                if (lane >= o) incl = fmin(incl, tt);
-                            }
-                            double excl = shfl_up_d(incl, 1);
-                            if (lane == 0) excl = INF;
-                            const double cur = fmin(cr, excl);
-                            if (gv != INF && gv == cur) t++;
-                            cr = fmin(cr, shfl_d(incl, 31));
+                            tsum += (lane == 0) ? __reduce_add_sync(FULL, t) : (__reduce_add_sync(FULL, t), 0);
                         }
-                        tsum += __reduce_add_sync(FULL, t) * (lane == 0 ? 1 : 0);
                     }
+                    // warp partials: minimum, its multiplicity, first row, tie events
+                    double wm = lmin;
+                    for (int o = 16; o > 0; o >>= 1)
+                        wm = fmin(wm, __longlong_as_double(__shfl_xor_sync(FULL, __double_as_longlong(wm), o)));
+                    const int wT = __reduce_add_sync(FULL, lmin == wm ? lT : 0);
+                    const int wf = (int)__reduce_min_sync(FULL, (unsigned)(lmin == wm ? lfirst : INT_MAX));
+                    const int wts = __reduce_add_sync(FULL, tsum);
+                    if (lane == 0) {
+                        s_wmin[warp] = wm;
+                        s_wT[warp] = wT;
+                        s_wfirst[warp] = wf;
+                        s_wtsum[warp] = wts;
+                    }
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    // lane w carries warp w's partials into the combination below
+                    double lmin = lane < NW ? s_wmin[lane] : INF;
+                    const int lT = lane < NW ? s_wT[lane] : 0;
+                    const int lfirst = lane < NW ? s_wfirst[lane] : INT_MAX;
+                    const int tsum = lane < NW ? s_wtsum[lane] : 0;
+                    double carry = lmin;
+                    for (int o = 16; o > 0; o >>= 1)
+                        carry = fmin(carry, __longlong_as_double(__shfl_xor_sync(FULL, __double_as_longlong(carry), o)));
                     const double D = carry;
                     int mv_v = -1, mv_b = 0;
                     long long mv_ds = 0, mv_dc = 0;
