@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                                 const unsigned long long c0 = ctr + (unsigned long long)(total - (T - 1));
                                 int smax = 1;
                                 for (int s = 2 + lane; s <= T; s += 32)
-                                    if (below_is_zero(key, c0 + (unsigned long long)(s - 2), (uint32_t)s))
+                                    if (mod_is_zero(stream_value(key, c0 + (unsigned long long)(s - 2)), (uint32_t)s))
                                         smax = s;
                                 sstar = __reduce_max_sync(FULL, smax);
                             } else {
@@ -527,7 +527,28 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                             }
                         }
                         int row = L, need = 1;
-                        if (sstar > 1) {
+                        const int nchk = (n + 31) >> 5;
+                        if (sstar > 1 && nchk <= 32) {
+                            // lane = chunk of 32 rows: D-candidate counts per chunk, one scan
+                            // over the chunks, one within the chosen chunk
+                            int cs = 0;
+                            if (lane < nchk)
+                                for (int r = 0; r < 32; r++) {
+                                    const int vv = lane * 32 + r;
+                                    if (vv < n && rmin[vv] == D) cs += rcnt[vv];
+                                }
+                            const int ci = warp_incl_sum(cs, lane);
+                            const unsigned cb = __ballot_sync(FULL, ci >= sstar);
+                            const int ch = __ffs(cb) - 1;
+                            const int before = __shfl_sync(FULL, ci - cs, ch);
+                            const int vv = ch * 32 + lane;
+                            const int c = (vv < n && rmin[vv] == D) ? rcnt[vv] : 0;
+                            const int incl = warp_incl_sum(c, lane);
+                            const unsigned bm = __ballot_sync(FULL, before + incl >= sstar);
+                            const int src = __ffs(bm) - 1;
+                            row = ch * 32 + src;
+                            need = sstar - before - __shfl_sync(FULL, incl - c, src);
+                        } else if (sstar > 1) {
                             int cum = 0;
                             for (int base = 0; base < n; base += 32) {
                                 const int v = base + lane;
