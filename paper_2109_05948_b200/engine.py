@@ -1,0 +1,124 @@
+"""Device-resident generation of the memetic loop.
+
+One generation of `mc/engine.py:_generation_loop` (:203-316) for the
+k-colouring problem without the surrogate (the reference's ablation setting,
+`use_surrogate=False`, `mc/crossover.py:103-131`), with every array kept in
+HBM between the operators:
+
+    LS          improve_population -> TabuCol from the offspring     (:205-214)
+    distances   pairwise_distances(pop, improved)                    (:287-289)
+    pool        update_population(pop, improved, fitness, ...)      (:290)
+    matching    match_parents(pop, K)                                (:294)
+    offspring   build_offspring_batch + uniform selection           (:295-301)
+
+Same keys as the reference: LS `stream_key(seed, TAG_LS, t, i)`, GPX
+`stream_key(seed, TAG_CROSS, t, i K + j)`, selection
+`Stream.derive(seed, TAG_SELECT, t, i).below(K)`.  The state after every
+generation is bit-identical to the reference's (tests/test_engine_gpu.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import device as Dv
+from .population import min_spacing
+from .rng import TAG_CROSS, TAG_LS, TAG_SELECT, stream_keys
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+@dataclass
+class ColState:
+    """Population (assigns, fitness, distance matrix) and the offspring that
+    the next generation's local search starts from -- all device tensors."""
+
+    pop_assigns: torch.Tensor  # int32 [p, n]
+    pop_fitness: torch.Tensor  # int64 [p]
+    pop_dist: torch.Tensor  # int32 [p, p]
+    offspring: torch.Tensor  # int32 [p, n]
+    k: int
+    generation: int = 0
+    best_score: int = 2 ** 62
+
+    @property
+    def p(self):
+        return self.pop_assigns.shape[0]
+
+    @property
+    def n(self):
+        return self.pop_assigns.shape[1]
+
+
+def init_state(dg, init_assigns, k):
+    """`Population.from_colorings` of the initial colourings (`mc/population.py:47-56`)
+    with their conflict counts as fitness; the first offspring are the same
+    colourings (`mc/engine.py:199`)."""
+    a = torch.as_tensor(np.ascontiguousarray(init_assigns, dtype=np.int32)).to(dg.device)
+    p = a.shape[0]
+    _, within = Dv.pairwise(a[:0], a, k)
+    # conflicts of each colouring from scratch: edges with equal colours
+    fit = (a[:, dg.eu.long()] == a[:, dg.ev.long()]).sum(dim=1).to(torch.int64)
+    st = ColState(pop_assigns=a.clone(), pop_fitness=fit, pop_dist=within, offspring=a.clone(), k=k)
+    st.best_score = int(fit.min().item()) if p else 2 ** 62
+    return st
+
+
+def col_generation(dg, st, *, seed, depth, K, ms=None, timings=None):
+    """Advance `st` by one generation in place; returns the LS outputs."""
+    p, n, k, t = st.p, st.n, st.k, st.generation
+    dev = st.pop_assigns.device
+    ms = min_spacing(n) if ms is None else ms
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if timings is not None else None
+
+    def mark(i):
+        if ev:
+            ev[i].record()
+
+    mark(0)
+    keys = Dv.keys_to_tensor(stream_keys(seed, TAG_LS, t, p), dev)
+    ls = Dv.tabucol_batch(dg, st.offspring.clone(), k, keys, depth)
+    improved, imp_fit = ls["best_assigns"], ls["best_conflicts"]
+    st.best_score = min(st.best_score, int(imp_fit.min().item()))
+    mark(1)
+    cross, within = Dv.pairwise(st.pop_assigns, improved, k)
+    mark(2)
+    adm = torch.empty(p, dtype=torch.int32, device=dev)
+    rule = torch.empty(p, dtype=torch.uint8, device=dev)
+    new_dist = torch.empty((p, p), dtype=torch.int32, device=dev)
+    new_assigns = torch.empty((p, n), dtype=torch.int32, device=dev)
+    new_fit = torch.empty(p, dtype=torch.int64, device=dev)
+    P = N.ptr
+    N.check(N.lib().mcb_update_population(
+        P(st.pop_dist), P(cross), P(within), P(st.pop_fitness), P(imp_fit), p, p, int(ms),
+        P(st.pop_assigns), P(improved), n, P(adm), P(rule), P(new_dist), P(new_assigns), P(new_fit),
+        _stream()))
+    st.pop_assigns, st.pop_fitness, st.pop_dist = new_assigns, new_fit, new_dist
+    mark(3)
+    matches = torch.empty((p, K), dtype=torch.int64, device=dev)
+    N.check(N.lib().mcb_match_parents(P(st.pop_dist), p, int(K), n, P(matches), _stream()))
+    mark(4)
+    ck = Dv.keys_to_tensor(stream_keys(seed, TAG_CROSS, t, p * K), dev)
+    cands = Dv.gpx_batch(st.pop_assigns, matches, k, ck)
+    # uniform selection: Stream.derive(seed, TAG_SELECT, t, i).below(K) = stream_value(key, 0) % K
+    sk = Dv.keys_to_tensor(stream_keys(seed, TAG_SELECT, t, p), dev)
+    sv = torch.empty(p, dtype=torch.int64, device=dev)
+    zeros = torch.zeros(p, dtype=torch.int64, device=dev)
+    N.check(N.lib().mcb_stream_values(P(sk), P(zeros), P(sv), p, _stream()))
+    hi, lo = (sv >> 32) & 0xFFFFFFFF, sv & 0xFFFFFFFF  # unsigned 64-bit value mod K in int64
+    sel = ((hi % K) * ((1 << 32) % K) + lo % K) % K
+    st.offspring = cands[torch.arange(p, device=dev), sel].contiguous()
+    mark(5)
+    st.generation = t + 1
+    if timings is not None:
+        torch.cuda.synchronize()
+        for name, i in (("ls", 0), ("distances", 1), ("update_population", 2), ("match_parents", 3),
+                        ("offspring", 4)):
+            timings[name] = timings.get(name, 0.0) + ev[i].elapsed_time(ev[i + 1]) / 1e3
+    return ls

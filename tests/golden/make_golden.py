@@ -16,6 +16,8 @@ inputs, the outputs of the reference's own hot-path kernels:
 * gpx.npz       build_offspring_batch / gpx (`crossover.py:69-93`)
 * distance.npz  pairwise_distances / approx_partition_distance (`distance.py:75-155`)
 * population.npz  update_population / match_parents (`population.py:59-141`)
+* engine.npz    k-colouring generations without the surrogate, chained from the
+                reference's own operators as `engine.py:_generation_loop` does
 
 Inputs are regenerated in the tests from the recorded parameters with the
 package's own generators (which are themselves pinned by graphs.npz and the
@@ -291,6 +293,53 @@ def gen_population(out):
     out["cases"] = np.array([c[0] for c in POP_CASES])
 
 
+# --------------------------------------------------------------------------
+# engine: generations of mc/engine.py:_generation_loop (:203-316) for COL with
+# use_surrogate=False, chained from the reference's own functions
+#   (name, seed, n, p_edge, k, p, K, depth, generations)
+# --------------------------------------------------------------------------
+ENGINE_CASES = [
+    ("e1", 3, 70, 0.5, 9, 12, 3, 400, 4),
+    ("e2", 5, 90, 0.3, 6, 16, 5, 600, 3),
+]
+
+
+def gen_engine(out):
+    from memcolor.coloring import Coloring as RC
+    from memcolor.coloring import col_conflicts as rcc
+    from memcolor.crossover import build_and_select_offspring
+    from memcolor.distance import pairwise_distances as rpd
+    from memcolor.init import init_col_population
+
+    for name, seed, n, pe, k, p, K, depth, G in ENGINE_CASES:
+        g = ref_rand_graph(seed, n, pe)
+        init = init_col_population(n, k, p, seed)
+        fit = np.array([rcc(g, c) for c in init.colorings], dtype=np.int64)
+        pop = RPOP.Population.from_colorings(init.colorings, fit)
+        ms = RPOP.min_spacing(n)
+        offspring = list(init.colorings)
+        pre = name + "__"
+        out[pre + "params"] = np.array([seed, n, int(pe * 1000), k, p, K, depth, G], dtype=np.int64)
+        out[pre + "init"] = pop.assigns.astype(np.int32)
+        for t in range(G):
+            res = RLS.improve_population(g, offspring, RLS.COL, seed, generation=t, depth=depth)
+            imp = np.stack([r.best.assign for r in res]).astype(np.int32)
+            imp_fit = np.array([min(r.best_score, int(RLS.INF_SCORE)) for r in res], dtype=np.int64)
+            cross, within = rpd(pop.assigns, imp, k=k)
+            pop = RPOP.update_population(pop, imp, imp_fit, cross, within, ms)
+            matches = RPOP.match_parents(pop, K)
+            batch = build_and_select_offspring(pop, matches, None, seed, t, use_surrogate=False)
+            offspring = [RC(batch.selected_assigns[i], k) for i in range(p)]
+            out[pre + f"g{t}_improved"] = imp
+            out[pre + f"g{t}_pop"] = pop.assigns.astype(np.int32)
+            out[pre + f"g{t}_fit"] = pop.fitness.astype(np.int64)
+            out[pre + f"g{t}_dist"] = pop.dist.astype(np.int32)
+            out[pre + f"g{t}_matches"] = matches.astype(np.int64)
+            out[pre + f"g{t}_selected"] = batch.selected_index.astype(np.int64)
+            out[pre + f"g{t}_offspring"] = batch.selected_assigns.astype(np.int32)
+    out["cases"] = np.array([c[0] for c in ENGINE_CASES])
+
+
 def gen_rng(out):
     rows = []
     for seed, tag, idx in [(1, 2, (0, 0)), (1, 1, (0,)), (2024, 2, (5, 11)), (7, 1, ()),
@@ -321,7 +370,7 @@ def main():
     only = set(sys.argv[1:])
     for fn, name in [(gen_rng, "rng"), (gen_graphs, "graphs"), (gen_tabucol, "tabucol"),
                      (gen_wvcp, "wvcp"), (gen_gpx, "gpx"), (gen_distance, "distance"),
-                     (gen_population, "population")]:
+                     (gen_population, "population"), (gen_engine, "engine")]:
         if only and name not in only:
             continue
         out = {}
