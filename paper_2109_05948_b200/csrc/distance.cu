@@ -8,14 +8,16 @@
 // matches; distance = n - total.
 //
 // Here the same greedy is evaluated without sorting k^2 cells:
-//   * M lives in shared memory as u16 counters (one warp-private tile);
+//   * M lives in shared memory as u16 counters (one warp-private tile); the
+//     first increment of a cell appends it to a compact list of the (<= n)
+//     nonzero cells, so no pass ever scans the k^2 tile;
 //   * entries >= 32 (at most n/32 of them, since they sum to <= n) are sorted
 //     explicitly and taken first, in the reference order;
 //   * every smaller value x = 31..1 is one "level": within a level the
 //     reference visits cells in flat order, i.e. rows ascending and, inside a
 //     row, columns ascending -- so a free row takes its lowest free column
-//     holding x.  Per-row bitmasks of the values present let a level skip
-//     rows without x, and a ballot over a row's columns finds that column.
+//     holding x.  The level's cells are scattered into row -> column bitmasks
+//     and one lane walks the free rows holding x with bit operations.
 // Zero cells add nothing to the total, so they are never visited.
 // The job space and the cross/within unranking are the reference's own
 // (:94-113), so ranks shard it by contiguous [job_begin, job_end) ranges.
@@ -29,46 +31,61 @@ namespace mcb {
 
 constexpr int PD_WARPS = 4;
 
+// Per-warp shared tile: the k x k overlap histogram (u8 counters, or u16 when
+// WIDE), the nonzero cells in first-touch order and bucketed by value, the
+// per-level row -> column and column -> row bitmasks, the explicit list of
+// entries >= 32 and the level counters.
 struct PdLayout {
-    size_t hist_words, rowlev, used, big, per;
+    size_t hist_words, list_words, big, cmask, per;
 };
 
-__host__ __device__ inline PdLayout pd_layout(int n, int k) {
+__host__ __device__ inline PdLayout pd_layout(int n, int k, bool wide) {
     PdLayout L;
-    L.hist_words = ((size_t)k * k + 1) / 2;
-    L.rowlev = (size_t)k;
-    L.used = 16;  // 8 row words + 8 column words (k <= 255)
+    const size_t kk = (size_t)k * k;
+    L.hist_words = wide ? (kk + 1) / 2 : (kk + 3) / 4;
+    L.list_words = ((size_t)n + 1) / 2;        // u16 (r << 8 | c) per cell
     L.big = (size_t)n / 32 + 2;
-    L.per = (L.hist_words + L.rowlev + L.used + L.big + 4) * 4;
+    L.cmask = (size_t)k * ((k + 31) / 32);
+    // hist + list + bucket + big + cmask + rmask + lvbeg[32] + lvcur[32] + rowused/colused[16] + bigcnt
+    L.per = (L.hist_words + 2 * L.list_words + L.big + 2 * L.cmask + 32 + 32 + 16 + 4) * 4;
     L.per = (L.per + 15) & ~(size_t)15;
     return L;
 }
 
+template <bool WIDE>
+__device__ __forceinline__ uint32_t hist_get(const uint32_t *hist, int flat) {
+    if (WIDE) return (hist[flat >> 1] >> (16 * (flat & 1))) & 0xFFFFu;
+    return (hist[flat >> 2] >> (8 * (flat & 3))) & 0xFFu;
+}
+
+template <int KWD, bool WIDE>
 __global__ void __launch_bounds__(PD_WARPS * 32)
     pairwise_kernel(const int32_t *__restrict__ pop, int64_t p, const int32_t *__restrict__ off,
                     int64_t q, int n, int k, int32_t *__restrict__ cross,
                     int32_t *__restrict__ within, int64_t job_begin, int64_t job_end,
                     int32_t *err) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const PdLayout L = pd_layout(n, k);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const PdLayout L = pd_layout(n, k, WIDE);
     uint32_t *hist = reinterpret_cast<uint32_t *>(smem + warp * L.per);
-    uint32_t *rowlev = hist + L.hist_words;
-    uint32_t *rowused = rowlev + L.rowlev;
-    uint32_t *colused = rowused + 8;
-    uint32_t *big = colused + 8;
-    uint32_t *bigcnt = big + L.big;
-    const int kk = k * k;
+    uint16_t *list = reinterpret_cast<uint16_t *>(hist + L.hist_words);
+    uint16_t *bucket = list + 2 * L.list_words;
+    uint32_t *big = reinterpret_cast<uint32_t *>(bucket + 2 * L.list_words);
+    uint32_t *cmask = big + L.big;   // [k][KWD]: row r -> columns holding the level
+    uint32_t *rmask = cmask + L.cmask;  // [k][KWD]: column c -> rows holding the level
+    uint32_t *lvbeg = rmask + L.cmask;
+    uint32_t *lvcur = lvbeg + 32;
+    uint32_t *s_used = lvcur + 32;   // rowused[8], colused[8] (entries >= 32 only)
+    uint32_t *bigcnt = s_used + 16;
+    const uint32_t lt_mask = (1u << lane) - 1u;
 
     for (size_t i = lane; i < L.hist_words; i += 32) hist[i] = 0u;
-    for (int r = lane; r < k; r += 32) rowlev[r] = 0u;
-    if (lane < 16) rowused[lane] = 0u;
-    if (lane == 0) *bigcnt = 0u;
+    for (size_t i = lane; i < 2 * L.cmask; i += 32) cmask[i] = 0u;
     __syncwarp();
 
     const int64_t pq = p * q;
-    for (int64_t job = job_begin + (int64_t)blockIdx.x * PD_WARPS + warp; job < job_end;
-         job += (int64_t)gridDim.x * PD_WARPS) {
+    for (int64_t job = job_begin + (int64_t)blockIdx.x * nwarps + warp; job < job_end;
+         job += (int64_t)gridDim.x * nwarps) {
         const int32_t *x, *y;
         int64_t oi, oj;
         bool is_cross = job < pq;
@@ -91,54 +108,86 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
             x = off + (size_t)oi * n;
             y = off + (size_t)oj * n;
         }
-        // overlap histogram
-        int bad = 0;
-        for (int v = lane; v < n; v += 32) {
-            const int a = x[v], b = y[v];
-            if (a < 0 || a >= k || b < 0 || b >= k) {
-                bad = 1;
-                continue;
+        lvbeg[lane] = 0u;
+        if (lane == 0) *bigcnt = 0u;
+        // overlap histogram; the first touch of a cell appends it to the list
+        int bad = 0, m = 0;
+        for (int v0 = 0; v0 < n; v0 += 32) {
+            const int v = v0 + lane;
+            bool first = false;
+            uint32_t cell = 0;
+            if (v < n) {
+                const int a = x[v], b = y[v];
+                if (a < 0 || a >= k || b < 0 || b >= k) {
+                    bad |= 1;
+                } else {
+                    const int code = a * k + b;
+                    const uint32_t sh = WIDE ? 16 * (code & 1) : 8 * (code & 3);
+                    const uint32_t old = atomicAdd(&hist[WIDE ? code >> 1 : code >> 2], 1u << sh);
+                    const uint32_t was = (old >> sh) & (WIDE ? 0xFFFFu : 0xFFu);
+                    first = was == 0u;
+                    if (!WIDE && was == 0xFFu) bad |= 2;  // u8 counter overflow
+                    cell = ((uint32_t)a << 8) | (uint32_t)b;
+                }
             }
-            const int code = a * k + b;
-            atomicAdd(&hist[code >> 1], 1u << (16 * (code & 1)));
+            const uint32_t bm = __ballot_sync(0xffffffffu, first);
+            if (first) list[m + __popc(bm & lt_mask)] = (uint16_t)cell;
+            m += __popc(bm);
         }
-        if (__any_sync(0xffffffffu, bad)) {
-            if (lane == 0) atomicExch(err, 1);
-            // clear and skip
+        bad = __reduce_or_sync(0xffffffffu, bad);
+        if (bad) {
+            if (lane == 0) atomicOr(err, bad);
+            __syncwarp();
             for (size_t i = lane; i < L.hist_words; i += 32) hist[i] = 0u;
             __syncwarp();
             continue;
         }
         __syncwarp();
-        // per-row value-presence masks; entries >= 32 go to the explicit list
+        // values: count each level; entries >= 32 go to the explicit list
         uint32_t levels = 0;
-        for (int r = 0; r < k; r++) {
-            uint32_t m = 0;
-            for (int c0 = 0; c0 < k; c0 += 32) {
-                const int c = c0 + lane;
-                if (c < k) {
-                    const int flat = r * k + c;
-                    const uint32_t val = (hist[flat >> 1] >> (16 * (flat & 1))) & 0xFFFFu;
-                    if (val >= 32) {
-                        m |= 1u;
-                        const uint32_t slot = atomicAdd(bigcnt, 1u);
-                        big[slot] = (val << 16) | (uint32_t)(0xFFFF - flat);
-                    } else if (val) {
-                        m |= 1u << val;
-                    }
-                }
+        for (int i = lane; i < m; i += 32) {
+            const uint32_t e = list[i];
+            const int flat = (int)(e >> 8) * k + (int)(e & 0xFFu);
+            const uint32_t val = hist_get<WIDE>(hist, flat);
+            if (val >= 32) {
+                levels |= 1u;
+                const uint32_t slot = atomicAdd(bigcnt, 1u);
+                big[slot] = (val << 16) | (uint32_t)(0xFFFF - flat);
+            } else {
+                levels |= 1u << val;
+                atomicAdd(&lvbeg[val], 1u);
             }
-            m = __reduce_or_sync(0xffffffffu, m);
-            if (lane == 0) rowlev[r] = m;
-            levels |= m;
+        }
+        levels = __reduce_or_sync(0xffffffffu, levels);
+        __syncwarp();
+        {   // bucket offsets: exclusive prefix over the 32 level counts
+            const uint32_t c = lvbeg[lane];
+            uint32_t inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            lvbeg[lane] = inc - c;
+            lvcur[lane] = inc - c;
         }
         __syncwarp();
+        for (int i = lane; i < m; i += 32) {
+            const uint32_t e = list[i];
+            const uint32_t val = hist_get<WIDE>(hist, (int)(e >> 8) * k + (int)(e & 0xFFu));
+            if (val < 32) bucket[atomicAdd(&lvcur[val], 1u)] = (uint16_t)e;
+        }
+        uint32_t rowused[KWD], colused[KWD];
+#pragma unroll
+        for (int w = 0; w < KWD; w++) rowused[w] = colused[w] = 0u;
         long long total = 0;
         int matched = 0;
         // big entries first: sort keys descending (value desc, flat asc)
         if (levels & 1u) {
-            const int nb = (int)*bigcnt;
+            if (lane < 16) s_used[lane] = 0u;
+            __syncwarp();
             if (lane == 0) {
+                const int nb = (int)*bigcnt;
                 for (int a = 1; a < nb; a++) {
                     const uint32_t t = big[a];
                     int b = a - 1;
@@ -152,10 +201,10 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
                     const uint32_t t = big[a];
                     const int flat = 0xFFFF - (int)(t & 0xFFFFu);
                     const int r = flat / k, c = flat % k;
-                    if (((rowused[r >> 5] >> (r & 31)) & 1u) || ((colused[c >> 5] >> (c & 31)) & 1u))
+                    if (((s_used[r >> 5] >> (r & 31)) & 1u) || ((s_used[8 + (c >> 5)] >> (c & 31)) & 1u))
                         continue;
-                    rowused[r >> 5] |= 1u << (r & 31);
-                    colused[c >> 5] |= 1u << (c & 31);
+                    s_used[r >> 5] |= 1u << (r & 31);
+                    s_used[8 + (c >> 5)] |= 1u << (c & 31);
                     total += t >> 16;
                     matched++;
                 }
@@ -163,44 +212,85 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
             total = __shfl_sync(0xffffffffu, total, 0);
             matched = __shfl_sync(0xffffffffu, matched, 0);
             __syncwarp();
+#pragma unroll
+            for (int w = 0; w < KWD; w++) {
+                rowused[w] = s_used[w];
+                colused[w] = s_used[8 + w];
+            }
         }
-        // levels 31..1, rows ascending, lowest free column
+        __syncwarp();
+        // levels 31..1.  Within a level the reference visits cells in flat
+        // order (rows ascending, then columns ascending).  That greedy equals
+        // repeated rounds in which every free row r whose lowest free column c
+        // (at this level) has r as its lowest free row takes (r, c): such a
+        // cell precedes every other live cell in its row and column, so the
+        // ordered greedy takes it too, and removing it leaves the rest of the
+        // greedy unchanged.  Rows are lanes (r = lane + 32 j).
         uint32_t lv = levels & ~1u;
         while (lv && matched < k) {
             const int xval = 31 - __clz(lv);
             lv &= ~(1u << xval);
-            for (int r0 = 0; r0 < k && matched < k; r0 += 32) {
-                const int r = r0 + lane;
-                const bool has = r < k && ((rowlev[r] >> xval) & 1u) &&
-                                 !((rowused[r >> 5] >> (r & 31)) & 1u);
-                uint32_t rows = __ballot_sync(0xffffffffu, has);
-                while (rows) {
-                    const int rr = r0 + __ffs(rows) - 1;
-                    rows &= rows - 1u;
-                    int found = -1;
-                    for (int c0 = 0; c0 < k && found < 0; c0 += 32) {
-                        const int c = c0 + lane;
-                        bool ok = false;
-                        if (c < k) {
-                            const int flat = rr * k + c;
-                            const uint32_t val = (hist[flat >> 1] >> (16 * (flat & 1))) & 0xFFFFu;
-                            ok = val == (uint32_t)xval && !((colused[c >> 5] >> (c & 31)) & 1u);
+            const int beg = (int)lvbeg[xval], end = (int)lvcur[xval];
+            for (int i = beg + lane; i < end; i += 32) {
+                const uint32_t e = bucket[i];
+                const int r = (int)(e >> 8), c = (int)(e & 0xFFu);
+                atomicOr(&cmask[r * KWD + (c >> 5)], 1u << (c & 31));
+                atomicOr(&rmask[c * KWD + (r >> 5)], 1u << (r & 31));
+            }
+            __syncwarp();
+            while (true) {
+                bool act = false;
+                int col[KWD];
+#pragma unroll
+                for (int j = 0; j < KWD; j++) {
+                    col[j] = -1;
+                    const int r = lane + 32 * j;
+                    if (r < k && !((rowused[j] >> lane) & 1u)) {
+                        int c = -1;
+#pragma unroll
+                        for (int w = KWD - 1; w >= 0; w--) {
+                            const uint32_t av = cmask[r * KWD + w] & ~colused[w];
+                            if (av) c = 32 * w + __ffs(av) - 1;
                         }
-                        const uint32_t bm = __ballot_sync(0xffffffffu, ok);
-                        if (bm) found = c0 + __ffs(bm) - 1;
-                    }
-                    if (found >= 0) {
-                        if (lane == 0) {
-                            rowused[rr >> 5] |= 1u << (rr & 31);
-                            colused[found >> 5] |= 1u << (found & 31);
+                        if (c >= 0) {
+                            act = true;
+                            int r2 = -1;
+#pragma unroll
+                            for (int w = KWD - 1; w >= 0; w--) {
+                                const uint32_t fr = rmask[c * KWD + w] & ~rowused[w];
+                                if (fr) r2 = 32 * w + __ffs(fr) - 1;
+                            }
+                            if (r2 == r) col[j] = c;
                         }
-                        __syncwarp();
-                        total += xval;
-                        matched++;
-                        if (matched >= k) break;
                     }
                 }
+                if (!__any_sync(0xffffffffu, act)) break;
+                int took = 0;
+#pragma unroll
+                for (int j = 0; j < KWD; j++) {
+                    const uint32_t tb = __ballot_sync(0xffffffffu, col[j] >= 0);
+                    rowused[j] |= tb;
+                    took += __popc(tb);
+                }
+#pragma unroll
+                for (int w = 0; w < KWD; w++) {
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int j = 0; j < KWD; j++)
+                        if (col[j] >= 0 && (col[j] >> 5) == w) mine |= 1u << (col[j] & 31);
+                    colused[w] |= __reduce_or_sync(0xffffffffu, mine);
+                }
+                total += (long long)xval * took;
+                matched += took;
+                if (matched >= k) break;
             }
+            for (int i = beg + lane; i < end; i += 32) {
+                const uint32_t e = bucket[i];
+                const int r = (int)(e >> 8), c = (int)(e & 0xFFu);
+                cmask[r * KWD + (c >> 5)] = 0u;
+                rmask[c * KWD + (r >> 5)] = 0u;
+            }
+            __syncwarp();
         }
         const int d = n - (int)total;
         if (lane == 0) {
@@ -211,18 +301,36 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
                 within[oj * q + oi] = d;
             }
         }
-        // reset the warp's tile for the next pair
-        __syncwarp();
-        for (int v = lane; v < n; v += 32) {
-            const int code = x[v] * k + y[v];
-            hist[code >> 1] = 0u;
+        // reset the warp's histogram for the next pair: only its nonzero cells
+        for (int i = lane; i < m; i += 32) {
+            const uint32_t e = list[i];
+            const int flat = (int)(e >> 8) * k + (int)(e & 0xFFu);
+            hist[WIDE ? flat >> 1 : flat >> 2] = 0u;
         }
-        for (int r = lane; r < k; r += 32) rowlev[r] = 0u;
-        if (lane < 16) rowused[lane] = 0u;
-        if (lane == 0) *bigcnt = 0u;
         __syncwarp();
     }
 }
+
+namespace {
+
+using PdKernel = void (*)(const int32_t *, int64_t, const int32_t *, int64_t, int, int, int32_t *,
+                          int32_t *, int64_t, int64_t, int32_t *);
+
+template <bool WIDE>
+PdKernel pd_pick(int kwd) {
+    switch (kwd) {
+        case 1: return pairwise_kernel<1, WIDE>;
+        case 2: return pairwise_kernel<2, WIDE>;
+        case 3: return pairwise_kernel<3, WIDE>;
+        case 4: return pairwise_kernel<4, WIDE>;
+        case 5: return pairwise_kernel<5, WIDE>;
+        case 6: return pairwise_kernel<6, WIDE>;
+        case 7: return pairwise_kernel<7, WIDE>;
+        default: return pairwise_kernel<8, WIDE>;
+    }
+}
+
+}  // namespace
 
 int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n, int64_t k,
                  int32_t *cross, int32_t *within, int64_t job_begin, int64_t job_end,
@@ -234,30 +342,38 @@ int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, i
     if (job_begin >= job_end || n == 0) return MCB_OK;
     if (k < 1) return set_error(MCB_ERR_VALUE, "pairwise: k must be >= 1");
     if (k > 255 || n > 65535) return set_error(MCB_ERR_UNSUPPORTED, "pairwise: k<=255, n<=65535");
-    const PdLayout L = pd_layout((int)n, (int)k);
-    const size_t smem = PD_WARPS * L.per;
-    if (smem > (size_t)max_smem_optin())
-        return set_error(MCB_ERR_UNSUPPORTED, "pairwise: k too large for shared memory");
-    if (cudaFuncSetAttribute(pairwise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return set_error(MCB_ERR_CUDA, "pairwise: smem attribute failed");
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pairwise_kernel, PD_WARPS * 32, smem);
-    nb = std::max(nb, 1);
-    const int64_t jobs = job_end - job_begin;
-    const int grid = (int)std::min<int64_t>((jobs + PD_WARPS - 1) / PD_WARPS, (int64_t)nb * num_sms());
     int32_t *err = (int32_t *)workspace(256);
     if (!err) return set_error(MCB_ERR_CUDA, "pairwise: workspace");
-    cudaMemsetAsync(err, 0, 4, st);
-    pairwise_kernel<<<grid, PD_WARPS * 32, smem, st>>>(pop, p, off, q, (int)n, (int)k, cross, within,
-                                                       job_begin, job_end, err);
-    int32_t herr = 0;
-    if (cudaGetLastError() != cudaSuccess ||
-        cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess)
-        return set_error(MCB_ERR_CUDA, "pairwise kernel failed: %s",
-                         cudaGetErrorString(cudaGetLastError()));
-    if (herr) return set_error(MCB_ERR_RANGE, "pairwise: color id out of range [0, k)");
+    // u8 counters first; a launch in which some class overlap reached 256
+    // (possible only when n >= 256) is re-run with u16 counters
+    for (int wide = 0; wide < 2; wide++) {
+        const PdLayout L = pd_layout((int)n, (int)k, wide);
+        // warps per block: as many of PD_WARPS as shared memory holds
+        int warps = PD_WARPS;
+        while (warps > 1 && (size_t)warps * L.per > (size_t)max_smem_optin()) warps >>= 1;
+        const size_t smem = warps * L.per;
+        if (smem > (size_t)max_smem_optin())
+            return set_error(MCB_ERR_UNSUPPORTED, "pairwise: k too large for shared memory");
+        const PdKernel kern = wide ? pd_pick<true>((int)(k + 31) / 32) : pd_pick<false>((int)(k + 31) / 32);
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return set_error(MCB_ERR_CUDA, "pairwise: smem attribute failed");
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, warps * 32, smem);
+        nb = std::max(nb, 1);
+        const int64_t jobs = job_end - job_begin;
+        const int grid = (int)std::min<int64_t>((jobs + warps - 1) / warps, (int64_t)nb * num_sms());
+        cudaMemsetAsync(err, 0, 4, st);
+        kern<<<grid, warps * 32, smem, st>>>(pop, p, off, q, (int)n, (int)k, cross, within, job_begin,
+                                                job_end, err);
+        int32_t herr = 0;
+        if (cudaGetLastError() != cudaSuccess ||
+            cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return set_error(MCB_ERR_CUDA, "pairwise kernel failed: %s",
+                             cudaGetErrorString(cudaGetLastError()));
+        if (herr & 1) return set_error(MCB_ERR_RANGE, "pairwise: color id out of range [0, k)");
+        if (!(herr & 2)) break;
+    }
     (void)flags;
     return MCB_OK;
 }

@@ -109,3 +109,22 @@ def test_gpx_rows_sharding_matches_full():
         kk = D.keys_to_tensor(keys[lo * 4:hi * 4], "cuda")
         parts.append(D.gpx_rows(pop, m, lo, 30, kk).cpu().numpy())
     np.testing.assert_array_equal(np.concatenate(parts), full)
+
+
+@pytest.mark.parametrize("n,k", [(1100, 2), (700, 3), (1000, 12), (1000, 83), (3000, 200), (2000, 255)])
+def test_distance_structured_vs_oracle(n, k, oracle_lib):
+    """Permuted copies with noise: many overlap levels per pair, entries >= 32
+    (small k), u8 counter overflow -> the u16 re-run (k = 2, 3), and every
+    column-word count KWD = ceil(k / 32) up to 8."""
+    rs = np.random.default_rng(n + k)
+    P = random_col_assigns(n, k, 6, n)
+    Q = np.empty((7, n), np.int32)
+    for j in range(7):
+        src = P[j % 6]
+        Q[j] = rs.permutation(k)[src]
+        noise = rs.random(n) < (0.05 + 0.1 * j)
+        Q[j, noise] = rs.integers(0, k, int(noise.sum()))
+    c, w = DI.pairwise_distances(P, Q, k=k)
+    rc, rw = oracle_lib.pairwise(P, Q, k)
+    np.testing.assert_array_equal(c, rc)
+    np.testing.assert_array_equal(w, rw)
