@@ -58,10 +58,34 @@ __device__ __forceinline__ uint32_t hist_get(const uint32_t *hist, int flat) {
     return (hist[flat >> 2] >> (8 * (flat & 3))) & 0xFFu;
 }
 
+// colour ids -> u8 rows of NB (multiple of 16) bytes, range-checked once per
+// colouring instead of once per pair
+__global__ void pd_to_u8_kernel(const int32_t *__restrict__ src, int64_t rows, int n, int nb, int k,
+                                uint8_t *__restrict__ dst, int32_t *err) {
+    const int64_t words = rows * (nb / 4);
+    int bad = 0;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = w / (nb / 4);
+        const int v0 = (int)(w - row * (nb / 4)) * 4;
+        uint32_t out = 0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            if (v0 + b < n) {
+                const int a = src[row * n + v0 + b];
+                if (a < 0 || a >= k) bad = 1;
+                out |= (uint32_t)(a & 0xFF) << (8 * b);
+            }
+        }
+        reinterpret_cast<uint32_t *>(dst)[w] = out;
+    }
+    if (bad) atomicOr(err, 1);
+}
+
 template <int KWD, bool WIDE>
 __global__ void __launch_bounds__(PD_WARPS * 32)
-    pairwise_kernel(const int32_t *__restrict__ pop, int64_t p, const int32_t *__restrict__ off,
-                    int64_t q, int n, int k, int32_t *__restrict__ cross,
+    pairwise_kernel(const uint8_t *__restrict__ pop, int64_t p, const uint8_t *__restrict__ off,
+                    int64_t q, int n, int nb, int k, int32_t *__restrict__ cross,
                     int32_t *__restrict__ within, int64_t job_begin, int64_t job_end,
                     int32_t *err) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -86,14 +110,14 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
     const int64_t pq = p * q;
     for (int64_t job = job_begin + (int64_t)blockIdx.x * nwarps + warp; job < job_end;
          job += (int64_t)gridDim.x * nwarps) {
-        const int32_t *x, *y;
+        const uint8_t *x, *y;
         int64_t oi, oj;
         bool is_cross = job < pq;
         if (is_cross) {
             oi = job / q;
             oj = job % q;
-            x = pop + (size_t)oi * n;
-            y = off + (size_t)oj * n;
+            x = pop + (size_t)oi * nb;
+            y = off + (size_t)oj * nb;
         } else {
             // unrank r into (i < j) with row i holding q-1-i pairs (:106-112)
             const int64_t r = job - pq;
@@ -105,34 +129,38 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
             while (i + 1 <= q - 2 && S(i + 1) <= r) i++;
             oi = i;
             oj = i + 1 + (r - S(i));
-            x = off + (size_t)oi * n;
-            y = off + (size_t)oj * n;
+            x = off + (size_t)oi * nb;
+            y = off + (size_t)oj * nb;
         }
         lvbeg[lane] = 0u;
         if (lane == 0) *bigcnt = 0u;
-        // overlap histogram; the first touch of a cell appends it to the list
+        // overlap histogram (4 vertices per 32-bit load); the first touch of
+        // a cell appends it to the list
         int bad = 0, m = 0;
-        for (int v0 = 0; v0 < n; v0 += 32) {
-            const int v = v0 + lane;
-            bool first = false;
-            uint32_t cell = 0;
-            if (v < n) {
-                const int a = x[v], b = y[v];
-                if (a < 0 || a >= k || b < 0 || b >= k) {
-                    bad |= 1;
-                } else {
-                    const int code = a * k + b;
+        const int nw = (n + 3) >> 2;
+        for (int w0 = 0; w0 < nw; w0 += 32) {
+            const int w = w0 + lane;
+            uint32_t xa = 0, yb = 0;
+            if (w < nw) {
+                xa = __ldg(reinterpret_cast<const uint32_t *>(x) + w);
+                yb = __ldg(reinterpret_cast<const uint32_t *>(y) + w);
+            }
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                bool first = false;
+                const uint32_t a = (xa >> (8 * b)) & 0xFFu, c = (yb >> (8 * b)) & 0xFFu;
+                if (4 * w + b < n) {
+                    const int code = (int)a * k + (int)c;
                     const uint32_t sh = WIDE ? 16 * (code & 1) : 8 * (code & 3);
                     const uint32_t old = atomicAdd(&hist[WIDE ? code >> 1 : code >> 2], 1u << sh);
                     const uint32_t was = (old >> sh) & (WIDE ? 0xFFFFu : 0xFFu);
                     first = was == 0u;
                     if (!WIDE && was == 0xFFu) bad |= 2;  // u8 counter overflow
-                    cell = ((uint32_t)a << 8) | (uint32_t)b;
                 }
+                const uint32_t bm = __ballot_sync(0xffffffffu, first);
+                if (first) list[m + __popc(bm & lt_mask)] = (uint16_t)((a << 8) | c);
+                m += __popc(bm);
             }
-            const uint32_t bm = __ballot_sync(0xffffffffu, first);
-            if (first) list[m + __popc(bm & lt_mask)] = (uint16_t)cell;
-            m += __popc(bm);
         }
         bad = __reduce_or_sync(0xffffffffu, bad);
         if (bad) {
@@ -313,7 +341,7 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
 
 namespace {
 
-using PdKernel = void (*)(const int32_t *, int64_t, const int32_t *, int64_t, int, int, int32_t *,
+using PdKernel = void (*)(const uint8_t *, int64_t, const uint8_t *, int64_t, int, int, int, int32_t *,
                           int32_t *, int64_t, int64_t, int32_t *);
 
 template <bool WIDE>
@@ -342,8 +370,20 @@ int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, i
     if (job_begin >= job_end || n == 0) return MCB_OK;
     if (k < 1) return set_error(MCB_ERR_VALUE, "pairwise: k must be >= 1");
     if (k > 255 || n > 65535) return set_error(MCB_ERR_UNSUPPORTED, "pairwise: k<=255, n<=65535");
-    int32_t *err = (int32_t *)workspace(256);
-    if (!err) return set_error(MCB_ERR_CUDA, "pairwise: workspace");
+    // u8 copies of both populations (rows padded to 16 bytes) after the flag word
+    const int nb = (int)((n + 15) & ~(int64_t)15);
+    uint8_t *ws = (uint8_t *)workspace(256 + (size_t)(p + q) * nb);
+    if (!ws) return set_error(MCB_ERR_CUDA, "pairwise: workspace");
+    int32_t *err = (int32_t *)ws;
+    uint8_t *pop8 = ws + 256, *off8 = pop8 + (size_t)p * nb;
+    cudaMemsetAsync(err, 0, 4, st);
+    for (int side = 0; side < 2; side++) {
+        const int64_t rows = side ? q : p;
+        if (rows == 0) continue;
+        const int64_t words = rows * (nb / 4);
+        const int g = (int)std::min<int64_t>((words + 255) / 256, (int64_t)num_sms() * 8);
+        pd_to_u8_kernel<<<g, 256, 0, st>>>(side ? off : pop, rows, (int)n, nb, (int)k, side ? off8 : pop8, err);
+    }
     // u8 counters first; a launch in which some class overlap reached 256
     // (possible only when n >= 256) is re-run with u16 counters
     for (int wide = 0; wide < 2; wide++) {
@@ -357,14 +397,13 @@ int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, i
         const PdKernel kern = wide ? pd_pick<true>((int)(k + 31) / 32) : pd_pick<false>((int)(k + 31) / 32);
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return set_error(MCB_ERR_CUDA, "pairwise: smem attribute failed");
-        int nb = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, warps * 32, smem);
-        nb = std::max(nb, 1);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
+        per_sm = std::max(per_sm, 1);
         const int64_t jobs = job_end - job_begin;
-        const int grid = (int)std::min<int64_t>((jobs + warps - 1) / warps, (int64_t)nb * num_sms());
-        cudaMemsetAsync(err, 0, 4, st);
-        kern<<<grid, warps * 32, smem, st>>>(pop, p, off, q, (int)n, (int)k, cross, within, job_begin,
-                                                job_end, err);
+        const int grid = (int)std::min<int64_t>((jobs + warps - 1) / warps, (int64_t)per_sm * num_sms());
+        kern<<<grid, warps * 32, smem, st>>>(pop8, p, off8, q, (int)n, nb, (int)k, cross, within, job_begin,
+                                             job_end, err);
         int32_t herr = 0;
         if (cudaGetLastError() != cudaSuccess ||
             cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
@@ -373,6 +412,7 @@ int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, i
                              cudaGetErrorString(cudaGetLastError()));
         if (herr & 1) return set_error(MCB_ERR_RANGE, "pairwise: color id out of range [0, k)");
         if (!(herr & 2)) break;
+        cudaMemsetAsync(err, 0, 4, st);
     }
     (void)flags;
     return MCB_OK;
