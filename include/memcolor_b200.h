@@ -191,6 +191,19 @@ int mcb_match_parents(const int32_t *dist, int64_t p, int64_t K, int64_t max_dis
                       void *stream);
 int mcb_match_parents_host(const int32_t *dist, int64_t p, int64_t K, int64_t max_dist, int64_t *matches,
                            void *stream);
+/*
+ * Randomized greedy colourings for weighted runs, p at once
+ * (mc/init.py:30-46 greedy_wvcp_init, :57-64 init_wvcp_population): every
+ * individual i walks `order` int32[n] (the reference's greedy_order, :23-27)
+ * with stream key keys[i] (= stream_key(seed, TAG_INIT, i)); CSR adjacency
+ * indptr int64[n+1] / indices int32[2m].  Out: assigns int32[p,n] (legal
+ * colourings) and used int32[p] (colours each opened; the run's palette is
+ * their maximum).  MCB_ERR_UNSUPPORTED beyond 1024 colours or n > 32767.
+ */
+int mcb_greedy_wvcp_init(const int32_t *order, const int64_t *indptr, const int32_t *indices, int64_t n,
+                         const uint64_t *keys, int64_t p, int32_t *assigns, int32_t *used, void *stream);
+int mcb_greedy_wvcp_init_host(const int32_t *order, const int64_t *indptr, const int32_t *indices, int64_t n,
+                              const uint64_t *keys, int64_t p, int32_t *assigns, int32_t *used, void *stream);
 
 #ifdef __cplusplus
 }

@@ -477,4 +477,33 @@ int mcb_match_parents_host(const int32_t *dist, int64_t p, int64_t K, int64_t ma
     return ar.download();
 }
 
+int mcb_greedy_wvcp_init(const int32_t *order, const int64_t *indptr, const int32_t *indices, int64_t n,
+                         const uint64_t *keys, int64_t p, int32_t *assigns, int32_t *used, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return greedy_init_run(order, indptr, indices, n, keys, p, assigns, used, (cudaStream_t)stream);
+}
+
+int mcb_greedy_wvcp_init_host(const int32_t *order, const int64_t *indptr, const int32_t *indices, int64_t n,
+                              const uint64_t *keys, int64_t p, int32_t *assigns, int32_t *used, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 1 || p < 0) return set_error(MCB_ERR_VALUE, "bad shape");
+    Arena ar(st);
+    const int32_t *dord, *dind;
+    const int64_t *dptr;
+    const uint64_t *dkeys;
+    int32_t *dasg, *dused;
+    ar.add(order, &dord, (size_t)n);
+    ar.add(indptr, &dptr, (size_t)n + 1);
+    ar.add(indices, &dind, (size_t)std::max<int64_t>(indptr[n], 1));
+    ar.add(keys, &dkeys, (size_t)p);
+    ar.add(assigns, &dasg, (size_t)p * n, false, true);
+    ar.add(used, &dused, (size_t)p, false, true);
+    int rc = ar.upload();
+    if (rc) return rc;
+    rc = greedy_init_run(dord, dptr, dind, n, dkeys, p, dasg, dused, st);
+    if (rc) return rc;
+    return ar.download();
+}
+
 }  // extern "C"

@@ -83,6 +83,8 @@ int update_population_run(const int32_t *pdist, const int32_t *cross, const int3
                           int64_t *out_fit, cudaStream_t st);
 int match_parents_run(const int32_t *dist, int64_t p, int64_t K, int64_t max_dist, int64_t *matches,
                       cudaStream_t st);
+int greedy_init_run(const int32_t *order, const int64_t *indptr, const int32_t *indices, int64_t n,
+                    const uint64_t *keys, int64_t p, int32_t *assigns, int32_t *used, cudaStream_t st);
 int stream_values_run(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out, int64_t count,
                       cudaStream_t st);
 

@@ -1,11 +1,13 @@
 """Device-resident generation of the memetic loop.
 
-One generation of `mc/engine.py:_generation_loop` (:203-316) for the
-k-colouring problem without the surrogate (the reference's ablation setting,
-`use_surrogate=False`, `mc/crossover.py:103-131`), with every array kept in
-HBM between the operators:
+One generation of `mc/engine.py:_generation_loop` (:203-316) without the
+surrogate (the reference's ablation setting, `use_surrogate=False`,
+`mc/crossover.py:103-131`), for k-colouring (`run_col_fixed_k`, :346-368) and
+weighted colouring (`run_wvcp`, :321-343), with every array kept in HBM
+between the operators:
 
-    LS          improve_population -> TabuCol from the offspring     (:205-214)
+    init        init_col_population / init_wvcp_population (greedy, on the GPU)
+    LS          improve_population -> TabuCol / iterated WVCP tabu   (:205-214)
     distances   pairwise_distances(pop, improved)                    (:287-289)
     pool        update_population(pop, improved, fitness, ...)      (:290)
     matching    match_parents(pop, K)                                (:294)
@@ -46,6 +48,7 @@ class ColState:
     k: int
     generation: int = 0
     best_score: int = 2 ** 62
+    mode: str = "col"
 
     @property
     def p(self):
@@ -70,8 +73,46 @@ def init_state(dg, init_assigns, k):
     return st
 
 
+INF_SCORE = 2 ** 62
+
+
+def wvcp_scores(dg, assigns, k):
+    """`wvcp_score` (`mc/coloring.py:53-67`) of every row: the sum over
+    nonempty classes of the class's largest weight."""
+    p = assigns.shape[0]
+    w = dg.weights.unsqueeze(0).expand(p, -1)
+    mx = torch.zeros((p, k), dtype=torch.int64, device=assigns.device)
+    mx.scatter_reduce_(1, assigns.long(), w, reduce="amax", include_self=True)
+    return mx.sum(dim=1)
+
+
+def init_state_wvcp(dg, g, p, seed):
+    """`run_wvcp`'s start (`mc/engine.py:330-335`): p randomized greedy
+    colourings built on the GPU (`init_wvcp_population`, `mc/init.py:57-64`),
+    palette k = the most colours any of them opened, fitness = score."""
+    from .init import greedy_wvcp_assigns, stream_keys_init
+
+    a, used = greedy_wvcp_assigns(g, stream_keys_init(seed, p), device=True)
+    k = int(used.max().item())
+    fit = wvcp_scores(dg, a, k)
+    st = ColState(pop_assigns=a.clone(), pop_fitness=fit, pop_dist=Dv.pairwise(a[:0], a, k)[1],
+                  offspring=a.clone(), k=k, mode="wvcp")
+    st.best_score = int(fit.min().item())
+    return st
+
+
 def col_generation(dg, st, *, seed, depth, K, ms=None, timings=None):
-    """Advance `st` by one generation in place; returns the LS outputs."""
+    """k-colouring generation (kept name); see `generation`."""
+    return generation(dg, st, seed=seed, depth=depth, K=K, ms=ms, timings=timings)
+
+
+def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, phi0=None):
+    """Advance `st` by one generation in place; returns the LS outputs.
+
+    WVCP (`st.mode == "wvcp"`): `improve_population(..., WVCP, ...)`
+    (`mc/localsearch.py:642-662`) -- phi0 = (k / 2n) max weight, schedule on,
+    `max_rounds` rounds of `depth`; an individual that never reached a legal
+    colouring keeps its start with fitness INF_SCORE."""
     p, n, k, t = st.p, st.n, st.k, st.generation
     dev = st.pop_assigns.device
     ms = min_spacing(n) if ms is None else ms
@@ -83,8 +124,17 @@ def col_generation(dg, st, *, seed, depth, K, ms=None, timings=None):
 
     mark(0)
     keys = Dv.keys_to_tensor(stream_keys(seed, TAG_LS, t, p), dev)
-    ls = Dv.tabucol_batch(dg, st.offspring.clone(), k, keys, depth)
-    improved, imp_fit = ls["best_assigns"], ls["best_conflicts"]
+    if st.mode == "wvcp":
+        if phi0 is None:
+            phi0 = (k / (2.0 * n)) * dg.max_weight
+        ls = Dv.wvcp_batch(dg, st.offspring.clone(), k, keys, depth, max_rounds, True, phi0)
+        legal = ls["best_scores"] < INF_SCORE
+        improved = torch.where(legal[:, None], ls["best_assigns"], st.offspring).contiguous()
+        imp_fit = torch.where(legal, ls["best_scores"], torch.full_like(ls["best_scores"], INF_SCORE))
+        ls["best_assigns"], ls["best_scores"] = improved, imp_fit
+    else:
+        ls = Dv.tabucol_batch(dg, st.offspring.clone(), k, keys, depth)
+        improved, imp_fit = ls["best_assigns"], ls["best_conflicts"]
     st.best_score = min(st.best_score, int(imp_fit.min().item()))
     mark(1)
     cross, within = Dv.pairwise(st.pop_assigns, improved, k)

@@ -16,6 +16,7 @@ inputs, the outputs of the reference's own hot-path kernels:
 * gpx.npz       build_offspring_batch / gpx (`crossover.py:69-93`)
 * distance.npz  pairwise_distances / approx_partition_distance (`distance.py:75-155`)
 * population.npz  update_population / match_parents (`population.py:59-141`)
+* init.npz      init_wvcp_population greedy colourings (`init.py:23-64`)
 * engine.npz    k-colouring generations without the surrogate, chained from the
                 reference's own operators as `engine.py:_generation_loop` does
 
@@ -338,6 +339,55 @@ def gen_engine(out):
             out[pre + f"g{t}_selected"] = batch.selected_index.astype(np.int64)
             out[pre + f"g{t}_offspring"] = batch.selected_assigns.astype(np.int32)
     out["cases"] = np.array([c[0] for c in ENGINE_CASES])
+    gen_engine_wvcp(out)
+
+
+ENGINE_WVCP_CASES = [  # (name, seed, n, p_edge, wmax, p, K, depth, rounds, G)
+    ("w1", 2, 60, 0.5, 20, 10, 3, 120, 4, 3),
+    ("w2", 4, 80, 0.3, 50, 12, 4, 160, 3, 3),
+    ("w3", 6, 70, 0.7, 10, 8, 3, 1, 1, 3),  # too short to repair offspring: INF fitness
+]
+
+
+def gen_engine_wvcp(out):
+    """Weighted generations: greedy init (`init.py:57-64`), fitness
+    `wvcp_score` (`engine.py:332`), LS `improve_population(..., WVCP, ...)`."""
+    from memcolor.coloring import Coloring as RC
+    from memcolor.coloring import wvcp_score as rws
+    from memcolor.crossover import build_and_select_offspring
+    from memcolor.distance import pairwise_distances as rpd
+    from memcolor.init import init_wvcp_population
+
+    for name, seed, n, pe, wmax, p, K, depth, rounds, G in ENGINE_WVCP_CASES:
+        g = ref_rand_graph(seed, n, pe, wmax=wmax)
+        init = init_wvcp_population(g, p, seed)
+        k = init.k
+        fit = np.array([rws(g, c)[0] for c in init.colorings], dtype=np.int64)
+        pop = RPOP.Population.from_colorings(init.colorings, fit)
+        ms = RPOP.min_spacing(n)
+        offspring = list(init.colorings)
+        pre = name + "__"
+        out[pre + "params"] = np.array([seed, n, int(pe * 1000), wmax, p, K, depth, rounds, G, k],
+                                       dtype=np.int64)
+        out[pre + "init"] = pop.assigns.astype(np.int32)
+        out[pre + "init_fit"] = fit
+        for t in range(G):
+            res = RLS.improve_population(g, offspring, RLS.WVCP, seed, generation=t, depth=depth,
+                                         max_rounds=rounds)
+            imp = np.stack([r.best.assign for r in res]).astype(np.int32)
+            imp_fit = np.array([min(r.best_score, int(RLS.INF_SCORE)) for r in res], dtype=np.int64)
+            cross, within = rpd(pop.assigns, imp, k=k)
+            pop = RPOP.update_population(pop, imp, imp_fit, cross, within, ms)
+            matches = RPOP.match_parents(pop, K)
+            batch = build_and_select_offspring(pop, matches, None, seed, t, use_surrogate=False)
+            offspring = [RC(batch.selected_assigns[i], k) for i in range(p)]
+            out[pre + f"g{t}_improved"] = imp
+            out[pre + f"g{t}_imp_fit"] = imp_fit
+            out[pre + f"g{t}_pop"] = pop.assigns.astype(np.int32)
+            out[pre + f"g{t}_fit"] = pop.fitness.astype(np.int64)
+            out[pre + f"g{t}_dist"] = pop.dist.astype(np.int32)
+            out[pre + f"g{t}_offspring"] = batch.selected_assigns.astype(np.int32)
+    out["wvcp_cases"] = np.array([c[0] for c in ENGINE_WVCP_CASES])
 
 
 def gen_rng(out):
@@ -364,13 +414,35 @@ def gen_graphs(out):
     out["rows"] = np.array([repr(r) for r in rows])
 
 
+INIT_CASES = [  # (name, seed, n, p_edge, wmax, p, master_seed)
+    ("c125", 1, 125, 0.5, 100, 8, 11),
+    ("c4shape", 1, 500, 0.5, 100, 6, 3),
+    ("small", 3, 50, 0.4, 9, 10, 5),
+    ("dense", 5, 300, 0.9, 1, 4, 2),
+    ("edgeless", 16, 40, 0.0, 4, 3, 9),
+    ("vdense", 7, 200, 0.97, 5, 3, 1),
+]
+
+
+def gen_init(out):
+    from memcolor.init import init_wvcp_population as rinit
+
+    for name, seed, n, pe, wmax, p, ms in INIT_CASES:
+        g = ref_rand_graph(seed, n, pe, wmax=wmax)
+        res = rinit(g, p, ms)
+        out[f"{name}__params"] = np.array([seed, n, pe, wmax, p, ms], dtype=np.float64)
+        out[f"{name}__assigns"] = np.stack([c.assign for c in res.colorings]).astype(np.int32)
+        out[f"{name}__k"] = np.array(res.k)
+    out["cases"] = np.array([c[0] for c in INIT_CASES])
+
+
 def main():
     """python make_golden.py [name ...]  (default: every fixture)"""
     os.makedirs(HERE, exist_ok=True)
     only = set(sys.argv[1:])
     for fn, name in [(gen_rng, "rng"), (gen_graphs, "graphs"), (gen_tabucol, "tabucol"),
                      (gen_wvcp, "wvcp"), (gen_gpx, "gpx"), (gen_distance, "distance"),
-                     (gen_population, "population"), (gen_engine, "engine")]:
+                     (gen_population, "population"), (gen_engine, "engine"), (gen_init, "init")]:
         if only and name not in only:
             continue
         out = {}

@@ -36,3 +36,29 @@ def test_generations_match_reference(name):
         np.testing.assert_array_equal(st.offspring.cpu().numpy(), ENG[pre + f"g{t}_offspring"],
                                       err_msg=f"g{t} offspring")
     assert st.generation == G
+
+
+@pytest.mark.parametrize("name", [str(c) for c in ENG["wvcp_cases"]])
+def test_wvcp_generations_match_reference(name):
+    """Weighted runs: greedy init on the GPU, iterated WVCP tabu, INF fitness
+    for individuals that never reach a legal colouring (case w3)."""
+    pre = name + "__"
+    seed, n, pe, wmax, p, K, depth, rounds, G, k = (int(x) for x in ENG[pre + "params"])
+    g = rand_graph(seed, n, pe / 1000.0, wmax=wmax)
+    dg = Dv.DeviceGraph(g, "cuda")
+    st = E.init_state_wvcp(dg, g, p, seed)
+    assert st.k == k
+    np.testing.assert_array_equal(st.pop_assigns.cpu().numpy(), ENG[pre + "init"])
+    np.testing.assert_array_equal(st.pop_fitness.cpu().numpy(), ENG[pre + "init_fit"])
+    for t in range(G):
+        ls = E.generation(dg, st, seed=seed, depth=depth, K=K, max_rounds=rounds)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(ls["best_assigns"].cpu().numpy(), ENG[pre + f"g{t}_improved"],
+                                      err_msg=f"{name} g{t} LS")
+        np.testing.assert_array_equal(ls["best_scores"].cpu().numpy(), ENG[pre + f"g{t}_imp_fit"],
+                                      err_msg=f"{name} g{t} LS fitness")
+        np.testing.assert_array_equal(st.pop_assigns.cpu().numpy(), ENG[pre + f"g{t}_pop"], err_msg=f"g{t} pop")
+        np.testing.assert_array_equal(st.pop_fitness.cpu().numpy(), ENG[pre + f"g{t}_fit"], err_msg=f"g{t} fit")
+        np.testing.assert_array_equal(st.pop_dist.cpu().numpy(), ENG[pre + f"g{t}_dist"], err_msg=f"g{t} dist")
+        np.testing.assert_array_equal(st.offspring.cpu().numpy(), ENG[pre + f"g{t}_offspring"],
+                                      err_msg=f"g{t} offspring")

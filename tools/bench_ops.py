@@ -177,6 +177,31 @@ def bench_match_parents(a):
             "alg_bytes_per_row": 4 * p}
 
 
+def bench_greedy_init(a):
+    """init_wvcp_population at the C4 shape: G(500,.5), w in [1,100], p = 8192."""
+    from oracle import init_oracle as IO
+    from paper_2109_05948_b200.graph import rand_graph
+    from paper_2109_05948_b200.init import greedy_wvcp_assigns, stream_keys_init
+
+    g = rand_graph(1, 500, 0.5, wmax=100)
+    p = 8192
+    keys = stream_keys_init(1, p)
+    greedy_wvcp_assigns(g, keys[:8], device=True)
+
+    def run():
+        greedy_wvcp_assigns(g, keys, device=True)
+
+    t, _ = timed(run, reps=3)
+    pc = 8
+    t0 = time.perf_counter()
+    IO.init_wvcp_population(g.adj_indptr, g.adj_indices, g.weights, g.degrees, keys[:pc])
+    tc = time.perf_counter() - t0
+    return {"op": "greedy_init", "unit": "colourings/s", "gpu": p / t, "cpu": pc / tc, "cores": 1,
+            "config": "G(500,.5) w in [1,100], p=8192 (C4 shape)",
+            "cpu_sample": f"{pc} colourings with the restated reference loop (mc/init.py:30-46)",
+            "gpu_ms": 1e3 * t}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ops", default="wvcp,gpx,distance")
@@ -190,7 +215,8 @@ def main():
     oracle.build()
     for op in a.ops.split(","):
         r = {"wvcp": bench_wvcp, "gpx": bench_gpx, "distance": bench_distance,
-             "update_population": bench_update_population, "match_parents": bench_match_parents}[op](a)
+             "update_population": bench_update_population, "match_parents": bench_match_parents,
+             "greedy_init": bench_greedy_init}[op](a)
         r["speedup_vs_cpu"] = r["gpu"] / r["cpu"]
         print(json.dumps(r), flush=True)
 
