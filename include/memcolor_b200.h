@@ -204,6 +204,16 @@ int mcb_greedy_wvcp_init(const int32_t *order, const int64_t *indptr, const int3
                          const uint64_t *keys, int64_t p, int32_t *assigns, int32_t *used, void *stream);
 int mcb_greedy_wvcp_init_host(const int32_t *order, const int64_t *indptr, const int32_t *indices, int64_t n,
                               const uint64_t *keys, int64_t p, int32_t *assigns, int32_t *used, void *stream);
+/*
+ * First layer of the surrogate network on colour ids (mc/surrogate.py:146
+ * with the one-hot encoding of :123-133 folded in).  Forward (backward = 0):
+ * src = Lam [n, L], dst = z [B, k, L], z[b,i,:] = sum_{v: assigns[b,v]=i} Lam[v,:].
+ * Backward (backward = 1): src = dz [B, k, L], dst = dLam [n, L],
+ * dLam[v,:] = sum_b dz[b, assigns[b,v], :] (:209).  dtype_bytes 4 (float32)
+ * or 8 (float64); device pointers; deterministic summation order.
+ */
+int mcb_segsum(int dtype_bytes, int backward, const void *src, const int32_t *assigns, int64_t B, int64_t n,
+               int64_t k, int64_t L, void *dst, void *stream);
 
 #ifdef __cplusplus
 }

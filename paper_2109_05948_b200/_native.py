@@ -30,7 +30,7 @@ EXPORTS = [
     "mcb_probe_smem_bandwidth", "mcb_debug_phase_cycles", "mcb_debug_warp_stats",
     "mcb_debug_modcheck", "mcb_tabucol_describe",
     "mcb_update_population", "mcb_update_population_host", "mcb_match_parents", "mcb_match_parents_host",
-    "mcb_greedy_wvcp_init", "mcb_greedy_wvcp_init_host",
+    "mcb_greedy_wvcp_init", "mcb_greedy_wvcp_init_host", "mcb_segsum",
 ]
 
 _lib = None
@@ -72,6 +72,7 @@ def _declare(L):
     L.mcb_match_parents_host.argtypes = [P, I64, I64, I64, P, P]
     L.mcb_greedy_wvcp_init.argtypes = [P, P, P, I64, P, I64, P, P, P]
     L.mcb_greedy_wvcp_init_host.argtypes = [P, P, P, I64, P, I64, P, P, P]
+    L.mcb_segsum.argtypes = [C.c_int, C.c_int, P, P, I64, I64, I64, I64, P, P]
     for name in EXPORTS[3:]:
         getattr(L, name).restype = C.c_int
 

@@ -506,4 +506,10 @@ int mcb_greedy_wvcp_init_host(const int32_t *order, const int64_t *indptr, const
     return ar.download();
 }
 
+int mcb_segsum(int dtype_bytes, int backward, const void *src, const int32_t *assigns, int64_t B, int64_t n,
+               int64_t k, int64_t L, void *dst, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return segsum_run(dtype_bytes, backward != 0, src, assigns, B, n, k, L, dst, (cudaStream_t)stream);
+}
+
 }  // extern "C"

@@ -85,6 +85,8 @@ int match_parents_run(const int32_t *dist, int64_t p, int64_t K, int64_t max_dis
                       cudaStream_t st);
 int greedy_init_run(const int32_t *order, const int64_t *indptr, const int32_t *indices, int64_t n,
                     const uint64_t *keys, int64_t p, int32_t *assigns, int32_t *used, cudaStream_t st);
+int segsum_run(int dtype, bool backward, const void *src, const int32_t *assigns, int64_t B, int64_t n,
+               int64_t k, int64_t L, void *dst, cudaStream_t st);
 int stream_values_run(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out, int64_t count,
                       cudaStream_t st);
 

@@ -17,6 +17,7 @@ inputs, the outputs of the reference's own hot-path kernels:
 * distance.npz  pairwise_distances / approx_partition_distance (`distance.py:75-155`)
 * population.npz  update_population / match_parents (`population.py:59-141`)
 * init.npz      init_wvcp_population greedy colourings (`init.py:23-64`)
+* surrogate.npz SurrogateNet init / gradients / online training / predictions (`surrogate.py`)
 * engine.npz    k-colouring generations without the surrogate, chained from the
                 reference's own operators as `engine.py:_generation_loop` does
 
@@ -436,13 +437,61 @@ def gen_init(out):
     out["cases"] = np.array([c[0] for c in INIT_CASES])
 
 
+SURROGATE_CASES = [  # (name, n, k, seed, dtype, use_bn, B, epochs, batch, generations)
+    ("s64", 24, 5, 3, "float64", True, 40, 3, 8, 2),
+    ("s32", 24, 5, 3, "float32", True, 40, 3, 8, 2),
+    ("nobn", 20, 4, 7, "float64", False, 30, 2, 7, 2),
+]
+
+
+def surrogate_targets(assigns):
+    """Deterministic synthetic targets for the surrogate fixtures."""
+    a = assigns.astype(np.float64)
+    return 3.0 * (assigns == 0).sum(axis=1) + 0.5 * a[:, 0] - 0.25 * a[:, -1] + 10.0
+
+
+def gen_surrogate(out):
+    from memcolor.rng import TAG_TRAIN
+    from memcolor.rng import Stream as RStream
+    from memcolor.surrogate import SurrogateNet as RNet
+
+    for name, n, k, seed, dt, bn, B, epochs, bs, G in SURROGATE_CASES:
+        pre = name + "__"
+        net = RNet(n, problem="col", arch="small", seed=seed, dtype=np.dtype(dt), use_bn=bn)
+        assigns = random_col_assigns(n, k, B, seed + 100)
+        test = random_col_assigns(n, k, 16, seed + 200)
+        y = surrogate_targets(assigns)
+        out[pre + "params"] = np.array([n, k, seed, 1 if dt == "float64" else 0, int(bn), B, epochs, bs, G])
+        out[pre + "pred0"] = net.predict_assigns(test, k)
+        # one train-mode forward + hand-written backward on the first 8 rows
+        x = net.one_hot(assigns[:8], k)
+        pred = net.forward(x, mode="train", keep_cache=True, update_running=False)
+        dout = (2.0 * (pred - ((y[:8] - y[:8].mean()) / y[:8].std())) / 8).astype(net.dtype)
+        grads = net._backward(dout)
+        for j, g in enumerate(grads):
+            out[pre + f"grad{j}"] = np.asarray(g, dtype=np.float64)
+        out[pre + "train_pred"] = pred.astype(np.float64)
+        for layer in net.layers:
+            layer.cache = None
+        for t in range(G):
+            losses = net.train_generation(assigns, y + t, k, epochs, bs, RStream.derive(seed, TAG_TRAIN, t))
+            out[pre + f"g{t}_losses"] = np.array(losses)
+            out[pre + f"g{t}_pred"] = net.predict_assigns(test, k)
+        for i, layer in enumerate(net.layers):
+            for nm in ("lam", "gam", "beta", "bn_scale", "bn_shift", "run_mean", "run_var"):
+                out[pre + f"l{i}_{nm}"] = np.asarray(getattr(layer, nm), dtype=np.float64)
+        out[pre + "adam_t"] = np.array(net.adam_t)
+    out["cases"] = np.array([c[0] for c in SURROGATE_CASES])
+
+
 def main():
     """python make_golden.py [name ...]  (default: every fixture)"""
     os.makedirs(HERE, exist_ok=True)
     only = set(sys.argv[1:])
     for fn, name in [(gen_rng, "rng"), (gen_graphs, "graphs"), (gen_tabucol, "tabucol"),
                      (gen_wvcp, "wvcp"), (gen_gpx, "gpx"), (gen_distance, "distance"),
-                     (gen_population, "population"), (gen_engine, "engine"), (gen_init, "init")]:
+                     (gen_population, "population"), (gen_engine, "engine"), (gen_init, "init"),
+                     (gen_surrogate, "surrogate")]:
         if only and name not in only:
             continue
         out = {}
