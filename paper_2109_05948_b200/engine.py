@@ -106,8 +106,16 @@ def col_generation(dg, st, *, seed, depth, K, ms=None, timings=None):
     return generation(dg, st, seed=seed, depth=depth, K=K, ms=ms, timings=timings)
 
 
-def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, phi0=None):
+def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, phi0=None, net=None,
+               epochs=1, batch_size=64):
     """Advance `st` by one generation in place; returns the LS outputs.
+
+    With a surrogate ``net`` (`surrogate.SurrogateNet`; the reference's
+    `use_surrogate=True`): after the LS it trains on (LS start points,
+    realized best scores) when at least two are finite, with
+    `Stream.derive(seed, TAG_TRAIN, t)` (`mc/engine.py:263-281`), and every
+    individual keeps the candidate with the lowest prediction
+    (`mc/crossover.py:114-118`) instead of a uniform draw.
 
     WVCP (`st.mode == "wvcp"`): `improve_population(..., WVCP, ...)`
     (`mc/localsearch.py:642-662`) -- phi0 = (k / 2n) max weight, schedule on,
@@ -136,6 +144,13 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
         ls = Dv.tabucol_batch(dg, st.offspring.clone(), k, keys, depth)
         improved, imp_fit = ls["best_assigns"], ls["best_conflicts"]
     st.best_score = min(st.best_score, int(imp_fit.min().item()))
+    if net is not None:
+        from .rng import TAG_TRAIN, Stream
+
+        mask = imp_fit < INF_SCORE
+        if int(mask.sum().item()) >= 2:
+            net.train_generation(st.offspring[mask], imp_fit[mask].double().cpu().numpy(), k, epochs, batch_size,
+                                 Stream.derive(seed, TAG_TRAIN, t))
     mark(1)
     cross, within = Dv.pairwise(st.pop_assigns, improved, k)
     mark(2)
@@ -156,13 +171,17 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
     mark(4)
     ck = Dv.keys_to_tensor(stream_keys(seed, TAG_CROSS, t, p * K), dev)
     cands = Dv.gpx_batch(st.pop_assigns, matches, k, ck)
-    # uniform selection: Stream.derive(seed, TAG_SELECT, t, i).below(K) = stream_value(key, 0) % K
-    sk = Dv.keys_to_tensor(stream_keys(seed, TAG_SELECT, t, p), dev)
-    sv = torch.empty(p, dtype=torch.int64, device=dev)
-    zeros = torch.zeros(p, dtype=torch.int64, device=dev)
-    N.check(N.lib().mcb_stream_values(P(sk), P(zeros), P(sv), p, _stream()))
-    hi, lo = (sv >> 32) & 0xFFFFFFFF, sv & 0xFFFFFFFF  # unsigned 64-bit value mod K in int64
-    sel = ((hi % K) * ((1 << 32) % K) + lo % K) % K
+    if net is not None:
+        pred = net.predict_assigns_device(cands.reshape(p * K, n), k).reshape(p, K)
+        sel = pred.argmin(dim=1)
+    else:
+        # uniform selection: Stream.derive(seed, TAG_SELECT, t, i).below(K) = stream_value(key, 0) % K
+        sk = Dv.keys_to_tensor(stream_keys(seed, TAG_SELECT, t, p), dev)
+        sv = torch.empty(p, dtype=torch.int64, device=dev)
+        zeros = torch.zeros(p, dtype=torch.int64, device=dev)
+        N.check(N.lib().mcb_stream_values(P(sk), P(zeros), P(sv), p, _stream()))
+        hi, lo = (sv >> 32) & 0xFFFFFFFF, sv & 0xFFFFFFFF  # unsigned 64-bit value mod K in int64
+        sel = ((hi % K) * ((1 << 32) % K) + lo % K) % K
     st.offspring = cands[torch.arange(p, device=dev), sel].contiguous()
     mark(5)
     st.generation = t + 1

@@ -341,6 +341,59 @@ def gen_engine(out):
             out[pre + f"g{t}_offspring"] = batch.selected_assigns.astype(np.int32)
     out["cases"] = np.array([c[0] for c in ENGINE_CASES])
     gen_engine_wvcp(out)
+    gen_engine_surrogate(out)
+
+
+ENGINE_SURROGATE_CASES = [  # (name, seed, n, p_edge, k, p, K, depth, G, epochs, batch)
+    ("es1", 3, 60, 0.5, 8, 12, 4, 300, 3, 2, 5),
+]
+
+
+def gen_engine_surrogate(out):
+    """k-colouring generations with the surrogate (`use_surrogate=True`,
+    float64 net, arch "small"): training on (restart points, realized scores)
+    with TAG_TRAIN streams (`engine.py:263-281`) and argmin selection
+    (`crossover.py:114-118`)."""
+    from memcolor.coloring import Coloring as RC
+    from memcolor.coloring import col_conflicts as rcc
+    from memcolor.crossover import build_and_select_offspring
+    from memcolor.distance import pairwise_distances as rpd
+    from memcolor.init import init_col_population
+    from memcolor.rng import TAG_TRAIN
+    from memcolor.rng import Stream as RStream
+    from memcolor.surrogate import SurrogateNet as RNet
+
+    for name, seed, n, pe, k, p, K, depth, G, epochs, bs in ENGINE_SURROGATE_CASES:
+        g = ref_rand_graph(seed, n, pe)
+        init = init_col_population(n, k, p, seed)
+        fit = np.array([rcc(g, c) for c in init.colorings], dtype=np.int64)
+        pop = RPOP.Population.from_colorings(init.colorings, fit)
+        ms = RPOP.min_spacing(n)
+        net = RNet(n, problem="col", arch="small", seed=seed, dtype=np.float64)
+        offspring = list(init.colorings)
+        pre = name + "__"
+        out[pre + "params"] = np.array([seed, n, int(pe * 1000), k, p, K, depth, G, epochs, bs], dtype=np.int64)
+        out[pre + "init"] = pop.assigns.astype(np.int32)
+        for t in range(G):
+            res = RLS.improve_population(g, offspring, RLS.COL, seed, generation=t, depth=depth)
+            realized = np.array([r.best_score for r in res], dtype=np.float64)
+            realized[realized >= float(RLS.INF_SCORE)] = np.nan
+            mask = np.isfinite(realized)
+            if mask.sum() >= 2:
+                off = np.stack([c.assign for c in offspring])
+                net.train_generation(off[mask], realized[mask], k, epochs, bs, RStream.derive(seed, TAG_TRAIN, t))
+            imp = np.stack([r.best.assign for r in res]).astype(np.int32)
+            imp_fit = np.array([min(r.best_score, int(RLS.INF_SCORE)) for r in res], dtype=np.int64)
+            cross, within = rpd(pop.assigns, imp, k=k)
+            pop = RPOP.update_population(pop, imp, imp_fit, cross, within, ms)
+            matches = RPOP.match_parents(pop, K)
+            batch = build_and_select_offspring(pop, matches, net, seed, t, use_surrogate=True)
+            offspring = [RC(batch.selected_assigns[i], k) for i in range(p)]
+            out[pre + f"g{t}_pop"] = pop.assigns.astype(np.int32)
+            out[pre + f"g{t}_predicted"] = batch.predicted.astype(np.float64)
+            out[pre + f"g{t}_selected"] = batch.selected_index.astype(np.int64)
+            out[pre + f"g{t}_offspring"] = batch.selected_assigns.astype(np.int32)
+    out["surrogate_cases"] = np.array([c[0] for c in ENGINE_SURROGATE_CASES])
 
 
 ENGINE_WVCP_CASES = [  # (name, seed, n, p_edge, wmax, p, K, depth, rounds, G)

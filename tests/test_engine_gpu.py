@@ -62,3 +62,23 @@ def test_wvcp_generations_match_reference(name):
         np.testing.assert_array_equal(st.pop_dist.cpu().numpy(), ENG[pre + f"g{t}_dist"], err_msg=f"g{t} dist")
         np.testing.assert_array_equal(st.offspring.cpu().numpy(), ENG[pre + f"g{t}_offspring"],
                                       err_msg=f"g{t} offspring")
+
+
+@pytest.mark.parametrize("name", [str(c) for c in ENG["surrogate_cases"]])
+def test_surrogate_generations_match_reference(name):
+    """Surrogate-guided generations (float64 net): online training on the LS
+    start points, predictions of all p K candidates, argmin selection."""
+    from paper_2109_05948_b200.surrogate import SurrogateNet
+
+    pre = name + "__"
+    seed, n, pe, k, p, K, depth, G, epochs, bs = (int(x) for x in ENG[pre + "params"])
+    g = rand_graph(seed, n, pe / 1000.0)
+    dg = Dv.DeviceGraph(g, "cuda")
+    st = E.init_state(dg, ENG[pre + "init"], k)
+    net = SurrogateNet(n, problem="col", arch="small", seed=seed, dtype=np.float64)
+    for t in range(G):
+        E.generation(dg, st, seed=seed, depth=depth, K=K, net=net, epochs=epochs, batch_size=bs)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(st.pop_assigns.cpu().numpy(), ENG[pre + f"g{t}_pop"], err_msg=f"g{t} pop")
+        np.testing.assert_array_equal(st.offspring.cpu().numpy(), ENG[pre + f"g{t}_offspring"],
+                                      err_msg=f"g{t} offspring")
