@@ -214,6 +214,23 @@ int mcb_greedy_wvcp_init_host(const int32_t *order, const int64_t *indptr, const
  */
 int mcb_segsum(int dtype_bytes, int backward, const void *src, const int32_t *assigns, int64_t B, int64_t n,
                int64_t k, int64_t L, void *dst, void *stream);
+/*
+ * Inference path of the surrogate (eval mode, :137-178 with the one-hot
+ * folded in).  mcb_colour_order: stable counting sort of each coloring's
+ * vertices by colour -> order int32[B,n], offs int32[B,k+1].
+ * mcb_segsum_sorted: z[b,i,:] = sum over colour-i vertices of Lam[v,:] in that
+ * order; with A, C non-NULL the eval epilogue y = leaky(s A[col] + C[col],
+ * slope) is applied (A, C: the folded batch norm + biases).
+ * mcb_rowbias_affine_leaky: in place z[b,i,:] = leaky((z[b,i,:] + r[b,:]) A + C).
+ * dtype_bytes 4 or 8; device pointers.
+ */
+int mcb_colour_order(const int32_t *assigns, int64_t B, int64_t n, int64_t k, int32_t *order, int32_t *offs,
+                     void *stream);
+int mcb_segsum_sorted(int dtype_bytes, const void *lam, const int32_t *order, const int32_t *offs, int64_t B,
+                      int64_t n, int64_t k, int64_t L, const void *A, const void *C, double slope, void *z,
+                      void *stream);
+int mcb_rowbias_affine_leaky(int dtype_bytes, void *z, const void *r, const void *A, const void *C, double slope,
+                             int64_t B, int64_t k, int64_t L, void *stream);
 
 #ifdef __cplusplus
 }

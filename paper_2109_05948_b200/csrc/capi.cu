@@ -512,4 +512,23 @@ int mcb_segsum(int dtype_bytes, int backward, const void *src, const int32_t *as
     return segsum_run(dtype_bytes, backward != 0, src, assigns, B, n, k, L, dst, (cudaStream_t)stream);
 }
 
+int mcb_colour_order(const int32_t *assigns, int64_t B, int64_t n, int64_t k, int32_t *order, int32_t *offs,
+                     void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return colour_order_run(assigns, B, n, k, order, offs, (cudaStream_t)stream);
+}
+
+int mcb_segsum_sorted(int dtype_bytes, const void *lam, const int32_t *order, const int32_t *offs, int64_t B,
+                      int64_t n, int64_t k, int64_t L, const void *A, const void *C, double slope, void *z,
+                      void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return segsum_sorted_run(dtype_bytes, lam, order, offs, B, n, k, L, A, C, slope, z, (cudaStream_t)stream);
+}
+
+int mcb_rowbias_affine_leaky(int dtype_bytes, void *z, const void *r, const void *A, const void *C, double slope,
+                             int64_t B, int64_t k, int64_t L, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return rowbias_affine_leaky_run(dtype_bytes, z, r, A, C, slope, B, k, L, (cudaStream_t)stream);
+}
+
 }  // extern "C"

@@ -87,6 +87,12 @@ int greedy_init_run(const int32_t *order, const int64_t *indptr, const int32_t *
                     const uint64_t *keys, int64_t p, int32_t *assigns, int32_t *used, cudaStream_t st);
 int segsum_run(int dtype, bool backward, const void *src, const int32_t *assigns, int64_t B, int64_t n,
                int64_t k, int64_t L, void *dst, cudaStream_t st);
+int colour_order_run(const int32_t *assigns, int64_t B, int64_t n, int64_t k, int32_t *order, int32_t *offs,
+                     cudaStream_t st);
+int segsum_sorted_run(int dtype, const void *lam, const int32_t *order, const int32_t *offs, int64_t B, int64_t n,
+                      int64_t k, int64_t L, const void *A, const void *C, double slope, void *z, cudaStream_t st);
+int rowbias_affine_leaky_run(int dtype, void *z, const void *r, const void *A, const void *C, double slope,
+                             int64_t B, int64_t k, int64_t L, cudaStream_t st);
 int stream_values_run(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out, int64_t count,
                       cudaStream_t st);
 

@@ -130,3 +130,20 @@ def test_segsum_kernel_vs_one_hot_matmul(dtype):
     a[3, 7] = k  # out of range -> ValueError, like the reference's one-hot indexing
     with pytest.raises(ValueError):
         N.check(N.lib().mcb_segsum(es, 0, N.ptr(lam), N.ptr(a), B, n, k, L, N.ptr(z), s))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("use_bn", [True, False])
+def test_fused_eval_path_matches_autograd_path(dtype, use_bn):
+    """predict_assigns (colour-sorted segment sums + fused epilogues) equals
+    the training-path forward in eval mode after some training (non-trivial
+    running statistics)."""
+    net = SurrogateNet(40, arch="small", seed=2, dtype=dtype, use_bn=use_bn)
+    a = random_col_assigns(40, 7, 50, 4)
+    net.train_generation(a, _targets(a), 7, 2, 8, Stream.derive(2, TAG_TRAIN, 0))
+    test = random_col_assigns(40, 7, 33, 9)
+    fast = net.predict_assigns(test, 7, chunk=16)
+    with torch.no_grad():
+        slow = net.forward_assigns(test, 7, mode="eval").double().cpu().numpy() * net.target_std + net.target_mean
+    tol = 1e-10 if dtype == np.float64 else 1e-4
+    np.testing.assert_allclose(fast, slow, rtol=tol, atol=tol)

@@ -202,6 +202,39 @@ def bench_greedy_init(a):
             "gpu_ms": 1e3 * t}
 
 
+def bench_surrogate(a):
+    """Surrogate per generation at C3: predict p K = 16384 x 16 candidates
+    (n = 1000, k = 83, arch "small", float32) + one training epoch on p rows."""
+    from paper_2109_05948_b200.rng import TAG_TRAIN, Stream
+    from paper_2109_05948_b200.surrogate import SurrogateNet
+
+    n, k, p, K = 1000, 83, a.pop_p, 16
+    net = SurrogateNet(n, problem="col", arch="small", seed=1)
+    cands = torch.randint(0, k, (p * K, n), dtype=torch.int32, device="cuda")
+    train = cands[:p]
+    y = np.random.default_rng(1).random(p) * 100
+
+    def run():
+        net.train_generation(train, y, k, 1, 64, Stream.derive(1, TAG_TRAIN, 0))
+        return net.predict_assigns_device(cands, k)
+
+    t, _ = timed(run, reps=1)
+    # reference-style CPU cost: dense one-hot numpy forward, bounded sample
+    lam = [l.lam.cpu().numpy() for l in net.layers]
+    x = np.zeros((64, k, n), np.float32)
+    a_ = cands[:64].cpu().numpy()
+    x[np.arange(64)[:, None], a_, np.arange(n)[None, :]] = 1
+    t0 = time.perf_counter()
+    h = x
+    for w in lam:
+        h = np.maximum(h @ w, 0)
+    tc = (time.perf_counter() - t0) / 64
+    return {"op": "surrogate", "unit": "candidates/s", "gpu": p * K / t, "cpu": 1.0 / tc, "cores": os.cpu_count(),
+            "config": f"n={n} k={k} arch small float32: predict {p}x{K} candidates + 1 epoch on {p} rows (batch 64)",
+            "cpu_sample": "64 candidates, dense one-hot numpy matmuls (forward only, no BN: a lower bound)",
+            "gpu_ms": 1e3 * t}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ops", default="wvcp,gpx,distance")
@@ -216,7 +249,7 @@ def main():
     for op in a.ops.split(","):
         r = {"wvcp": bench_wvcp, "gpx": bench_gpx, "distance": bench_distance,
              "update_population": bench_update_population, "match_parents": bench_match_parents,
-             "greedy_init": bench_greedy_init}[op](a)
+             "greedy_init": bench_greedy_init, "surrogate": bench_surrogate}[op](a)
         r["speedup_vs_cpu"] = r["gpu"] / r["cpu"]
         print(json.dumps(r), flush=True)
 
