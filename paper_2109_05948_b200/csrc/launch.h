@@ -33,8 +33,11 @@ struct TabucolArgs {
 };
 int tabucol_run(const TabucolArgs &a, cudaStream_t st);
 // warp-per-individual kernel (tabucol_warp.cu); -1 = shape outside its envelope
+// work_list/nwork: a subset of individuals (nullptr/-1: all); spill: the
+// variant whose tabu ring continues in global memory (no 1024-entry limit)
 int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *work_counter, int32_t *ovf_list,
-                        int32_t *ovf_count, int32_t *err_flag);
+                        int32_t *ovf_count, int32_t *err_flag, const int32_t *work_list = nullptr,
+                        int64_t nwork = -1, bool spill = false);
 int tabucol_phase_cycles(unsigned long long *out, int reset);
 int tabucol_warp_stats(unsigned long long *out);
 

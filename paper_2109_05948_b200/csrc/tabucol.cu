@@ -1107,7 +1107,9 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
 
     const size_t tab = (size_t)n * kp;
     const int grid_cap = 16 * num_sms();
-    const size_t ctl_bytes = 256 + 1024 + sizeof(int32_t) * (size_t)A.p;
+    // control words, per-SM tickets, overflow list of the warp pass, overflow
+    // list of its spill pass
+    const size_t ctl_bytes = 256 + 1024 + 2 * sizeof(int32_t) * (size_t)A.p;
     const size_t ng_stride = (tab + 255) & ~(size_t)255, ns_stride = (tab * 2 + 255) & ~(size_t)255;
     const size_t wg_stride = (tab * 2 + 255) & ~(size_t)255, ws_stride = (tab * 4 + 255) & ~(size_t)255;
     const int wide_grid = std::min<int>((int)A.p, 2 * num_sms());
@@ -1133,12 +1135,16 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     P.sm_ticket = ctl32 + 64;  // 256 per-SM counters
     uint8_t *tables = ws + tables_off;
 
-    // fast path: one individual per warp (tabucol_warp.cu); overflowing
-    // individuals land on the list the wide pass below consumes, and the wide
-    // pass is launched only when that list is not empty
+    // fast path: one individual per warp (tabucol_warp.cu).  Individuals whose
+    // tabu list outgrows the 1024-entry register ring re-run on the SPILL
+    // variant (ring continued in global memory); what still overflows (gamma
+    // > 63, tenure >= 8190) lands on the list the wide pass below consumes,
+    // which is launched only when that list is not empty
     bool warp_done = false;
+    int32_t *ovf_warp = ctl32 + 64 + 256, *ovf_spill = ovf_warp + A.p;
+    int32_t *ovf_final = ovf_warp, *ovf_final_count = ctl32 + 2;
     if (variant == 0) {
-        rc = tabucol_warp_launch(A, st, ctl32 + 0, ctl32 + 64 + 256, ctl32 + 2, ctl32 + 3);
+        rc = tabucol_warp_launch(A, st, ctl32 + 0, ovf_warp, ctl32 + 2, ctl32 + 3);
         if (rc > 0) return rc;
         warp_done = rc == MCB_OK;
     }
@@ -1149,6 +1155,20 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
             return set_error(MCB_ERR_CUDA, "tabucol: kernel failed: %s", cudaGetErrorString(cudaGetLastError()));
         if (h[1] == 1) return set_error(MCB_ERR_RANGE, "color id out of range [0, k)");
         if (h[0] == 0) return MCB_OK;
+        if (!getenv("MCB_NO_SPILL")) {
+            rc = tabucol_warp_launch(A, st, ctl32 + 4, ovf_spill, ctl32 + 5, ctl32 + 3, ovf_warp, h[0], true);
+            if (rc > 0) return rc;
+            if (rc == MCB_OK) {
+                int32_t h2 = 0;
+                if (cudaMemcpyAsync(&h2, ctl32 + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                    cudaStreamSynchronize(st) != cudaSuccess)
+                    return set_error(MCB_ERR_CUDA, "tabucol: spill pass failed: %s",
+                                     cudaGetErrorString(cudaGetLastError()));
+                if (h2 == 0) return MCB_OK;
+                ovf_final = ovf_spill;
+                ovf_final_count = ctl32 + 5;
+            }
+        }
     }
 
     // CSR row offsets -> __constant__ (u32) when they fit
@@ -1183,8 +1203,8 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     Q.ovf_list = nullptr;
     Q.ovf_count = nullptr;
     if (variant != 2) {
-        Q.work = ctl32 + 64 + 256;
-        Q.nwork_dev = ctl32 + 2;
+        Q.work = ovf_final;
+        Q.nwork_dev = ovf_final_count;
     }
     Q.ws_gamma = tables + narrow_ws;
     Q.ws_g_stride = wg_stride;

@@ -78,6 +78,9 @@ struct WarpTabuParams {
     int64_t *log_iter, *log_tt, *log_cnt;
     int64_t *counters;
     int nwork;
+    const int32_t *work_list;  // individual ids (nullptr: 0 .. nwork-1)
+    uint32_t *spill;           // SPILL variant: per-warp ring rows in global memory
+    int spill_rows;            // rows per warp (power of two)
     int32_t *work_counter;
     int32_t *ovf_list, *ovf_count, *err_flag;
     uint32_t flags;
@@ -110,6 +113,7 @@ enum {
     WS_EVENTS,
     WS_REMOVES,
     WS_BEST,
+    WS_SPILL_ROWS,
     WS_CY_SCAN = 16,
     WS_CY_SELECT,
     WS_CY_MOVE,
@@ -374,7 +378,7 @@ struct Swz {
     __device__ __forceinline__ static int phys(int c, int gg) { return 4 * pw(c >> 2, gg) + (c & 3); }
 };
 
-template <int KV, int CH, bool BITSET>
+template <int KV, int CH, bool BITSET, bool SPILL>
 __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(WarpTabuParams P) {
     constexpr int KP = 16 * KV, KW = 4 * KV;
     constexpr int RW = 2;  // conflicting rows per lane per scan round
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
         if (lane == 0) wi = atomicAdd(P.work_counter, 1);
         wi = __shfl_sync(FULLM, wi, 0);
         if (wi >= P.nwork) break;
-        const int ind = wi;
+        const int ind = P.work_list ? P.work_list[wi] : wi;
         const uint64_t key = P.keys[ind];
         int32_t *a_io = P.assigns + (size_t)ind * n;
         int32_t *b_out = P.best_assigns + (size_t)ind * n;
@@ -522,6 +526,13 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
         int nrows = 0;
         uint32_t ins = 0;
         uint32_t next_exp = 0;  // lower bound of the earliest live expiry (valid if nrows)
+        // SPILL: rows pushed out of the register ring (older than all register
+        // rows) continue, in age order, in this warp's global ring [sp_head,
+        // sp_tail); sp_next bounds their earliest live expiry from below
+        uint32_t *spw = nullptr;
+        uint32_t sp_head = 0, sp_tail = 0, sp_next = 0;
+        const uint32_t sp_mask = (uint32_t)P.spill_rows - 1u;
+        if constexpr (SPILL) spw = P.spill + ((size_t)blockIdx.x * (blockDim.x >> 5) + wid) * P.spill_rows * 32;
 
         // ---------------- iterations (:320-405) ----------------
         if (k >= 2 && !bad) {
@@ -556,6 +567,42 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                     nrows = last + 1;
                     next_exp = it32 + __reduce_min_sync(FULLM, dmin);
                     __syncwarp();
+                }
+                if constexpr (SPILL) {
+                    if (sp_head != sp_tail && (int)(sp_next - it32) <= 0) {
+                        // spilled rows, 8 loads in flight; fully dead rows at
+                        // the old end are released
+                        uint32_t dmin = 0x4000u, newhead = sp_head;
+                        bool lead = true;
+                        for (uint32_t r0 = sp_head; r0 != sp_tail; r0 += 8) {
+                            uint32_t e8[8];
+#pragma unroll
+                            for (int q = 0; q < 8; q++)
+                                e8[q] = (r0 + q != sp_tail && (int)(sp_tail - (r0 + q)) > 0)
+                                            ? spw[((r0 + q) & sp_mask) * 32 + lane]
+                                            : 0u;
+#pragma unroll
+                            for (int q = 0; q < 8; q++) {
+                                if ((int)(sp_tail - (r0 + q)) <= 0) break;
+                                const uint32_t e = e8[q];
+                                const uint32_t dist = ent_dist(e, it32);
+                                const bool hit = (e >> 31) != 0u && dist == 0u;
+                                if (hit) {
+                                    const int v = (e >> 21) & 0x3FF, c = (e >> 14) & 0x7F;
+                                    gam[(size_t)v * KP + S::phys(c, S::g(v))] &= (uint8_t)~TABU;
+                                    spw[((r0 + q) & sp_mask) * 32 + lane] = 0u;
+                                }
+                                const bool live = (e >> 31) != 0u && !hit;
+                                if (live) dmin = min(dmin, dist);
+                                if (__any_sync(FULLM, live)) lead = false;
+                                else if (lead) newhead = r0 + q + 1;
+                            }
+                            if ((int)(sp_tail - (r0 + 8)) <= 0) break;
+                        }
+                        sp_head = newhead;
+                        sp_next = it32 + __reduce_min_sync(FULLM, dmin);
+                        __syncwarp();
+                    }
                 }
                 WPH(WS_CY_EXPIRE);
 
@@ -888,21 +935,50 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                         // (v, a) is re-tabu'd while tabu: the older entry is void
                         WST(WS_SUPERSEDE, 1);
                         const uint32_t key_vc = ent_pack(v, a, 0) & 0xFFFFC000u;
+                        bool found = false;
 #pragma unroll
                         for (int j = 0; j < KE; j++) {
                             if (j >= nrows) break;
                             const bool hit = (ring[j] & 0xFFFFC000u) == key_vc;
                             if (hit) ring[j] = 0u;
-                            if (__any_sync(FULLM, hit)) break;
+                            if (__any_sync(FULLM, hit)) {
+                                found = true;
+                                break;
+                            }
                         }
+                        if constexpr (SPILL) {
+                            if (!found) {
+                                for (uint32_t r = sp_head; r != sp_tail; r++) {
+                                    uint32_t *slot = spw + (r & sp_mask) * 32 + lane;
+                                    const bool hit = (*slot & 0xFFFFC000u) == key_vc;
+                                    if (hit) *slot = 0u;
+                                    if (__any_sync(FULLM, hit)) break;
+                                }
+                            }
+                        }
+                        (void)found;
                     }
                     {
                         // insert at (row 0, lane ins % 32); a full row 0 shifts the rows
                         const int L = (int)(ins & 31u);
                         if (L == 0 && ins != 0u) {
                             if (__any_sync(FULLM, (ring[KE - 1] >> 31) != 0u)) {
-                                bad = true;  // > 1024 live tabu entries
-                                break;
+                                if constexpr (SPILL) {
+                                    if (sp_tail - sp_head > sp_mask) {
+                                        bad = true;  // cannot happen: tenure < 8190
+                                        break;
+                                    }
+                                    const uint32_t e = ring[KE - 1];
+                                    spw[(sp_tail & sp_mask) * 32 + lane] = e;
+                                    WST(WS_SPILL_ROWS, 1);
+                                    const uint32_t dm =
+                                        __reduce_min_sync(FULLM, (e >> 31) ? ent_dist(e, it32) : 0x4000u);
+                                    if (sp_head == sp_tail || (int)(it32 + dm - sp_next) < 0) sp_next = it32 + dm;
+                                    sp_tail++;
+                                } else {
+                                    bad = true;  // > 1024 live tabu entries: the SPILL variant
+                                    break;
+                                }
                             }
 #pragma unroll
                             for (int j = KE - 1; j > 0; j--) ring[j] = ring[j - 1];
@@ -1144,23 +1220,24 @@ __global__ void tw_csr16_kernel(const int64_t *indptr, const int32_t *indices, i
 // ---------------------------------------------------------------------------
 using KernT = void (*)(WarpTabuParams);
 
-template <int KV>
+template <int KV, bool SPILL>
 static KernT pick_mode(int ch) {
     switch (ch) {
-        case 8: return tabucol_warp_kernel<KV, 8, true>;
-        case 16: return tabucol_warp_kernel<KV, 16, true>;
-        case 32: return tabucol_warp_kernel<KV, 32, true>;
-        default: return tabucol_warp_kernel<KV, 32, false>;  // CSR, n <= 1024
+        case 8: return tabucol_warp_kernel<KV, 8, true, SPILL>;
+        case 16: return tabucol_warp_kernel<KV, 16, true, SPILL>;
+        case 32: return tabucol_warp_kernel<KV, 32, true, SPILL>;
+        default: return tabucol_warp_kernel<KV, 32, false, SPILL>;  // CSR, n <= 1024
     }
 }
+template <bool SPILL>
 static KernT pick_kernel(int kv, int ch) {
     switch (kv) {
-        case 1: return pick_mode<1>(ch);
-        case 2: return pick_mode<2>(ch);
-        case 3: return pick_mode<3>(ch);
-        case 4: return pick_mode<4>(ch);
-        case 6: return pick_mode<6>(ch);
-        case 8: return pick_mode<8>(ch);
+        case 1: return pick_mode<1, SPILL>(ch);
+        case 2: return pick_mode<2, SPILL>(ch);
+        case 3: return pick_mode<3, SPILL>(ch);
+        case 4: return pick_mode<4, SPILL>(ch);
+        case 6: return pick_mode<6, SPILL>(ch);
+        case 8: return pick_mode<8, SPILL>(ch);
         default: return nullptr;
     }
 }
@@ -1270,7 +1347,8 @@ static int upload_divtab(cudaStream_t st) {
 }
 
 int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, int32_t *ovf_list,
-                        int32_t *ovf_count, int32_t *err_flag) {
+                        int32_t *ovf_count, int32_t *err_flag, const int32_t *work_list, int64_t nwork,
+                        bool spill) {
     if (A.flags & (MCB_FLAG_FORCE_WIDE | MCB_FLAG_FORCE_GLOBAL | MCB_FLAG_PROFILE)) return -1;
     if (A.flags & MCB_FLAG_WSTATS) {
         // reset the counters of this launch
@@ -1278,15 +1356,19 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
         cudaMemcpyToSymbolAsync(g_wstats, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
     }
     WarpPlan pl;
-    if (!tw_plan((int)A.n, (int)A.k, A.p, &pl)) return -1;
-    KernT kern = pick_kernel(pl.kv, pl.ch);
+    if (nwork < 0) nwork = A.p;
+    if (!tw_plan((int)A.n, (int)A.k, nwork, &pl)) return -1;
+    KernT kern = spill ? pick_kernel<true>(pl.kv, pl.ch) : pick_kernel<false>(pl.kv, pl.ch);
     if (!kern) return -1;
     if (int rc = upload_divtab(st)) return rc;
     const int n = (int)A.n, kp = 16 * pl.kv;
     const size_t smem = pl.bitset_bytes + (size_t)pl.warps * pl.warp_smem;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return set_error(MCB_ERR_CUDA, "tabucol_warp: smem attribute (%zu) failed", smem);
-    const size_t spill_bytes = 0;
+    // SPILL: 256 rows x 32 entries per resident warp (tenure < 8190 keeps the
+    // live rows of register ring + spill under 32 + 256)
+    constexpr int SPILL_ROWS = 256;
+    const size_t spill_bytes = spill ? (size_t)pl.grid * pl.warps * SPILL_ROWS * 32 * 4 : 0;
     (void)kp;
     int64_t nnz_h = 0;
     if (cudaMemcpyAsync(&nnz_h, A.indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
@@ -1298,6 +1380,9 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
     WarpTabuParams P{};
     P.assigns = A.assigns;
     P.best_assigns = A.best_assigns;
+    P.spill = spill ? reinterpret_cast<uint32_t *>(ws) : nullptr;
+    P.spill_rows = SPILL_ROWS;
+    P.work_list = work_list;
     uint8_t *gbase = ws + ((spill_bytes + 255) & ~(size_t)255);
     if (pl.ch) {
         if (cudaMemsetAsync(gbase, 0, pl.bitset_global, st) != cudaSuccess)
@@ -1329,7 +1414,7 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
     P.log_tt = A.log_tt;
     P.log_cnt = A.log_cnt;
     P.counters = A.counters;
-    P.nwork = (int)A.p;
+    P.nwork = (int)nwork;
     P.work_counter = ctl32;
     P.ovf_list = ovf_list;
     P.ovf_count = ovf_count;
@@ -1338,8 +1423,9 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
     P.warp_smem = (int)pl.warp_smem;
     P.bitset_bytes = (int)pl.bitset_bytes;
     if (getenv("MCB_VERBOSE"))
-        fprintf(stderr, "[mcb] tabucol_warp<kv=%d,%s%d> grid=%d warps/CTA=%d smem=%zu\n", pl.kv,
-                pl.ch ? "bitset ch=" : "csr", pl.ch, pl.grid, pl.warps, smem);
+        fprintf(stderr, "[mcb] tabucol_warp<kv=%d,%s%d%s> grid=%d warps/CTA=%d smem=%zu work=%lld\n", pl.kv,
+                pl.ch ? "bitset ch=" : "csr", pl.ch, spill ? ",spill" : "", pl.grid, pl.warps, smem,
+                (long long)nwork);
     kern<<<pl.grid, 32 * pl.warps, smem, st>>>(P);
     if (cudaGetLastError() != cudaSuccess) return set_error(MCB_ERR_CUDA, "tabucol_warp launch failed");
     return MCB_OK;

@@ -35,7 +35,8 @@ SHAPES = [
 ]
 FALLBACK = [
     (11, 200, 0.8, 2, 8, 500),      # gamma > 63 at the start -> CTA kernel
-    (12, 300, 0.3, 6, 8, 2000),     # tenure ~1350 -> more than 1000 live tabu entries
+    (12, 300, 0.3, 6, 8, 2000),     # tenure ~1350 -> > 1024 live tabu entries -> SPILL variant
+    (1, 1000, 0.5, 83, 6, 2500),    # config 2 (C3) shape from random colourings: tenure ~1800 -> SPILL
 ]
 
 
@@ -67,7 +68,7 @@ def test_warp_variants_vs_oracle(shape, mode, monkeypatch, oracle_lib):
     _check(_run(g, A, k, keys, depth, monkeypatch, mode), ref, f"{shape}/{mode}")
 
 
-@pytest.mark.parametrize("shape", FALLBACK, ids=["gamma_overflow", "ring_overflow"])
+@pytest.mark.parametrize("shape", FALLBACK, ids=["gamma_overflow", "ring_overflow", "c3_random_start"])
 def test_warp_fallback_vs_oracle(shape, monkeypatch, oracle_lib):
     seed, n, pe, k, pop, depth = shape
     g = rand_graph(seed, n, pe)
@@ -91,6 +92,26 @@ def test_warp_supersede_path_is_exercised(monkeypatch):
     assert buf[0] == pop * depth or buf[0] > 0  # iterations ran in the warp kernel
     assert buf[4] > 0, "no supersede event in the supersede case"
     assert buf[2] > 0, "no aspiration round"
+
+
+def test_spill_variant_runs_for_long_tabu_lists(monkeypatch):
+    """The C3 shape from random colourings keeps > 1024 tabu entries live: the
+    individuals re-run on the SPILL variant (rows spilled to global memory),
+    bit-exact vs the oracle above; MCB_NO_SPILL routes them to the CTA kernel
+    instead, with the same results."""
+    seed, n, pe, k, pop, depth = FALLBACK[2]
+    g = rand_graph(seed, n, pe)
+    A = random_col_assigns(n, k, pop, seed)
+    keys = stream_keys(seed, TAG_LS, 0, pop)
+    monkeypatch.delenv("MCB_NO_WARP_KERNEL", raising=False)
+    a = LS._run_tabucol_batch(g, A.copy(), k, keys, depth, flags=N.FLAG_WSTATS)
+    buf = (ctypes.c_ulonglong * 40)()
+    N.check(N.lib().mcb_debug_warp_stats(ctypes.addressof(buf)))
+    assert buf[10] > 0, "no ring row spilled"
+    monkeypatch.setenv("MCB_NO_SPILL", "1")
+    b = LS._run_tabucol_batch(g, A.copy(), k, keys, depth)
+    for key in ("end_assigns", "best_assigns", "best_conflicts", "iters_used"):
+        np.testing.assert_array_equal(a[key], b[key])
 
 
 def test_draw_divisibility_paths():
