@@ -82,3 +82,22 @@ def test_surrogate_generations_match_reference(name):
         np.testing.assert_array_equal(st.pop_assigns.cpu().numpy(), ENG[pre + f"g{t}_pop"], err_msg=f"g{t} pop")
         np.testing.assert_array_equal(st.offspring.cpu().numpy(), ENG[pre + f"g{t}_offspring"],
                                       err_msg=f"g{t} offspring")
+
+
+def test_engine_selection_is_in_range_and_keeps_shapes():
+    """A larger random k-colouring run: shapes, dtypes and invariants after
+    two generations (distance matrix symmetric with zero diagonal, fitness =
+    conflicts of the stored colourings)."""
+    g = rand_graph(9, 150, 0.4)
+    dg = Dv.DeviceGraph(g, "cuda")
+    from paper_2109_05948_b200.init import random_col_assigns
+
+    st = E.init_state(dg, random_col_assigns(150, 9, 64, 9), 9)
+    for _ in range(2):
+        E.generation(dg, st, seed=9, depth=300, K=5)
+    d = st.pop_dist.cpu().numpy()
+    assert (d == d.T).all() and (np.diagonal(d) == 0).all()
+    a = st.pop_assigns.cpu().numpy()
+    conf = (a[:, g.edges[:, 0]] == a[:, g.edges[:, 1]]).sum(axis=1)
+    np.testing.assert_array_equal(conf, st.pop_fitness.cpu().numpy())
+    assert st.offspring.shape == (64, 150) and st.generation == 2

@@ -55,3 +55,14 @@ def test_greedy_init_too_many_colours():
     with pytest.raises(ValueError):
         greedy_wvcp_assigns(g, stream_keys_init(1, 1))
     torch.cuda.synchronize()
+
+
+def test_greedy_init_edge_cases():
+    g1 = rand_graph(1, 1, 0.5, wmax=3)  # one vertex: colour 0, one colour
+    a, used = greedy_wvcp_assigns(g1, stream_keys_init(2, 3))
+    assert a.tolist() == [[0], [0], [0]] and used.tolist() == [1, 1, 1]
+    g = rand_graph(1, 50, 0.3, wmax=5)
+    a, used = greedy_wvcp_assigns(g, stream_keys_init(2, 0))  # empty population
+    assert a.shape == (0, 50) and used.shape == (0,)
+    out = init_wvcp_population(g, 0, 1)
+    assert out.colorings == [] and out.k == 0

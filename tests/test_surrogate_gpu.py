@@ -147,3 +147,20 @@ def test_fused_eval_path_matches_autograd_path(dtype, use_bn):
         slow = net.forward_assigns(test, 7, mode="eval").double().cpu().numpy() * net.target_std + net.target_mean
     tol = 1e-10 if dtype == np.float64 else 1e-4
     np.testing.assert_allclose(fast, slow, rtol=tol, atol=tol)
+
+
+def test_surrogate_api_edges():
+    net = SurrogateNet(12, arch="small", seed=0)
+    assert net.predict_assigns(np.zeros((0, 12), np.int32), 3).shape == (0,)
+    with pytest.raises(ValueError):
+        net.predict_assigns(np.zeros((2, 11), np.int32), 3)  # wrong vertex count
+    with pytest.raises(ValueError):
+        net.predict_assigns(np.full((2, 12), 3, np.int32), 3)  # colour id >= k
+    with pytest.raises(ValueError):
+        net.train_generation(np.zeros((0, 12), np.int32), np.zeros(0), 3, 1, 4, Stream.derive(0, TAG_TRAIN, 0))
+    with pytest.raises(ValueError):
+        net.forward(np.zeros((2, 3, 11)))
+    # a single training example: std 0 -> 1 (`:266-268`), one minibatch of 1
+    losses = net.train_generation(np.zeros((1, 12), np.int32), np.array([5.0]), 3, 2, 4,
+                                  Stream.derive(0, TAG_TRAIN, 1))
+    assert len(losses) == 2 and net.target_std == 1.0 and net.target_mean == 5.0
