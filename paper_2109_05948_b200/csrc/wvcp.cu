@@ -70,6 +70,8 @@ struct WvParams {
     int64_t *log_cnt;
     uint32_t flags;
     int nwork;
+    const int32_t *work_list;  // individual ids (nullptr: 0 .. nwork-1)
+    int32_t *ovf_list, *ovf_count;  // u8 gamma: individuals whose gamma reached 256
     int32_t *work_counter;
     int32_t *err_flag;
     uint16_t *ws_wc;  // per-CTA [k][nranks]
@@ -80,7 +82,7 @@ struct WvCtrl {
     long long it, score, conflicts, best, nlog, diag;
     unsigned long long ctr;
     double phi;
-    int work, mv_v, mv_a, mv_b, has_move;
+    int work, mv_v, mv_a, mv_b, has_move, ovf;
     long long red[WV_NT / 32];
     long long red2[WV_NT / 32];
 };
@@ -129,7 +131,12 @@ __device__ __forceinline__ double shfl_d(double x, int src) {
     return __longlong_as_double(__shfl_sync(0xffffffffu, __double_as_longlong(x), src));
 }
 
+// GT: gamma element type.  uint8_t halves the dominant shared-memory table
+// (2 -> 4 individuals per SM at config 4); a count that would reach 256 stops
+// the individual, which the host re-runs with uint16_t.
+template <typename GT>
 __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
+    constexpr bool NARROW = sizeof(GT) == 1;
     constexpr int NT = WV_NT, NW = NT / 32;
     constexpr unsigned FULL = 0xffffffffu;
     const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -144,7 +151,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
         off += (bytes + 15) & ~(size_t)15;
         return p;
     };
-    uint16_t *gamma = reinterpret_cast<uint16_t *>(take((size_t)n * k * 2));
+    GT *gamma = reinterpret_cast<GT *>(take((size_t)n * k * sizeof(GT)));
     uint32_t *tabu_until = reinterpret_cast<uint32_t *>(take((size_t)n * 4));
     int32_t *wgt = reinterpret_cast<int32_t *>(take((size_t)n * 4));
     uint16_t *wrk = reinterpret_cast<uint16_t *>(take((size_t)n * 2));
@@ -211,10 +218,13 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
     };
 
     for (;;) {
-        if (tid == 0) ctl.work = atomicAdd(P.work_counter, 1);
+        if (tid == 0) {
+            ctl.work = atomicAdd(P.work_counter, 1);
+            ctl.ovf = 0;
+        }
         __syncthreads();
-        const int ind = ctl.work;
-        if (ind >= P.nwork) break;
+        if (ctl.work >= P.nwork) break;
+        const int ind = P.work_list ? P.work_list[ctl.work] : ctl.work;
         const uint64_t key = P.keys[ind];
         int32_t *a_io = P.assigns + (size_t)ind * n;
         int32_t *b_out = P.best_assigns + (size_t)ind * n;
@@ -229,13 +239,20 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
             }
             assign[v] = (uint8_t)c;
         }
-        for (size_t i = tid; i < (size_t)n * k / 2; i += NT) reinterpret_cast<uint32_t *>(gamma)[i] = 0u;
-        if ((n * k) & 1) gamma[n * k - 1] = 0;
+        // (the table's region is padded to 16 bytes: whole words are zeroed)
+        for (size_t i = tid; i < ((size_t)n * k * sizeof(GT) + 3) / 4; i += NT)
+            reinterpret_cast<uint32_t *>(gamma)[i] = 0u;
         for (size_t i = tid; i < (size_t)k * nranks; i += NT) wc[i] = 0;
         __syncthreads();
         for (int u = tid; u < n; u += NT) {  // gamma rows owned per thread
-            uint16_t *row = gamma + (size_t)u * k;
-            for (int64_t idx = P.indptr[u]; idx < P.indptr[u + 1]; idx++) row[assign[__ldg(P.indices + idx)]]++;
+            GT *row = gamma + (size_t)u * k;
+            bool o = false;
+            for (int64_t idx = P.indptr[u]; idx < P.indptr[u + 1]; idx++) {
+                GT &x = row[assign[__ldg(P.indices + idx)]];
+                if (NARROW && x == (GT)0xFF) o = true;
+                else x++;
+            }
+            if (o) ctl.ovf = 1;
         }
         __syncthreads();
         {  // wc[c][rank] member counts (u16 pairs updated with 32-bit atomics)
@@ -284,6 +301,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
 
         // ---------------- rounds (:156-258) ----------------
         for (int64_t rnd = 0; rnd < P.rounds; rnd++) {
+            if (NARROW && ctl.ovf) break;  // read after a barrier: uniform
             if (tid == 0 && P.schedule_on && rnd == P.rounds - 1) {
                 ctl.phi = P.forced_phi;
                 phis[P.rounds] = ctl.phi;
@@ -304,7 +322,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     for (int v = tid; v < n; v += NT) {
                         const int a = assign[v];
                         const int rem = (wrk[v] == max_rank[a]) ? (int)uniq_drop[a] : 0;
-                        const uint16_t *row = gamma + (size_t)v * k;
+                        const GT *row = gamma + (size_t)v * k;
                         const int gva = row[a];
                         const bool frozen = (uint64_t)it < tabu_until[v];
                         const int wv = wgt[v];
@@ -342,7 +360,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     for (int v = tid; v < n; v += NT) {
                         const int a = assign[v];
                         const long long rem = (wrk[v] == max_rank[a]) ? uniq_drop[a] : 0;
-                        const uint16_t *row = gamma + (size_t)v * k;
+                        const GT *row = gamma + (size_t)v * k;
                         const int gva = row[a];
                         const bool frozen = (uint64_t)it < tabu_until[v];
                         const long long wv = wgt[v];
@@ -365,7 +383,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                 for (int v = tid; v < n; v += NT) {
                     const int a = assign[v];
                     const long long rem = (wrk[v] == max_rank[a]) ? uniq_drop[a] : 0;
-                    const uint16_t *row = gamma + (size_t)v * k;
+                    const GT *row = gamma + (size_t)v * k;
                     const int gva = row[a];
                     const bool frozen = (uint64_t)it < tabu_until[v];
                     const long long wv = wgt[v];
@@ -448,7 +466,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                             const double R = shfl_d(RM, src);
                             const int a = assign[wvx];
                             const long long rem = (wrk[wvx] == max_rank[a]) ? uniq_drop[a] : 0;
-                            const uint16_t *row = gamma + (size_t)wvx * k;
+                            const GT *row = gamma + (size_t)wvx * k;
                             const int gva = row[a];
                             const bool frozen = (uint64_t)it < tabu_until[wvx];
                             const long long wv = wgt[wvx];
@@ -569,7 +587,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                         const int v = row;
                         const int a = assign[v];
                         const long long rem = (wrk[v] == max_rank[a]) ? uniq_drop[a] : 0;
-                        const uint16_t *rw = gamma + (size_t)v * k;
+                        const GT *rw = gamma + (size_t)v * k;
                         const int gva = rw[a];
                         const bool frozen = (uint64_t)it < tabu_until[v];
                         const long long wv = wgt[v];
@@ -645,7 +663,9 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     for (int64_t idx = P.indptr[v] + tid; idx < P.indptr[v + 1]; idx += NT) {
                         const int u = __ldg(P.indices + idx);
                         gamma[(size_t)u * k + a]--;
-                        gamma[(size_t)u * k + b]++;
+                        const GT old = gamma[(size_t)u * k + b];
+                        if (NARROW && old == (GT)0xFF) ctl.ovf = 1;
+                        gamma[(size_t)u * k + b] = (GT)(old + 1);
                     }
                     if (tid == 0) {
                         const int r = wrk[v];
@@ -695,6 +715,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     }
                 }
                 __syncthreads();
+                if (NARROW && ctl.ovf) break;
             }
             if (tid == 0) {  // phi schedule (:251-258)
                 if (P.schedule_on && rnd < P.rounds - 1) {
@@ -705,6 +726,11 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                 }
             }
             __syncthreads();
+        }
+        if (NARROW && ctl.ovf) {
+            if (tid == 0) P.ovf_list[atomicAdd(P.ovf_count, 1)] = ind;
+            __syncthreads();
+            continue;
         }
         for (int v = tid; v < n; v += NT) a_io[v] = assign[v];
         if (tid == 0) {
@@ -718,11 +744,35 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
     }
 }
 
-static size_t wv_smem(int n, int k) {
+static size_t wv_smem(int n, int k, int gbytes) {
     auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
-    return a16((size_t)n * k * 2) + a16((size_t)n * 4) + a16((size_t)n * 4) + a16((size_t)n * 2) +
+    return a16((size_t)n * k * gbytes) + a16((size_t)n * 4) + a16((size_t)n * 4) + a16((size_t)n * 2) +
            a16((size_t)n) + a16((size_t)n * 8) + a16((size_t)n * 2) + a16((size_t)k * 4) +
            2 * a16((size_t)k * 8) + a16((size_t)k * 4) + a16((size_t)2 * n * 4) + a16((size_t)n * 8);
+}
+
+template <typename GT>
+static int wvcp_launch(WvParams P, int64_t nwork, cudaStream_t st, uint8_t *ws_base, size_t ws_cap_ctas,
+                       size_t wc_stride) {
+    const size_t smem = wv_smem(P.n, P.k, sizeof(GT));
+    if (smem > (size_t)max_smem_optin())
+        return set_error(MCB_ERR_UNSUPPORTED, "wvcp: n*k too large for shared memory (%zu B)", smem);
+    if (cudaFuncSetAttribute(wvcp_kernel<GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "wvcp: smem attribute failed");
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wvcp_kernel<GT>, WV_NT, smem);
+    nb = std::max(nb, 1);
+    const int grid = (int)std::min<int64_t>(std::min<int64_t>(nwork, (int64_t)nb * num_sms()), ws_cap_ctas);
+    P.nwork = (int)nwork;
+    P.ws_wc = reinterpret_cast<uint16_t *>(ws_base);
+    P.ws_wc_stride = wc_stride;
+    if (getenv("MCB_VERBOSE"))
+        fprintf(stderr, "[mcb] wvcp<gamma u%d> grid=%d (%d/SM) smem=%zu work=%lld\n", (int)(8 * sizeof(GT)), grid,
+                nb, smem, (long long)nwork);
+    wvcp_kernel<GT><<<grid, WV_NT, smem, st>>>(P);
+    if (cudaGetLastError() != cudaSuccess) return set_error(MCB_ERR_CUDA, "wvcp launch failed");
+    return MCB_OK;
 }
 
 int wvcp_run(const WvcpArgs &A, cudaStream_t st) {
@@ -733,18 +783,14 @@ int wvcp_run(const WvcpArgs &A, cudaStream_t st) {
     if (A.rounds * A.depth >= (int64_t)1 << 31)
         return set_error(MCB_ERR_UNSUPPORTED, "wvcp: rounds*depth must be < 2^31");
     if (A.p == 0) return MCB_OK;
-    const size_t smem = wv_smem((int)A.n, (int)A.k);
-    if (smem > (size_t)max_smem_optin())
-        return set_error(MCB_ERR_UNSUPPORTED, "wvcp: n*k too large for shared memory (%zu B)", smem);
-    if (cudaFuncSetAttribute(wvcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return set_error(MCB_ERR_CUDA, "wvcp: smem attribute failed");
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wvcp_kernel, WV_NT, smem);
-    nb = std::max(nb, 1);
-    const int grid = (int)std::min<int64_t>(A.p, (int64_t)nb * num_sms());
+    // gamma u8 first (twice the individuals per SM); individuals whose gamma
+    // would reach 256 re-run with u16 (MCB_WVCP_WIDE=1: u16 throughout)
+    const bool wide_only = getenv("MCB_WVCP_WIDE") != nullptr ||
+                           wv_smem((int)A.n, (int)A.k, 1) > (size_t)max_smem_optin();
+    const size_t max_ctas = (size_t)16 * num_sms();
     const size_t wc_stride = (((size_t)A.k * A.nranks + 1) / 2 * 2 + 127) & ~(size_t)127;  // u16 elements
-    uint8_t *ws = (uint8_t *)workspace(256 + (size_t)grid * wc_stride * 2);
+    const size_t ctl_bytes = (256 + 4 * (size_t)A.p + 255) & ~(size_t)255;
+    uint8_t *ws = (uint8_t *)workspace(ctl_bytes + max_ctas * wc_stride * 2);
     if (!ws) return set_error(MCB_ERR_CUDA, "wvcp: workspace");
     cudaMemsetAsync(ws, 0, 256, st);
     WvParams P{};
@@ -780,21 +826,38 @@ int wvcp_run(const WvcpArgs &A, cudaStream_t st) {
     P.log_asp = A.log_asp;
     P.log_cnt = A.log_cnt;
     P.flags = A.flags;
-    P.nwork = (int)A.p;
-    int32_t *ctl32 = reinterpret_cast<int32_t *>(ws);
-    P.work_counter = ctl32;
+    int32_t *ctl32 = reinterpret_cast<int32_t *>(ws);  // [0], [2] work counters, [1] err, [3] ovf count
     P.err_flag = ctl32 + 1;
-    P.ws_wc = reinterpret_cast<uint16_t *>(ws + 256);
-    P.ws_wc_stride = wc_stride;
-    if (getenv("MCB_VERBOSE")) fprintf(stderr, "[mcb] wvcp grid=%d (%d/SM) smem=%zu\n", grid, nb, smem);
-    wvcp_kernel<<<grid, WV_NT, smem, st>>>(P);
-    int32_t err = 0;
-    if (cudaGetLastError() != cudaSuccess ||
-        cudaMemcpyAsync(&err, P.err_flag, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess)
-        return set_error(MCB_ERR_CUDA, "wvcp kernel failed: %s", cudaGetErrorString(cudaGetLastError()));
-    if (err == 1) return set_error(MCB_ERR_RANGE, "color id out of range [0, k)");
-    if (err) return set_error(MCB_ERR_CUDA, "wvcp: internal error %d", err);
+    int32_t *ovf = reinterpret_cast<int32_t *>(ws + 256);
+    int rc;
+    int32_t h[3] = {0, 0, 0};
+    if (!wide_only) {
+        P.work_counter = ctl32;
+        P.work_list = nullptr;
+        P.ovf_list = ovf;
+        P.ovf_count = ctl32 + 3;
+        rc = wvcp_launch<uint8_t>(P, A.p, st, ws + ctl_bytes, max_ctas, wc_stride);
+        if (rc) return rc;
+        if (cudaMemcpyAsync(h, ctl32 + 1, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return set_error(MCB_ERR_CUDA, "wvcp kernel failed: %s", cudaGetErrorString(cudaGetLastError()));
+        if (h[0] == 1) return set_error(MCB_ERR_RANGE, "color id out of range [0, k)");
+        if (h[0]) return set_error(MCB_ERR_CUDA, "wvcp: internal error %d", h[0]);
+    }
+    if (wide_only || h[2] > 0) {
+        P.work_counter = ctl32 + 2;
+        P.work_list = wide_only ? nullptr : ovf;
+        P.ovf_list = nullptr;
+        P.ovf_count = nullptr;
+        rc = wvcp_launch<uint16_t>(P, wide_only ? A.p : h[2], st, ws + ctl_bytes, max_ctas, wc_stride);
+        if (rc) return rc;
+        int32_t err = 0;
+        if (cudaMemcpyAsync(&err, P.err_flag, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return set_error(MCB_ERR_CUDA, "wvcp kernel failed: %s", cudaGetErrorString(cudaGetLastError()));
+        if (err == 1) return set_error(MCB_ERR_RANGE, "color id out of range [0, k)");
+        if (err) return set_error(MCB_ERR_CUDA, "wvcp: internal error %d", err);
+    }
     return MCB_OK;
 }
 

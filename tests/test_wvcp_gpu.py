@@ -73,3 +73,29 @@ def test_wvcp_single_apis():
     assert len(res.phi_trajectory) == 4
     pop = LS.improve_population(g, [c, c, c], LS.WVCP, 3, depth=100, max_rounds=2)
     assert len(pop) == 3 and pop[0].iterations_used == 200
+
+
+@pytest.mark.parametrize("case", ["init_overflow", "mixed"])
+def test_wvcp_gamma_overflow_reruns_wide(case, oracle_lib, monkeypatch):
+    """u8 gamma table first: individuals whose neighbour counts reach 256 re-run
+    with u16.  `init_overflow`: degree ~570 on 2 colours (every individual
+    overflows at the start); `mixed`: 3 colours where some starts stay below
+    256 and moves push counts across it.  Both bit-exact vs the oracle, and
+    identical to forcing u16 throughout (MCB_WVCP_WIDE)."""
+    if case == "init_overflow":
+        g, k, p, depth = rand_graph(41, 600, 0.95, wmax=7), 2, 4, 60
+    else:
+        g, k, p, depth = rand_graph(42, 800, 0.97, wmax=9), 3, 6, 80
+    A = random_col_assigns(g.n, k, p, 5)
+    keys = stream_keys(3, TAG_LS, 0, p)
+    phi0 = LS.default_wvcp_phi0(g, k)
+    ref = oracle_lib.wvcp_batch(g, A.copy(), k, keys, depth, 2, True, phi0, log_moves=True)
+    monkeypatch.delenv("MCB_WVCP_WIDE", raising=False)
+    got = LS._run_wvcp_batch(g, A.copy(), k, keys, depth, 2, True, phi0, log_moves=True)
+    monkeypatch.setenv("MCB_WVCP_WIDE", "1")
+    wide = LS._run_wvcp_batch(g, A.copy(), k, keys, depth, 2, True, phi0, log_moves=True)
+    for key in ("end_assigns", "best_assigns", "best_scores", "end_scores", "end_conflicts", "phi_used"):
+        np.testing.assert_array_equal(got[key], ref[key], err_msg=key)
+        np.testing.assert_array_equal(wide[key], ref[key], err_msg=key)
+    for a, b in zip(got["log"], ref["log"]):
+        np.testing.assert_array_equal(a, b)
