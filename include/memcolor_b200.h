@@ -68,6 +68,10 @@ int mcb_debug_phase_cycles(unsigned long long *out, int reset);
 /* Diagnostics: counters of the last warp-kernel TabuCol launch made with
  * MCB_FLAG_WSTATS (out: 40 counters, see tabucol_warp.cu WS_*). */
 int mcb_debug_warp_stats(unsigned long long *out);
+/* WVCP kernel under MCB_FLAG_WSTATS: out[0] iterations, out[1..8] thread 0's
+ * cycles per phase (pass 1, chunk minima, prefix + walks, warp-0 section,
+ * gamma update, class refresh, best copy, tail); reset != 0 clears them. */
+int mcb_debug_wvcp_stats(unsigned long long *out, int reset);
 /* Diagnostics: the exact fp64 divisibility test of the reservoir draws against
  * the 64-bit integer %, on `count` pseudo-random pairs; out: #mismatches. */
 int mcb_debug_modcheck(int64_t count, unsigned long long *mismatches);

@@ -96,6 +96,7 @@ int segsum_sorted_run(int dtype, const void *lam, const int32_t *order, const in
                       int64_t k, int64_t L, const void *A, const void *C, double slope, void *z, cudaStream_t st);
 int rowbias_affine_leaky_run(int dtype, void *z, const void *r, const void *A, const void *C, double slope,
                              int64_t B, int64_t k, int64_t L, cudaStream_t st);
+int wvcp_stats(unsigned long long *out, int reset);
 int stream_values_run(const uint64_t *keys, const uint64_t *ctrs, uint64_t *out, int64_t count,
                       cudaStream_t st);
 

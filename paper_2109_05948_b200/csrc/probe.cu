@@ -58,6 +58,7 @@ extern "C" int mcb_debug_phase_cycles(unsigned long long *out, int reset) {
 }
 
 extern "C" int mcb_debug_warp_stats(unsigned long long *out) { return mcb::tabucol_warp_stats(out); }
+extern "C" int mcb_debug_wvcp_stats(unsigned long long *out, int reset) { return mcb::wvcp_stats(out, reset); }
 
 // Diagnostics: mod_is_zero (common.cuh) against the 64-bit % on `count`
 // pseudo-random (x, s) pairs, s drawn log-uniformly from [1, 2^32).

@@ -134,7 +134,12 @@ __device__ __forceinline__ double shfl_d(double x, int src) {
 // GT: gamma element type.  uint8_t halves the dominant shared-memory table
 // (2 -> 4 individuals per SM at config 4); a count that would reach 256 stops
 // the individual, which the host re-runs with uint16_t.
-template <typename GT>
+// MCB_FLAG_WSTATS: thread 0's cycles per phase, summed over all iterations
+// ([0] iterations, [1..8] phases: pass 1, chunk minima, prefix + walks, warp-0
+// section, gamma update, class refresh, best copy, tail)
+__device__ unsigned long long g_wvstats[16];
+
+template <typename GT, bool STATS>
 __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
     constexpr bool NARROW = sizeof(GT) == 1;
     constexpr int NT = WV_NT, NW = NT / 32;
@@ -308,7 +313,24 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
             }
             for (int v = tid; v < n; v += NT) tabu_until[v] = 0;
             __syncthreads();
+            // phase counters live in shared memory (thread 0 only): no registers
+            // held across the iteration when the flag is off
+            __shared__ unsigned long long s_wsa[9];
+            __shared__ long long s_wt0;
+            constexpr bool wst = STATS;
+            if (wst && tid == 0)
+                for (int i = 0; i < 9; i++) s_wsa[i] = 0;
+#define WVPH(i)                                              \
+    if (wst && tid == 0) {                                   \
+        const long long t1 = clock64();                      \
+        s_wsa[i] += (unsigned long long)(t1 - s_wt0);        \
+        s_wt0 = t1;                                          \
+    }
             for (int64_t step = 0; step < P.depth; step++) {
+                if (wst && tid == 0) {
+                    s_wsa[0]++;
+                    s_wt0 = clock64();
+                }
                 const long long it = ctl.it, score = ctl.score, conflicts = ctl.conflicts,
                                 best = ctl.best;
                 const double phi = ctl.phi;
@@ -408,6 +430,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     rcnt[v] = (uint16_t)cnt;
                 }
                 __syncthreads();
+                WVPH(1);
                 // prefix-min over the rows in vertex order, parallel over the warps:
                 // chunks of 32 rows (warp w: chunks w, w + NW, ...); (1) chunk
                 // minima; (2) each warp enters its chunks with the minimum of the
@@ -425,6 +448,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     if (lane == 0) s_cmin[cb] = x;
                 }
                 __syncthreads();
+                WVPH(2);
                 {
                     double lmin = INF;
                     int lT = 0, lfirst = INT_MAX, tsum = 0;
@@ -512,6 +536,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     }
                 }
                 __syncthreads();
+                WVPH(3);
                 if (warp == 0) {
                     // lane w carries warp w's partials into the combination below
                     double lmin = lane < NW ? s_wmin[lane] : INF;
@@ -657,6 +682,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     (void)mv_b;
                 }
                 __syncthreads();
+                WVPH(4);
                 if (ctl.has_move) {
                     const int v = ctl.mv_v, a = ctl.mv_a, b = ctl.mv_b;
                     // gamma over N(v) (:218-221)
@@ -674,9 +700,11 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                         assign[v] = (uint8_t)b;
                     }
                     __syncthreads();
+                    WVPH(5);
                     if (warp == 0) refresh_class(a);
                     else if (warp == 1) refresh_class(b);
                     __syncthreads();
+                    WVPH(6);
                     if (tid == 0 && ctl.conflicts == 0 && ctl.score < ctl.best) {
                         ctl.best = ctl.score;
                         ctl.red[0] = 1;  // copy flag
@@ -684,6 +712,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                         ctl.red[0] = 0;
                     }
                     __syncthreads();
+                    WVPH(7);
                     if (ctl.red[0])
                         for (int u = tid; u < n; u += NT) b_out[u] = assign[u];
                 }
@@ -715,8 +744,12 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     }
                 }
                 __syncthreads();
+                WVPH(8);
                 if (NARROW && ctl.ovf) break;
             }
+            if (wst && tid == 0)
+                for (int i = 0; i < 9; i++) atomicAdd(&g_wvstats[i], s_wsa[i]);
+#undef WVPH
             if (tid == 0) {  // phi schedule (:251-258)
                 if (P.schedule_on && rnd < P.rounds - 1) {
                     ctl.phi = (ctl.conflicts == 0) ? ctl.phi / 2.0 : ctl.phi * 2.0;
@@ -751,17 +784,17 @@ static size_t wv_smem(int n, int k, int gbytes) {
            2 * a16((size_t)k * 8) + a16((size_t)k * 4) + a16((size_t)2 * n * 4) + a16((size_t)n * 8);
 }
 
-template <typename GT>
-static int wvcp_launch(WvParams P, int64_t nwork, cudaStream_t st, uint8_t *ws_base, size_t ws_cap_ctas,
-                       size_t wc_stride) {
+template <typename GT, bool STATS>
+static int wvcp_launch_t(WvParams P, int64_t nwork, cudaStream_t st, uint8_t *ws_base, size_t ws_cap_ctas,
+                         size_t wc_stride) {
     const size_t smem = wv_smem(P.n, P.k, sizeof(GT));
     if (smem > (size_t)max_smem_optin())
         return set_error(MCB_ERR_UNSUPPORTED, "wvcp: n*k too large for shared memory (%zu B)", smem);
-    if (cudaFuncSetAttribute(wvcp_kernel<GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(wvcp_kernel<GT, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return set_error(MCB_ERR_CUDA, "wvcp: smem attribute failed");
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wvcp_kernel<GT>, WV_NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wvcp_kernel<GT, STATS>, WV_NT, smem);
     nb = std::max(nb, 1);
     const int grid = (int)std::min<int64_t>(std::min<int64_t>(nwork, (int64_t)nb * num_sms()), ws_cap_ctas);
     P.nwork = (int)nwork;
@@ -770,8 +803,26 @@ static int wvcp_launch(WvParams P, int64_t nwork, cudaStream_t st, uint8_t *ws_b
     if (getenv("MCB_VERBOSE"))
         fprintf(stderr, "[mcb] wvcp<gamma u%d> grid=%d (%d/SM) smem=%zu work=%lld\n", (int)(8 * sizeof(GT)), grid,
                 nb, smem, (long long)nwork);
-    wvcp_kernel<GT><<<grid, WV_NT, smem, st>>>(P);
+    wvcp_kernel<GT, STATS><<<grid, WV_NT, smem, st>>>(P);
     if (cudaGetLastError() != cudaSuccess) return set_error(MCB_ERR_CUDA, "wvcp launch failed");
+    return MCB_OK;
+}
+
+// the phase counters are a separate instantiation: zero cost when off
+template <typename GT>
+static int wvcp_launch(WvParams P, int64_t nwork, cudaStream_t st, uint8_t *ws_base, size_t ws_cap_ctas,
+                       size_t wc_stride) {
+    return (P.flags & MCB_FLAG_WSTATS) ? wvcp_launch_t<GT, true>(P, nwork, st, ws_base, ws_cap_ctas, wc_stride)
+                                       : wvcp_launch_t<GT, false>(P, nwork, st, ws_base, ws_cap_ctas, wc_stride);
+}
+
+int wvcp_stats(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, g_wvstats, sizeof(unsigned long long) * 16) != cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "wvcp stats unavailable");
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_wvstats, z, sizeof(z));
+    }
     return MCB_OK;
 }
 

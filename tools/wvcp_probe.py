@@ -1,0 +1,36 @@
+"""Per-phase cycles of the WVCP kernel (MCB_FLAG_WSTATS, thread 0's clock64
+between the CTA barriers), per iteration, at the config-4 shape.
+
+    python tools/wvcp_probe.py [--pop 592 --depth 300 --rounds 2]
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2109_05948_b200 import _native as N  # noqa: E402
+from paper_2109_05948_b200 import localsearch as LS  # noqa: E402
+from paper_2109_05948_b200.graph import rand_graph  # noqa: E402
+from paper_2109_05948_b200.init import random_col_assigns  # noqa: E402
+from paper_2109_05948_b200.rng import TAG_LS, stream_keys  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--pop", type=int, default=592)
+ap.add_argument("--depth", type=int, default=300)
+ap.add_argument("--rounds", type=int, default=2)
+a = ap.parse_args()
+g = rand_graph(1, 500, 0.5, wmax=100)
+k = 60
+A = random_col_assigns(500, k, a.pop, 1)
+keys = stream_keys(1, TAG_LS, 0, a.pop)
+phi0 = LS.default_wvcp_phi0(g, k)
+buf = (ctypes.c_ulonglong * 16)()
+N.check(N.lib().mcb_debug_wvcp_stats(ctypes.addressof(buf), 1))
+LS._run_wvcp_batch(g, A.copy(), k, keys, a.depth, a.rounds, True, phi0, flags=N.FLAG_WSTATS)
+N.check(N.lib().mcb_debug_wvcp_stats(ctypes.addressof(buf), 1))
+it = max(buf[0], 1)
+names = ["pass1", "chunk_min", "prefix_walks", "warp0", "gamma_update", "refresh", "best", "tail"]
+print(json.dumps({"iterations": buf[0], **{nm: round(buf[i + 1] / it, 1) for i, nm in enumerate(names)},
+                  "total": round(sum(buf[1:9]) / it, 1)}))
