@@ -164,3 +164,21 @@ def test_surrogate_api_edges():
     losses = net.train_generation(np.zeros((1, 12), np.int32), np.array([5.0]), 3, 2, 4,
                                   Stream.derive(0, TAG_TRAIN, 1))
     assert len(losses) == 2 and net.target_std == 1.0 and net.target_mean == 5.0
+
+
+def test_tf32_option_is_close_and_off_by_default():
+    """tf32=True (opt-in) runs the GEMMs on the tensor cores: predictions stay
+    within TF32 rounding of the float32 net; the default leaves the global
+    cuBLAS setting alone and computes in float32."""
+    a = random_col_assigns(64, 6, 40, 3)
+    test = random_col_assigns(64, 6, 30, 4)
+    y = _targets(a)
+    ref = SurrogateNet(64, arch="small", seed=5)
+    fast = SurrogateNet(64, arch="small", seed=5, tf32=True)
+    assert not ref.tf32 and fast.tf32
+    before = torch.backends.cuda.matmul.allow_tf32
+    ref.train_generation(a, y, 6, 2, 8, Stream.derive(5, TAG_TRAIN, 0))
+    fast.train_generation(a, y, 6, 2, 8, Stream.derive(5, TAG_TRAIN, 0))
+    p_ref, p_fast = ref.predict_assigns(test, 6), fast.predict_assigns(test, 6)
+    assert torch.backends.cuda.matmul.allow_tf32 == before
+    np.testing.assert_allclose(p_fast, p_ref, rtol=2e-2, atol=2e-2 * np.abs(p_ref).max())

@@ -219,6 +219,9 @@ def bench_surrogate(a):
         return net.predict_assigns_device(cands, k)
 
     t, _ = timed(run, reps=1)
+    net.tf32 = True  # opt-in tensor-core GEMMs (not the reference's float32 products)
+    t_tf32, _ = timed(run, reps=1)
+    net.tf32 = False
     # reference-style CPU cost: dense one-hot numpy forward, bounded sample
     lam = [l.lam.cpu().numpy() for l in net.layers]
     x = np.zeros((64, k, n), np.float32)
@@ -232,7 +235,7 @@ def bench_surrogate(a):
     return {"op": "surrogate", "unit": "candidates/s", "gpu": p * K / t, "cpu": 1.0 / tc, "cores": os.cpu_count(),
             "config": f"n={n} k={k} arch small float32: predict {p}x{K} candidates + 1 epoch on {p} rows (batch 64)",
             "cpu_sample": "64 candidates, dense one-hot numpy matmuls (forward only, no BN: a lower bound)",
-            "gpu_ms": 1e3 * t}
+            "gpu_ms": 1e3 * t, "gpu_ms_tf32_opt_in": 1e3 * t_tf32}
 
 
 def main():
