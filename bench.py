@@ -322,6 +322,7 @@ def run_ours(args):
                          "(C restatement of _tabucol_batch, OpenMP)"}
 
     clocks = clk.summary()
+    traffic, traffic_src = ncu_traffic(D // world)
     line = {
         "metric": METRIC,
         "value": value,
@@ -343,7 +344,7 @@ def run_ours(args):
                        ", NCCL all_gather of elites per step" if world > 1 else ""),
                    "l2": "flushed (256 MB write) between timed steps"},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-                     "frac": achieved / smem_peak, "traffic": None,
+                     "frac": achieved / smem_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": kernel_desc,
                      "peak_source": "measured: mcb_probe_smem_bandwidth (LDS.128 stream, all SMs)",
                      "alg_bytes_per_launch": alg_bytes_total / args.steps,
@@ -361,6 +362,25 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def ncu_traffic(individuals):
+    """DRAM bytes (read + write) of one launch of the TabuCol kernel from the
+    committed `ncu --set full` capture (profiles/r01c_tabucol_warp_ncu_raw.csv:
+    one wave of 1184 individuals x 50k iterations, same kernel variant), scaled
+    to this launch's individuals; (None, reason) when the capture is absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01c_tabucol_warp_ncu_raw.csv")
+    try:
+        import csv
+
+        rows = list(csv.reader(open(path)))
+        h, u, v = rows[0], rows[1], rows[2]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = sum(float(v[h.index(m)]) * scale[u[h.index(m)]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        return tot * individuals / 1184.0, ("ncu --set full of the same kernel variant (profiles/r01c_tabucol_warp_ncu_raw"
+                                            ".csv, D=1184), dram read+write scaled per individual; the state stays on chip")
+    except (OSError, ValueError, KeyError, IndexError):
+        return None, "no ncu capture in profiles/"
 
 
 def main():
