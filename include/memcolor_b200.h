@@ -218,6 +218,10 @@ int mcb_greedy_wvcp_init_host(const int32_t *order, const int64_t *indptr, const
  */
 int mcb_segsum(int dtype_bytes, int backward, const void *src, const int32_t *assigns, int64_t B, int64_t n,
                int64_t k, int64_t L, void *dst, void *stream);
+/* Same, without the colour-range check and its synchronising readback
+ * (CUDA-graph capturable); ids must already be in [0, k). */
+int mcb_segsum_async(int dtype_bytes, int backward, const void *src, const int32_t *assigns, int64_t B, int64_t n,
+                     int64_t k, int64_t L, void *dst, void *stream);
 /*
  * Inference path of the surrogate (eval mode, :137-178 with the one-hot
  * folded in).  mcb_colour_order: stable counting sort of each coloring's

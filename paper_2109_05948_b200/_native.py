@@ -30,7 +30,7 @@ EXPORTS = [
     "mcb_probe_smem_bandwidth", "mcb_debug_phase_cycles", "mcb_debug_warp_stats", "mcb_debug_wvcp_stats",
     "mcb_debug_modcheck", "mcb_tabucol_describe",
     "mcb_update_population", "mcb_update_population_host", "mcb_match_parents", "mcb_match_parents_host",
-    "mcb_greedy_wvcp_init", "mcb_greedy_wvcp_init_host", "mcb_segsum",
+    "mcb_greedy_wvcp_init", "mcb_greedy_wvcp_init_host", "mcb_segsum", "mcb_segsum_async",
     "mcb_colour_order", "mcb_segsum_sorted", "mcb_rowbias_affine_leaky",
 ]
 
@@ -75,6 +75,7 @@ def _declare(L):
     L.mcb_greedy_wvcp_init.argtypes = [P, P, P, I64, P, I64, P, P, P]
     L.mcb_greedy_wvcp_init_host.argtypes = [P, P, P, I64, P, I64, P, P, P]
     L.mcb_segsum.argtypes = [C.c_int, C.c_int, P, P, I64, I64, I64, I64, P, P]
+    L.mcb_segsum_async.argtypes = [C.c_int, C.c_int, P, P, I64, I64, I64, I64, P, P]
     L.mcb_colour_order.argtypes = [P, I64, I64, I64, P, P, P]
     L.mcb_segsum_sorted.argtypes = [C.c_int, P, P, P, I64, I64, I64, I64, P, P, C.c_double, P, P]
     L.mcb_rowbias_affine_leaky.argtypes = [C.c_int, P, P, P, P, C.c_double, I64, I64, I64, P]

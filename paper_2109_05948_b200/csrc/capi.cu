@@ -512,6 +512,12 @@ int mcb_segsum(int dtype_bytes, int backward, const void *src, const int32_t *as
     return segsum_run(dtype_bytes, backward != 0, src, assigns, B, n, k, L, dst, (cudaStream_t)stream);
 }
 
+int mcb_segsum_async(int dtype_bytes, int backward, const void *src, const int32_t *assigns, int64_t B, int64_t n,
+                     int64_t k, int64_t L, void *dst, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return segsum_run(dtype_bytes, backward != 0, src, assigns, B, n, k, L, dst, (cudaStream_t)stream, false);
+}
+
 int mcb_colour_order(const int32_t *assigns, int64_t B, int64_t n, int64_t k, int32_t *order, int32_t *offs,
                      void *stream) {
     std::lock_guard<std::mutex> lk(g_mu);

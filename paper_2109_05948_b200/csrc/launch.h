@@ -89,7 +89,7 @@ int match_parents_run(const int32_t *dist, int64_t p, int64_t K, int64_t max_dis
 int greedy_init_run(const int32_t *order, const int64_t *indptr, const int32_t *indices, int64_t n,
                     const uint64_t *keys, int64_t p, int32_t *assigns, int32_t *used, cudaStream_t st);
 int segsum_run(int dtype, bool backward, const void *src, const int32_t *assigns, int64_t B, int64_t n,
-               int64_t k, int64_t L, void *dst, cudaStream_t st);
+               int64_t k, int64_t L, void *dst, cudaStream_t st, bool checked = true);
 int colour_order_run(const int32_t *assigns, int64_t B, int64_t n, int64_t k, int32_t *order, int32_t *offs,
                      cudaStream_t st);
 int segsum_sorted_run(int dtype, const void *lam, const int32_t *order, const int32_t *offs, int64_t B, int64_t n,

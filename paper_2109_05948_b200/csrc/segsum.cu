@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(SS_TL)
             T *zb = z + (size_t)b * k * L;
             for (int i = 0; i < k; i++) zb[(size_t)i * L + col] = acc[i * SS_TL + c];
         }
-        if (bad) atomicExch(err, 1);
+        if (bad && err) atomicExch(err, 1);
     }
 }
 
@@ -219,7 +219,7 @@ int rowbias_affine_leaky_run(int dtype, void *z, const void *r, const void *A, c
 }
 
 int segsum_run(int dtype, bool backward, const void *src, const int32_t *assigns, int64_t B, int64_t n,
-               int64_t k, int64_t L, void *dst, cudaStream_t st) {
+               int64_t k, int64_t L, void *dst, cudaStream_t st, bool checked) {
     if (B < 0 || n < 1 || k < 1 || L < 1) return set_error(MCB_ERR_VALUE, "segsum: bad shape");
     if (dtype != 4 && dtype != 8) return set_error(MCB_ERR_VALUE, "segsum: dtype must be 4 or 8 bytes");
     if (B == 0) return MCB_OK;
@@ -227,9 +227,11 @@ int segsum_run(int dtype, bool backward, const void *src, const int32_t *assigns
     if (!backward) {
         const size_t smem = (size_t)k * SS_TL * dtype;
         if (smem > (size_t)max_smem_optin()) return set_error(MCB_ERR_UNSUPPORTED, "segsum: k too large");
-        int32_t *err = (int32_t *)workspace(256);
-        if (!err) return set_error(MCB_ERR_CUDA, "segsum: workspace");
-        cudaMemsetAsync(err, 0, 4, st);
+        // unchecked (graph-capturable): no flag word, no readback, no sync --
+        // the caller has range-checked the colour ids
+        int32_t *err = checked ? (int32_t *)workspace(256) : nullptr;
+        if (checked && !err) return set_error(MCB_ERR_CUDA, "segsum: workspace");
+        if (checked) cudaMemsetAsync(err, 0, 4, st);
         const int gx = (int)std::min<int64_t>(B, std::max<int64_t>(1, (int64_t)num_sms() * 16 / ty));
         if (dtype == 4) {
             cudaFuncSetAttribute(segsum_fwd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -240,6 +242,7 @@ int segsum_run(int dtype, bool backward, const void *src, const int32_t *assigns
             segsum_fwd_kernel<double><<<dim3(gx, ty), SS_TL, smem, st>>>((const double *)src, assigns, B, (int)n,
                                                                         (int)k, L, (double *)dst, err);
         }
+        if (!checked) return cudaGetLastError() == cudaSuccess ? MCB_OK : set_error(MCB_ERR_CUDA, "segsum launch failed");
         int32_t herr = 0;
         if (cudaGetLastError() != cudaSuccess ||
             cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||

@@ -124,13 +124,15 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
     p, n, k, t = st.p, st.n, st.k, st.generation
     dev = st.pop_assigns.device
     ms = min_spacing(n) if ms is None else ms
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if timings is not None else None
+    marks = []  # (stage ending here, event)
 
-    def mark(i):
-        if ev:
-            ev[i].record()
+    def mark(name):
+        if timings is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append((name, e))
 
-    mark(0)
+    mark(None)
     keys = Dv.keys_to_tensor(stream_keys(seed, TAG_LS, t, p), dev)
     if st.mode == "wvcp":
         if phi0 is None:
@@ -144,6 +146,7 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
         ls = Dv.tabucol_batch(dg, st.offspring.clone(), k, keys, depth)
         improved, imp_fit = ls["best_assigns"], ls["best_conflicts"]
     st.best_score = min(st.best_score, int(imp_fit.min().item()))
+    mark("ls")
     if net is not None:
         from .rng import TAG_TRAIN, Stream
 
@@ -151,9 +154,9 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
         if int(mask.sum().item()) >= 2:
             net.train_generation(st.offspring[mask], imp_fit[mask].double().cpu().numpy(), k, epochs, batch_size,
                                  Stream.derive(seed, TAG_TRAIN, t))
-    mark(1)
+        mark("surrogate_train")
     cross, within = Dv.pairwise(st.pop_assigns, improved, k)
-    mark(2)
+    mark("distances")
     adm = torch.empty(p, dtype=torch.int32, device=dev)
     rule = torch.empty(p, dtype=torch.uint8, device=dev)
     new_dist = torch.empty((p, p), dtype=torch.int32, device=dev)
@@ -165,12 +168,13 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
         P(st.pop_assigns), P(improved), n, P(adm), P(rule), P(new_dist), P(new_assigns), P(new_fit),
         _stream()))
     st.pop_assigns, st.pop_fitness, st.pop_dist = new_assigns, new_fit, new_dist
-    mark(3)
+    mark("update_population")
     matches = torch.empty((p, K), dtype=torch.int64, device=dev)
     N.check(N.lib().mcb_match_parents(P(st.pop_dist), p, int(K), n, P(matches), _stream()))
-    mark(4)
+    mark("match_parents")
     ck = Dv.keys_to_tensor(stream_keys(seed, TAG_CROSS, t, p * K), dev)
     cands = Dv.gpx_batch(st.pop_assigns, matches, k, ck)
+    mark("gpx")
     if net is not None:
         pred = net.predict_assigns_device(cands.reshape(p * K, n), k).reshape(p, K)
         sel = pred.argmin(dim=1)
@@ -183,11 +187,10 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
         hi, lo = (sv >> 32) & 0xFFFFFFFF, sv & 0xFFFFFFFF  # unsigned 64-bit value mod K in int64
         sel = ((hi % K) * ((1 << 32) % K) + lo % K) % K
     st.offspring = cands[torch.arange(p, device=dev), sel].contiguous()
-    mark(5)
+    mark("surrogate_select" if net is not None else "select")
     st.generation = t + 1
     if timings is not None:
         torch.cuda.synchronize()
-        for name, i in (("ls", 0), ("distances", 1), ("update_population", 2), ("match_parents", 3),
-                        ("offspring", 4)):
-            timings[name] = timings.get(name, 0.0) + ev[i].elapsed_time(ev[i + 1]) / 1e3
+        for (_, e0), (name, e1) in zip(marks[:-1], marks[1:]):
+            timings[name] = timings.get(name, 0.0) + e0.elapsed_time(e1) / 1e3
     return ls

@@ -182,3 +182,24 @@ def test_tf32_option_is_close_and_off_by_default():
     p_ref, p_fast = ref.predict_assigns(test, 6), fast.predict_assigns(test, 6)
     assert torch.backends.cuda.matmul.allow_tf32 == before
     np.testing.assert_allclose(p_fast, p_ref, rtol=2e-2, atol=2e-2 * np.abs(p_ref).max())
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_graph_training_equals_eager(dtype):
+    """CUDA-graph replays of the minibatch step (default) give exactly the
+    eager step's parameters, moments, running statistics and losses --
+    including a tail minibatch of another size and a second call that reuses
+    the captured graphs."""
+    a = random_col_assigns(30, 5, 45, 8)
+    y = _targets(a)
+    nets = [SurrogateNet(30, arch="small", seed=4, dtype=dtype) for _ in range(2)]
+    for t in range(2):
+        l0 = nets[0].train_generation(a, y + t, 5, 2, 8, Stream.derive(4, TAG_TRAIN, t), graphs=True)
+        l1 = nets[1].train_generation(a, y + t, 5, 2, 8, Stream.derive(4, TAG_TRAIN, t), graphs=False)
+        assert l0 == l1
+    for p0, p1 in zip(nets[0]._flat_params() + nets[0].adam_m + nets[0].adam_v,
+                      nets[1]._flat_params() + nets[1].adam_m + nets[1].adam_v):
+        assert torch.equal(p0, p1)
+    for l0, l1 in zip(nets[0].layers, nets[1].layers):
+        assert torch.equal(l0.run_mean, l1.run_mean) and torch.equal(l0.run_var, l1.run_var)
+    assert nets[0].adam_t == nets[1].adam_t == 2 * 2 * 6

@@ -29,18 +29,26 @@ ap.add_argument("--p", type=int, default=16384)
 ap.add_argument("--K", type=int, default=16)
 ap.add_argument("--depth", type=int, default=2000)
 ap.add_argument("--gens", type=int, default=2)
+ap.add_argument("--surrogate", action="store_true", help="surrogate-guided selection (arch small, float32)")
+ap.add_argument("--tf32", action="store_true", help="surrogate GEMMs on TF32 tensor cores (opt-in)")
+ap.add_argument("--epochs", type=int, default=1)
 a = ap.parse_args()
 t0 = time.time()
 g = rand_graph(1, a.n, 0.5)
 dg = Dv.DeviceGraph(g, "cuda")
 A = random_col_assigns(a.n, a.k, a.p, 1)
 st = E.init_state(dg, A, a.k)
+net = None
+if a.surrogate:
+    from paper_2109_05948_b200.surrogate import SurrogateNet
+
+    net = SurrogateNet(a.n, problem="col", arch="small", seed=1, tf32=a.tf32)
 torch.cuda.synchronize()
 for t in range(a.gens):
     tim = {}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    ls = E.col_generation(dg, st, seed=1, depth=a.depth, K=a.K, timings=tim)
+    ls = E.generation(dg, st, seed=1, depth=a.depth, K=a.K, timings=tim, net=net, epochs=a.epochs)
     e1.record()
     torch.cuda.synchronize()
     moves = int(ls["iters_used"].sum().item())
@@ -48,4 +56,6 @@ for t in range(a.gens):
                       "stages_s": {k_: round(v, 4) for k_, v in tim.items()},
                       "ls_moves": moves, "ls_moves_per_s": moves / tim["ls"],
                       "best": st.best_score, "pop_fitness_mean": float(st.pop_fitness.float().mean()),
-                      "config": f"G({a.n},.5) k={a.k} p={a.p} K={a.K} LS depth {a.depth}"}), flush=True)
+                      "config": f"G({a.n},.5) k={a.k} p={a.p} K={a.K} LS depth {a.depth}"
+                                + (f", surrogate small{' tf32' if a.tf32 else ''} {a.epochs} epoch(s)" if net else "")}),
+          flush=True)

@@ -219,6 +219,9 @@ def bench_surrogate(a):
         return net.predict_assigns_device(cands, k)
 
     t, _ = timed(run, reps=1)
+    t_train, _ = timed(lambda: net.train_generation(train, y, k, 1, 64, Stream.derive(1, TAG_TRAIN, 0)), reps=1)
+    t_train_eager, _ = timed(lambda: net.train_generation(train, y, k, 1, 64, Stream.derive(1, TAG_TRAIN, 0),
+                                                          graphs=False), reps=1)
     net.tf32 = True  # opt-in tensor-core GEMMs (not the reference's float32 products)
     t_tf32, _ = timed(run, reps=1)
     net.tf32 = False
@@ -235,7 +238,8 @@ def bench_surrogate(a):
     return {"op": "surrogate", "unit": "candidates/s", "gpu": p * K / t, "cpu": 1.0 / tc, "cores": os.cpu_count(),
             "config": f"n={n} k={k} arch small float32: predict {p}x{K} candidates + 1 epoch on {p} rows (batch 64)",
             "cpu_sample": "64 candidates, dense one-hot numpy matmuls (forward only, no BN: a lower bound)",
-            "gpu_ms": 1e3 * t, "gpu_ms_tf32_opt_in": 1e3 * t_tf32}
+            "gpu_ms": 1e3 * t, "gpu_ms_tf32_opt_in": 1e3 * t_tf32,
+            "train_epoch_ms_graphs": 1e3 * t_train, "train_epoch_ms_eager": 1e3 * t_train_eager}
 
 
 def main():
