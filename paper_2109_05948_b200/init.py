@@ -45,8 +45,6 @@ def stream_keys_init(master_seed, p, start=0):
 
 
 def init_col_population(n, k, p, master_seed):
-    from dataclasses import dataclass
-
     assigns = random_col_assigns(n, k, p, master_seed)
     return InitOutcome(colorings=[Coloring(a, k) for a in assigns], k=k)
 
