@@ -184,10 +184,6 @@ __device__ __forceinline__ uint32_t zero_flags(uint32_t z) {
     return ~(((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & 0x80808080u;
 }
 __device__ __forceinline__ int count_eq(uint32_t x, uint32_t M) { return __popc(zero_flags(x ^ M)); }
-__device__ __forceinline__ uint32_t min_bytes(uint32_t x) {
-    const uint32_t m2 = __vminu2(x & 0x00FF00FFu, __byte_perm(x, 0, 0x4341));
-    return min(m2 & 0xFFFFu, m2 >> 16);
-}
 // (minimum byte, #bytes at it) of a row held as KW words
 template <int KW>
 __device__ __forceinline__ void row_min_count(const uint32_t (&x)[KW], uint32_t xorv, int &m, int &c) {

@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     for (int o = 16; o > 0; o >>= 1)
                         carry = fmin(carry, __longlong_as_double(__shfl_xor_sync(FULL, __double_as_longlong(carry), o)));
                     const double D = carry;
-                    int mv_v = -1, mv_b = 0;
+                    int mv_v = -1;
                     long long mv_ds = 0, mv_dc = 0;
                     bool mv_tabu = false;
                     if (D != INF) {
@@ -643,7 +643,6 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                             cum += hc;
                         }
                         mv_v = v;
-                        mv_b = b;
                         mv_ds = bds;
                         mv_dc = bdc;
                         mv_tabu = frozen;
@@ -679,7 +678,6 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                         }
                     }
                     if (lane == 0) ctl.has_move = (mv_v >= 0);
-                    (void)mv_b;
                 }
                 __syncthreads();
                 WVPH(4);
