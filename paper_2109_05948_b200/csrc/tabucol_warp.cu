@@ -184,28 +184,6 @@ __device__ __forceinline__ uint32_t zero_flags(uint32_t z) {
     return ~(((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & 0x80808080u;
 }
 __device__ __forceinline__ int count_eq(uint32_t x, uint32_t M) { return __popc(zero_flags(x ^ M)); }
-// (minimum byte, #bytes at it) of a row held as KW words
-template <int KW>
-__device__ __forceinline__ void row_min_count(const uint32_t (&x)[KW], uint32_t xorv, int &m, int &c) {
-    uint32_t m0 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu, m3 = 0xFFFFFFFFu;
-#pragma unroll
-    for (int w = 0; w < KW; w += 2) {
-        const uint32_t y0 = x[w] ^ xorv;
-        m0 = __vminu2(m0, y0 & 0x00FF00FFu);
-        m1 = __vminu2(m1, __byte_perm(y0, 0, 0x4341));
-        if (w + 1 < KW) {
-            const uint32_t y1 = x[w + 1] ^ xorv;
-            m2 = __vminu2(m2, y1 & 0x00FF00FFu);
-            m3 = __vminu2(m3, __byte_perm(y1, 0, 0x4341));
-        }
-    }
-    const uint32_t mm = __vminu2(__vminu2(m0, m1), __vminu2(m2, m3));
-    m = (int)min(mm & 0xFFFFu, mm >> 16);
-    const uint32_t M = ((uint32_t)m * 0x01010101u) ^ xorv;
-    c = 0;
-#pragma unroll
-    for (int w = 0; w < KW; w++) c += count_eq(x[w], M);
-}
 template <int KV>
 __device__ __forceinline__ void load_row(const uint8_t *grow, uint32_t (&x)[4 * KV]) {
     const uint4 *r4 = reinterpret_cast<const uint4 *>(grow);
