@@ -29,7 +29,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .rng import TAG_CROSS, TAG_LS, stream_keys
+from .rng import TAG_CROSS, TAG_LS, TAG_SELECT, stream_keys, stream_values
 
 
 def shard_range(total, world, rank):
@@ -115,3 +115,33 @@ def offspring_sharded(pop, matches, k, master_seed, generation, gpx_fn, group=No
     keys = stream_keys(master_seed, TAG_CROSS, generation, (hi - lo) * K, start=lo * K)
     out = gpx_fn(pop, matches[lo:hi], k, keys, lo)
     return _all_gather_rows(out.astype(np.int32), p, group, device)
+
+
+def col_generation_sharded(g, pop_assigns, pop_fitness, pop_dist, offspring, k, master_seed, generation, depth,
+                           K, ms, ops, group=None, device="cpu"):
+    """One k-colouring generation of `mc/engine.py:_generation_loop` (:203-316,
+    uniform selection) with the population split over the ranks.
+
+    Sharded: the local search (by individual), the distance job space, GPX
+    (by individual).  Replicated on every rank (deterministic, so every rank
+    holds the same population afterwards): `update_population`,
+    `match_parents`, the `TAG_SELECT` draws.  `ops` maps "ls", "pair", "gpx"
+    to the callables of `improve_col_sharded` / `pairwise_sharded` /
+    `offspring_sharded`, "update" to `(pdist, pop_fit, pop_assigns, improved,
+    improved_fit, cross, within, ms) -> (admitted, by_rule, new_dist,
+    new_assigns, new_fit)` and "match" to `(dist, K) -> int64[p, K]`.
+    Returns (pop_assigns, pop_fitness, pop_dist, offspring, improved) as numpy.
+    """
+    ls = improve_col_sharded(g, offspring, k, master_seed, generation, depth, ops["ls"], group, device)
+    improved, imp_fit = ls["best_assigns"], ls["best_conflicts"].astype(np.int64)
+    cross, within = pairwise_sharded(pop_assigns, improved, k, ops["pair"], group, device)
+    _, _, new_dist, new_assigns, new_fit = ops["update"](pop_dist, pop_fitness, pop_assigns, improved, imp_fit,
+                                                         cross, within, ms)
+    matches = ops["match"](new_dist, K)
+    cands = offspring_sharded(new_assigns, matches, k, master_seed, generation, ops["gpx"], group, device)
+    p = new_assigns.shape[0]
+    # Stream.derive(seed, TAG_SELECT, t, i).below(K) = stream_value(key, 0) % K
+    sel = stream_values(stream_keys(master_seed, TAG_SELECT, generation, p), np.zeros(p, np.uint64)) % np.uint64(K)
+    off = cands[np.arange(p), sel.astype(np.int64)]
+    return new_assigns, new_fit, new_dist, np.ascontiguousarray(off), improved
+

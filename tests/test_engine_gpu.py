@@ -101,3 +101,46 @@ def test_engine_selection_is_in_range_and_keeps_shapes():
     conf = (a[:, g.edges[:, 0]] == a[:, g.edges[:, 1]]).sum(axis=1)
     np.testing.assert_array_equal(conf, st.pop_fitness.cpu().numpy())
     assert st.offspring.shape == (64, 150) and st.generation == 2
+
+
+def test_sharded_generation_composition_with_cuda_operators():
+    """`shard.col_generation_sharded` (single process: world 1) with the CUDA
+    operators as its compute reproduces the reference chain: the composition
+    that the N-GPU run uses with NCCL."""
+    from paper_2109_05948_b200 import distance as DI
+    from paper_2109_05948_b200 import localsearch as LSm
+    from paper_2109_05948_b200 import population as PP
+    from paper_2109_05948_b200.population import min_spacing
+    from paper_2109_05948_b200.shard import col_generation_sharded
+
+    def upd(pdist, fit, pa, imp, imp_fit, cross, within, ms):
+        pop = PP.Population(assigns=pa, k=0, fitness=fit, dist=pdist)
+        out = PP.update_population(pop, imp, imp_fit, cross, within, ms)
+        return None, out.admitted_by_rule, out.dist, out.assigns, out.fitness
+
+    def gpx_rows(pop, mrows, k, keys, off):
+        pt = torch.as_tensor(pop).cuda()
+        mt = torch.as_tensor(mrows).cuda()
+        kt = Dv.keys_to_tensor(keys, "cuda")
+        return Dv.gpx_rows(pt, mt, off, k, kt).cpu().numpy()
+
+    ops = {"ls": lambda g_, a, k_, keys, d: LSm._run_tabucol_batch(g_, a, k_, keys, d),
+           "pair": lambda a, b, k_, lo, hi: DI.pairwise_raw(a, b, k_, lo, hi),
+           "gpx": gpx_rows, "update": upd}
+    for name in [str(c) for c in ENG["cases"]]:
+        pre = name + "__"
+        seed, n, pe, k, p, K, depth, G = (int(x) for x in ENG[pre + "params"])
+        g = rand_graph(seed, n, pe / 1000.0)
+        A = ENG[pre + "init"].astype(np.int32)
+        fit = (A[:, g.edges[:, 0]] == A[:, g.edges[:, 1]]).sum(axis=1).astype(np.int64)
+        pd = DI.pairwise_raw(A[:0], A, k)[1]
+        off = A.copy()
+        # match_parents bounds distances by the population's n
+        ops["match"] = lambda d, K, n=n: PP.match_parents(
+            PP.Population(assigns=np.zeros((d.shape[0], n), np.int32), k=0, fitness=None, dist=d), K)
+        for t in range(G):
+            A, fit, pd, off, imp = col_generation_sharded(g, A, fit, pd, off, k, seed, t, depth, K,
+                                                          min_spacing(n), ops)
+            np.testing.assert_array_equal(A, ENG[pre + f"g{t}_pop"], err_msg=f"{name} g{t}")
+            np.testing.assert_array_equal(pd, ENG[pre + f"g{t}_dist"])
+            np.testing.assert_array_equal(off, ENG[pre + f"g{t}_offspring"])

@@ -84,3 +84,55 @@ def test_single_process_passthrough(oracle_lib):
     got = improve_col_sharded(g, A, 5, 9, 0, 300, ls)
     ref = oracle_lib.tabucol_batch(g, A.copy(), 5, stream_keys(9, TAG_LS, 0, 6), 300)
     np.testing.assert_array_equal(got["best_assigns"], ref["best_assigns"])
+
+
+def _gpx_rows_oracle(oracle, pop, mrows, k, keys, off):
+    """Offspring rows [off, off + rows) with the whole-population oracle (first
+    parent = the row's own individual): other rows get parent 0 and are dropped."""
+    p, K = pop.shape[0], mrows.shape[1]
+    m = np.zeros((p, K), np.int64)
+    kk = np.zeros(p * K, np.uint64)
+    m[off:off + mrows.shape[0]] = mrows
+    kk[off * K:(off + mrows.shape[0]) * K] = keys
+    return oracle.gpx_batch(pop, m, k, kk)[off:off + mrows.shape[0]]
+
+
+def _gen_worker(rank, world, port):
+    """World-2 sharded generations (oracle as the compute) reproduce the
+    reference-chained generations of tests/golden/engine.npz bit for bit."""
+    from conftest import load_golden
+    from oracle import oracle
+    from oracle import population_oracle as PO
+    from paper_2109_05948_b200.population import min_spacing
+    from paper_2109_05948_b200.shard import col_generation_sharded
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        ENG = load_golden("engine")
+        ops = {"ls": lambda g_, a, k_, keys, d: oracle.tabucol_batch(g_, a, k_, keys, d),
+               "pair": lambda a, b, k_, lo, hi: oracle.pairwise(a, b, k_, lo, hi),
+               "gpx": lambda pop, mrows, k_, keys, off: _gpx_rows_oracle(oracle, pop, mrows, k_, keys, off),
+               "update": PO.update_population, "match": PO.match_parents}
+        for name in ENG["cases"]:
+            pre = str(name) + "__"
+            seed, n, pe, k, p, K, depth, G = (int(x) for x in ENG[pre + "params"])
+            g = rand_graph(seed, n, pe / 1000.0)
+            A = ENG[pre + "init"].astype(np.int32)
+            fit = (A[:, g.edges[:, 0]] == A[:, g.edges[:, 1]]).sum(axis=1).astype(np.int64)
+            pd = oracle.pairwise(A[:0], A, k)[1]
+            off = A.copy()
+            for t in range(G):
+                A, fit, pd, off, imp = col_generation_sharded(g, A, fit, pd, off, k, seed, t, depth, K,
+                                                              min_spacing(n), ops)
+                np.testing.assert_array_equal(imp, ENG[pre + f"g{t}_improved"])
+                np.testing.assert_array_equal(A, ENG[pre + f"g{t}_pop"])
+                np.testing.assert_array_equal(fit, ENG[pre + f"g{t}_fit"])
+                np.testing.assert_array_equal(pd, ENG[pre + f"g{t}_dist"])
+                np.testing.assert_array_equal(off, ENG[pre + f"g{t}_offspring"])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_generations_world2():
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    mp.spawn(_gen_worker, args=(2, _free_port()), nprocs=2, join=True)
