@@ -309,9 +309,9 @@ def run_ours(args):
     except OSError:
         pass
 
-    # ---- CPU baseline: the oracle on this host, rank 0, bounded sample
+    # ---- CPU baseline: the oracle on this host, rank 0 at N = 1 only, bounded sample
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:
         cores = os.cpu_count() or 1
         n_ind = max(64, 2 * cores)
         v, m_, dt = cpu_sample(args.workload, cores, n_ind, depth=args.ref_depth)
