@@ -30,13 +30,12 @@ __global__ void __launch_bounds__(GI_WARPS * 32)
                        int64_t p, int32_t *__restrict__ assigns, int32_t *__restrict__ used_out,
                        int32_t *err) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const size_t per = (((size_t)n * 2 + 15) & ~(size_t)15) + 32 * 4;
     int16_t *asg = reinterpret_cast<int16_t *>(smem + warp * per);
     uint32_t *blk = reinterpret_cast<uint32_t *>(smem + warp * per + per - 32 * 4);
-    const uint32_t lt_mask = (1u << lane) - 1u;
 
-    for (int64_t ind = (int64_t)blockIdx.x * GI_WARPS + warp; ind < p; ind += (int64_t)gridDim.x * GI_WARPS) {
+    for (int64_t ind = (int64_t)blockIdx.x * nw + warp; ind < p; ind += (int64_t)gridDim.x * nw) {
         const uint64_t key = keys[ind];
         for (int v = lane; v < n; v += 32) asg[v] = -1;
         int used = 0;
@@ -80,7 +79,6 @@ __global__ void __launch_bounds__(GI_WARPS * 32)
             }
             __syncwarp();
         }
-        (void)lt_mask;
         int32_t *out = assigns + (size_t)ind * n;
         for (int v = lane; v < n; v += 32) out[v] = asg[v];
         if (lane == 0) {
@@ -97,19 +95,21 @@ int greedy_init_run(const int32_t *order, const int64_t *indptr, const int32_t *
     if (p == 0) return MCB_OK;
     if (n > 32767) return set_error(MCB_ERR_UNSUPPORTED, "greedy_init: n <= 32767");
     const size_t per = (((size_t)n * 2 + 15) & ~(size_t)15) + 32 * 4;
-    const size_t smem = GI_WARPS * per;
+    int warps = GI_WARPS;  // as many as shared memory holds
+    while (warps > 1 && warps * per > (size_t)max_smem_optin()) warps >>= 1;
+    const size_t smem = warps * per;
     if (smem > (size_t)max_smem_optin()) return set_error(MCB_ERR_UNSUPPORTED, "greedy_init: n too large");
     if (cudaFuncSetAttribute(greedy_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return set_error(MCB_ERR_CUDA, "greedy_init: smem attribute failed");
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, greedy_init_kernel, GI_WARPS * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, greedy_init_kernel, warps * 32, smem);
     per_sm = std::max(per_sm, 1);
-    const int grid = (int)std::min<int64_t>((p + GI_WARPS - 1) / GI_WARPS, (int64_t)per_sm * num_sms());
+    const int grid = (int)std::min<int64_t>((p + warps - 1) / warps, (int64_t)per_sm * num_sms());
     int32_t *err = (int32_t *)workspace(256);
     if (!err) return set_error(MCB_ERR_CUDA, "greedy_init: workspace");
     cudaMemsetAsync(err, 0, 4, st);
-    greedy_init_kernel<<<grid, GI_WARPS * 32, smem, st>>>(order, indptr, indices, (int)n, keys, p, assigns,
+    greedy_init_kernel<<<grid, warps * 32, smem, st>>>(order, indptr, indices, (int)n, keys, p, assigns,
                                                           used, err);
     int32_t herr = 0;
     if (cudaGetLastError() != cudaSuccess ||

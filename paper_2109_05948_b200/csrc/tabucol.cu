@@ -1058,6 +1058,12 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
         return set_error(MCB_ERR_UNSUPPORTED, "tabucol: n<=32767 and k<=255 required");
     if (A.p == 0) return MCB_OK;
     const int n = (int)A.n, k = (int)A.k, kp = (k + 3) & ~3;
+    // every shape must be able to fall back to the wide CTA pass, whose
+    // per-vertex state (u32 expiries, scan records, lists) lives in shared
+    // memory: ~39 B per vertex -> n <= ~5900 on B200
+    if (smem_bytes<uint16_t, uint32_t, false>(n, kp) > (size_t)max_smem_optin())
+        return set_error(MCB_ERR_UNSUPPORTED, "tabucol: n=%d needs %zu B of per-vertex shared state (max %d B)", n,
+                         smem_bytes<uint16_t, uint32_t, false>(n, kp), max_smem_optin());
 
     TabuParams P{};
     P.assigns = A.assigns;
