@@ -52,3 +52,16 @@ def test_vertex_limits_raise():
     gm = _path_graph(32767)  # the largest greedy init: fewer warps per block
     a, used = greedy_wvcp_assigns(gm, stream_keys_init(1, 2))
     assert (a[:, :-1] != a[:, 1:]).all() and (used <= 3).all()
+
+
+def test_shared_state_limits_raise_cleanly():
+    """WVCP and distances whose per-individual / per-pair shared-memory state
+    cannot fit: a ValueError naming the limit, not a CUDA failure."""
+    g = _path_graph(40000, wmax=3)
+    A = np.zeros((1, 40000), np.int32)
+    A[0, 1::2] = 1
+    with pytest.raises(ValueError, match="shared memory"):
+        LS._run_wvcp_batch(g, A, 3, stream_keys(1, TAG_LS, 0, 1), 5, 1, True, 1.0)
+    P = random_col_assigns(60000, 200, 1, 2)
+    with pytest.raises(ValueError, match="shared memory"):
+        DI.pairwise_distances(P, P, k=200)
