@@ -65,3 +65,22 @@ def test_shared_state_limits_raise_cleanly():
     P = random_col_assigns(60000, 200, 1, 2)
     with pytest.raises(ValueError, match="shared memory"):
         DI.pairwise_distances(P, P, k=200)
+
+
+@pytest.mark.parametrize("n,pe,k", [(1000, 0.9, 222), (1000, 0.5, 234)], ids=["dsjc1000.9-like", "r1000.5-like"])
+def test_shapes_beyond_the_papers_runs(n, pe, k, oracle_lib):
+    """Shapes the paper skipped (n k > 200,000, `PAPER.md:346`) run here,
+    bit-exact vs the oracle: TabuCol on the CTA kernel (k > 128) and the
+    distances (k^2 u8 counters: one warp per block)."""
+    g = rand_graph(9, n, pe)
+    A = random_col_assigns(n, k, 3, 9)
+    keys = stream_keys(9, TAG_LS, 0, 3)
+    ref = oracle_lib.tabucol_batch(g, A.copy(), k, keys, 400)
+    got = LS._run_tabucol_batch(g, A.copy(), k, keys, 400)
+    for key in ("best_assigns", "best_conflicts", "iters_used"):
+        np.testing.assert_array_equal(got[key], ref[key])
+    P, Q = got["best_assigns"], random_col_assigns(n, k, 2, 10)
+    c, w = DI.pairwise_distances(P, Q, k=k)
+    rc, rw = oracle_lib.pairwise(P, Q, k)
+    np.testing.assert_array_equal(c, rc)
+    np.testing.assert_array_equal(w, rw)
