@@ -99,3 +99,29 @@ def test_wvcp_gamma_overflow_reruns_wide(case, oracle_lib, monkeypatch):
         np.testing.assert_array_equal(wide[key], ref[key], err_msg=key)
     for a, b in zip(got["log"], ref["log"]):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("t", range(10))
+def test_wvcp_dyadic_phi_vs_oracle(t, oracle_lib):
+    """Random shapes with dyadic phi schedules (phi0 = t 2^-s: every reachable
+    phi takes the exact 32-bit integer objective path of csrc/wvcp.cu);
+    bit-exact vs the oracle, move logs included."""
+    rs = np.random.default_rng(500 + t)
+    n = int(rs.integers(2, 600))
+    pe = float(rs.uniform(0.05, 0.9))
+    k = int(rs.integers(2, 80))
+    wmax = int(rs.choice([1, 7, 100]))
+    p = int(rs.integers(1, 14))
+    depth = int(rs.integers(1, max(2, 1_500_000 // max(1, n * p))))
+    rounds = int(rs.integers(1, 5))
+    sched = bool(rs.integers(0, 2))
+    phi0 = float(rs.integers(1, 40)) * 2.0 ** -int(rs.integers(0, 4))
+    g = rand_graph(700 + t, n, pe, wmax=wmax)
+    A = random_col_assigns(n, k, p, 800 + t)
+    keys = stream_keys(t, TAG_LS, 3, p)
+    ref = oracle_lib.wvcp_batch(g, A.copy(), k, keys, depth, rounds, sched, phi0, log_moves=True)
+    got = LS._run_wvcp_batch(g, A.copy(), k, keys, depth, rounds, sched, phi0, log_moves=True)
+    for key in ("end_assigns", "best_assigns", "best_scores", "end_scores", "end_conflicts", "phi_used"):
+        np.testing.assert_array_equal(got[key], ref[key], err_msg=f"{t} {key}")
+    for a, b in zip(got["log"], ref["log"]):
+        np.testing.assert_array_equal(a, b, err_msg=f"{t} log")
