@@ -16,7 +16,7 @@
 // of four warps idle in the serial phases.  Here every phase is warp-synchronous
 // (shuffles / ballots, no __syncthreads in the loop), all per-individual
 // scalars live in registers (uniform across lanes), and an SM runs as many
-// independent individuals as shared memory holds (7 at G(500,.5) k=48).
+// independent individuals as shared memory holds (8 at G(500,.5) k=48).
 //
 // Gamma byte per (vertex, colour), shared memory, rows of KP = 16 KV bytes:
 //     bit 7  OWN   the vertex's own colour (never a candidate)
@@ -33,14 +33,17 @@
 // register ring ordered by age -- register row 0 holds the newest 32 entries
 // (lane = insertion % 32), the rows shift down once per 32 insertions -- so
 // every access uses a static register index; each iteration checks the rows
-// that still hold live entries (2 in steady state, 1024 entries at most) and
-// clears the TABU bit of entries expiring now.  Re-tabu of a tabu pair
-// invalidates the older entry (last write wins, :366).
+// that still hold live entries (2 in steady state) and clears the TABU bit of
+// entries expiring now.  Re-tabu of a tabu pair invalidates the older entry
+// (last write wins, :366).  The registers hold 1024 entries; the SPILL
+// instantiation continues the ring, in age order, in a per-warp global buffer
+// (individuals that need it are re-run on it from their start).
 //
-// Per CTA: the adjacency as a bitset, row v = 32 lane chunks of CH bits (lane
-// L owns vertices [L*CH, L*CH+CH)), so the neighbour update of a move is one
-// chunk load per lane and neighbours come out in ascending order.  Graphs whose
-// bitset does not fit use the CSR (u16 indices, L2) variant.
+// Adjacency: a lane-interleaved bitset, row v = 32 chunks of CH bits, bit q of
+// chunk L <-> vertex L + 32 q (the rows lane L owns in the gamma table), read
+// from L2 as soon as the moving vertex is known; the neighbour update is one
+// chunk per lane, all CH slots unrolled.  A CSR (u16 indices) variant remains
+// for A/B (MCB_WARP_MODE=csr).
 #include <algorithm>
 #include <climits>
 #include <utility>
