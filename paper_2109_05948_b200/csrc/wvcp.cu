@@ -19,14 +19,17 @@
 //
 // Parallel evaluation of the sequential reservoir, as in tabucol.cu: pass 1
 // computes every row's (min g, #candidates at the min) -- one vertex per thread,
-// all n rows; warp 0 runs the exclusive prefix-min over the rows in vertex
-// order, counts tie events of rows equal to the running minimum and walks the
-// rows that lower it (warp-cooperative, lanes over colours), giving the
-// counter offset of the final minimum group; the draws are then independent.
+// all n rows, in exact 32/64-bit integers when phi = t 2^-s (gv_mode); the
+// prefix minimum over the rows in vertex order runs on all 8 warps (chunks of
+// 32 rows entered with the minimum of the chunks before), counting the tie
+// events of rows equal to the running minimum and walking the rows that lower
+// it (lanes over colours); warp 0 combines the partials, draws the final
+// group's T - 1 independent reservoir draws, locates the move and applies it.
 //
-// State per individual: gamma u16[n][k] and the per-vertex arrays in shared
-// memory; the per-class weight-rank counts wc[k][nranks] in a per-CTA global
-// slice (touched for two classes per move).
+// State per individual: gamma u8[n][k] (u16 in the re-run of individuals whose
+// counts reach 256) and the per-vertex arrays in shared memory -- 4 CTAs per SM
+// at config 3; the per-class weight-rank counts wc[k][nranks] in a per-CTA
+// global slice (touched for two classes per move).
 #include <algorithm>
 #include <cfloat>
 #include <climits>
