@@ -106,8 +106,29 @@ def col_generation(dg, st, *, seed, depth, K, ms=None, timings=None):
     return generation(dg, st, seed=seed, depth=depth, K=K, ms=ms, timings=timings)
 
 
+def _gather_rows(local, total, world, rank, group):
+    """Rows [lo_r, hi_r) of every rank -> the whole (total, ...) tensor on this
+    device (NCCL all-gather of equal-size padded blocks)."""
+    import torch.distributed as dist
+
+    from .shard import shard_range
+
+    if not dist.is_initialized():
+        return local.contiguous()
+    cap = -(-total // world)
+    pad = torch.zeros((cap,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    buf = torch.empty((world * cap,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(buf, pad, group=group)
+    parts = []
+    for r in range(world):
+        lo, hi = shard_range(total, world, r)
+        parts.append(buf[r * cap: r * cap + (hi - lo)])
+    return torch.cat(parts, 0).contiguous()
+
+
 def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, phi0=None, net=None,
-               epochs=1, batch_size=64):
+               epochs=1, batch_size=64, group=None, force_shard=False):
     """Advance `st` by one generation in place; returns the LS outputs.
 
     With a surrogate ``net`` (`surrogate.SurrogateNet`; the reference's
@@ -120,7 +141,25 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
     WVCP (`st.mode == "wvcp"`): `improve_population(..., WVCP, ...)`
     (`mc/localsearch.py:642-662`) -- phi0 = (k / 2n) max weight, schedule on,
     `max_rounds` rounds of `depth`; an individual that never reached a legal
-    colouring keeps its start with fitness INF_SCORE."""
+    colouring keeps its start with fitness INF_SCORE.
+
+    Multi-GPU (`group`, one process per GPU, NCCL): every rank
+    holds the whole population; the LS runs on this rank's individuals
+    [lo, hi) with their global stream keys, the improved colourings and
+    fitness are all-gathered, the distance job space is split and the partial
+    matrices SUM-all-reduced, the pool update / matching / surrogate training
+    run replicated (deterministic), GPX and selection run on this rank's rows
+    and the offspring are all-gathered -- the same results on every rank as
+    one process (`shard.col_generation_sharded` is the host-level twin, tested
+    at world size 2)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 or (force_shard and dist.is_initialized()) else 0
+    if world > 1 or force_shard:
+        return _generation_sharded(dg, st, seed=seed, depth=depth, K=K, ms=ms, max_rounds=max_rounds, phi0=phi0,
+                                   net=net, epochs=epochs, batch_size=batch_size, group=group, world=world,
+                                   rank=rank)
     p, n, k, t = st.p, st.n, st.k, st.generation
     dev = st.pop_assigns.device
     ms = min_spacing(n) if ms is None else ms
@@ -194,3 +233,85 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
         for (_, e0), (name, e1) in zip(marks[:-1], marks[1:]):
             timings[name] = timings.get(name, 0.0) + e0.elapsed_time(e1) / 1e3
     return ls
+
+
+def _generation_sharded(dg, st, *, seed, depth, K, ms, max_rounds, phi0, net, epochs, batch_size, group, world,
+                        rank):
+    import torch.distributed as dist
+
+    from .shard import shard_range
+
+    p, n, k, t = st.p, st.n, st.k, st.generation
+    dev = st.pop_assigns.device
+    ms = min_spacing(n) if ms is None else ms
+    lo, hi = shard_range(p, world, rank)
+    keys = Dv.keys_to_tensor(stream_keys(seed, TAG_LS, t, hi - lo, start=lo), dev)
+    start = st.offspring[lo:hi].clone()
+    if st.mode == "wvcp":
+        if phi0 is None:
+            phi0 = (k / (2.0 * n)) * dg.max_weight
+        ls = Dv.wvcp_batch(dg, start.clone(), k, keys, depth, max_rounds, True, phi0)
+        legal = ls["best_scores"] < INF_SCORE
+        imp_loc = torch.where(legal[:, None], ls["best_assigns"], start).contiguous()
+        fit_loc = torch.where(legal, ls["best_scores"], torch.full_like(ls["best_scores"], INF_SCORE))
+    else:
+        ls = Dv.tabucol_batch(dg, start.clone(), k, keys, depth)
+        imp_loc, fit_loc = ls["best_assigns"], ls["best_conflicts"]
+    # elites: the improved colourings (uint8 over NVLink) and their fitness
+    improved = _gather_rows(imp_loc.to(torch.uint8) if k <= 256 else imp_loc, p, world, rank, group).to(torch.int32)
+    imp_fit = _gather_rows(fit_loc.contiguous(), p, world, rank, group)
+    st.best_score = min(st.best_score, int(imp_fit.min().item()))
+    if net is not None:
+        from .rng import TAG_TRAIN, Stream
+
+        mask = imp_fit < INF_SCORE
+        if int(mask.sum().item()) >= 2:
+            net.train_generation(st.offspring[mask], imp_fit[mask].double().cpu().numpy(), k, epochs, batch_size,
+                                 Stream.derive(seed, TAG_TRAIN, t))
+    # distances: this rank's slice of the job space, partial matrices summed
+    total = p * p + p * (p - 1) // 2
+    jlo, jhi = shard_range(total, world, rank)
+    cross = torch.zeros((p, p), dtype=torch.int32, device=dev)
+    within = torch.zeros((p, p), dtype=torch.int32, device=dev)
+    Dv.pairwise(st.pop_assigns, improved, k, jlo, jhi, cross=cross, within=within)
+    if dist.is_initialized():
+        dist.all_reduce(cross, group=group)
+        dist.all_reduce(within, group=group)
+    # pool update and matching: replicated, identical on every rank
+    adm = torch.empty(p, dtype=torch.int32, device=dev)
+    rule = torch.empty(p, dtype=torch.uint8, device=dev)
+    new_dist = torch.empty((p, p), dtype=torch.int32, device=dev)
+    new_assigns = torch.empty((p, n), dtype=torch.int32, device=dev)
+    new_fit = torch.empty(p, dtype=torch.int64, device=dev)
+    P = N.ptr
+    N.check(N.lib().mcb_update_population(
+        P(st.pop_dist), P(cross), P(within), P(st.pop_fitness), P(imp_fit), p, p, int(ms),
+        P(st.pop_assigns), P(improved), n, P(adm), P(rule), P(new_dist), P(new_assigns), P(new_fit),
+        _stream()))
+    st.pop_assigns, st.pop_fitness, st.pop_dist = new_assigns, new_fit, new_dist
+    matches = torch.empty((p, K), dtype=torch.int64, device=dev)
+    N.check(N.lib().mcb_match_parents(P(st.pop_dist), p, int(K), n, P(matches), _stream()))
+    # GPX and selection on this rank's rows, then the offspring all-gathered
+    ck = Dv.keys_to_tensor(stream_keys(seed, TAG_CROSS, t, (hi - lo) * K, start=lo * K), dev)
+    cands = Dv.gpx_rows(st.pop_assigns, matches[lo:hi].contiguous(), lo, k, ck)
+    rows = hi - lo
+    if net is not None:
+        sel = net.predict_assigns_device(cands.reshape(rows * K, n), k).reshape(rows, K).argmin(dim=1)
+    else:
+        sk = Dv.keys_to_tensor(stream_keys(seed, TAG_SELECT, t, rows, start=lo), dev)
+        sv = torch.empty(rows, dtype=torch.int64, device=dev)
+        zeros = torch.zeros(rows, dtype=torch.int64, device=dev)
+        N.check(N.lib().mcb_stream_values(P(sk), P(zeros), P(sv), rows, _stream()))
+        hi32, lo32 = (sv >> 32) & 0xFFFFFFFF, sv & 0xFFFFFFFF
+        sel = ((hi32 % K) * ((1 << 32) % K) + lo32 % K) % K
+    off_loc = cands[torch.arange(rows, device=dev), sel].contiguous()
+    st.offspring = _gather_rows(off_loc.to(torch.uint8) if k <= 256 else off_loc, p, world, rank, group).to(torch.int32)
+    st.generation = t + 1
+    out = dict(ls)
+    out["best_assigns"] = improved
+    if st.mode == "wvcp":
+        out["best_scores"] = imp_fit
+    else:
+        out["best_conflicts"] = imp_fit
+    return out
+

@@ -144,3 +144,31 @@ def test_sharded_generation_composition_with_cuda_operators():
             np.testing.assert_array_equal(A, ENG[pre + f"g{t}_pop"], err_msg=f"{name} g{t}")
             np.testing.assert_array_equal(pd, ENG[pre + f"g{t}_dist"])
             np.testing.assert_array_equal(off, ENG[pre + f"g{t}_offspring"])
+
+
+def test_device_sharded_generation_nccl_world1():
+    """The device-resident sharded generation (`engine.generation(...,
+    force_shard=True)`: LS shard + NCCL all-gathers, job-range distances +
+    all-reduce, GPX rows) inside a one-rank NCCL group reproduces the
+    reference chain; at world size N the same code splits the ranges."""
+    import torch.distributed as dist
+
+    from test_shard import _free_port
+
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+    try:
+        for name in [str(c) for c in ENG["cases"]]:
+            pre = name + "__"
+            seed, n, pe, k, p, K, depth, G = (int(x) for x in ENG[pre + "params"])
+            g = rand_graph(seed, n, pe / 1000.0)
+            dg = Dv.DeviceGraph(g, "cuda")
+            st = E.init_state(dg, ENG[pre + "init"], k)
+            for t in range(G):
+                E.generation(dg, st, seed=seed, depth=depth, K=K, force_shard=True)
+                torch.cuda.synchronize()
+                np.testing.assert_array_equal(st.pop_assigns.cpu().numpy(), ENG[pre + f"g{t}_pop"], err_msg=f"g{t}")
+                np.testing.assert_array_equal(st.pop_dist.cpu().numpy(), ENG[pre + f"g{t}_dist"])
+                np.testing.assert_array_equal(st.offspring.cpu().numpy(), ENG[pre + f"g{t}_offspring"])
+    finally:
+        dist.destroy_process_group()

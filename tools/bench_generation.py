@@ -4,6 +4,7 @@ LS (TabuCol), pairwise distances (p x p cross + p(p-1)/2 within), pool update,
 parent matching, offspring (GPX p x K + selection).
 
     python tools/bench_generation.py [--p 16384] [--depth 2000] [--gens 2]
+    torchrun --nproc-per-node N tools/bench_generation.py ...   (sharded over N GPUs, NCCL)
 
 The LS stage scales linearly with depth (config 2 asks 100,000 iterations);
 the other stages do not depend on it.
@@ -33,6 +34,13 @@ ap.add_argument("--surrogate", action="store_true", help="surrogate-guided selec
 ap.add_argument("--tf32", action="store_true", help="surrogate GEMMs on TF32 tensor cores (opt-in)")
 ap.add_argument("--epochs", type=int, default=1)
 a = ap.parse_args()
+world = int(os.environ.get("WORLD_SIZE", "1"))
+rank = int(os.environ.get("RANK", "0"))
+if world > 1:
+    import torch.distributed as dist
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    dist.init_process_group("nccl")
 t0 = time.time()
 g = rand_graph(1, a.n, 0.5)
 dg = Dv.DeviceGraph(g, "cuda")
@@ -52,9 +60,11 @@ for t in range(a.gens):
     e1.record()
     torch.cuda.synchronize()
     moves = int(ls["iters_used"].sum().item())
-    print(json.dumps({"generation": t, "total_s": e0.elapsed_time(e1) / 1e3,
+    if rank:
+        continue
+    print(json.dumps({"generation": t, "total_s": e0.elapsed_time(e1) / 1e3, "gpus": world,
                       "stages_s": {k_: round(v, 4) for k_, v in tim.items()},
-                      "ls_moves": moves, "ls_moves_per_s": moves / tim["ls"],
+                      "ls_moves": moves, "ls_moves_per_s": moves / tim["ls"] if "ls" in tim else None,
                       "best": st.best_score, "pop_fitness_mean": float(st.pop_fitness.float().mean()),
                       "config": f"G({a.n},.5) k={a.k} p={a.p} K={a.K} LS depth {a.depth}"
                                 + (f", surrogate small{' tf32' if a.tf32 else ''} {a.epochs} epoch(s)" if net else "")}),
