@@ -347,6 +347,7 @@ def run_ours(args):
                      "kernel": kernel_desc,
                      "peak_source": "measured: mcb_probe_smem_bandwidth (LDS.128 stream, all SMs)",
                      "alg_bytes_per_launch": alg_bytes_total / args.steps,
+                     "latency_bound": ncu_latency_evidence(),
                      "kernel_ms_per_launch": 1e3 * kern_s / args.steps,
                      "hbm_peak_gbs": peaks.get("hbm_gbs")},
         "cpu_baseline": cpu,
@@ -361,6 +362,25 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def ncu_latency_evidence():
+    """Issue-slot use and warp availability of the TabuCol kernel from the same
+    committed `ncu --set full` capture: the kernel is latency-bound, which is
+    why roofline.frac is low (profiles/r01d_summary.md)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01c_tabucol_warp_ncu_raw.csv")
+    try:
+        import csv
+
+        rows = list(csv.reader(open(path)))
+        h, v = rows[0], rows[2]
+        g = lambda m: round(float(v[h.index(m)]), 3)  # noqa: E731
+        return {"issue_slots_busy_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "warps_active_per_sm": g("sm__warps_active.avg.per_cycle_active"),
+                "warps_eligible_per_scheduler": g("smsp__warps_eligible.avg.per_cycle_active"),
+                "source": "profiles/r01c_tabucol_warp_ncu_raw.csv"}
+    except (OSError, ValueError, KeyError, IndexError):
+        return None
 
 
 def ncu_traffic(individuals):
