@@ -364,11 +364,20 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _ncu_capture():
+    """The newest committed `ncu --set full` capture of the TabuCol kernel."""
+    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    for name in ("r01d_tabucol_warp_ncu_raw.csv", "r01c_tabucol_warp_ncu_raw.csv"):
+        if os.path.exists(os.path.join(prof, name)):
+            return os.path.join(prof, name)
+    return os.path.join(prof, "missing.csv")
+
+
 def ncu_latency_evidence():
     """Issue-slot use and warp availability of the TabuCol kernel from the same
     committed `ncu --set full` capture: the kernel is latency-bound, which is
     why roofline.frac is low (profiles/r01d_summary.md)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01c_tabucol_warp_ncu_raw.csv")
+    path = _ncu_capture()
     try:
         import csv
 
@@ -378,7 +387,7 @@ def ncu_latency_evidence():
         return {"issue_slots_busy_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                 "warps_active_per_sm": g("sm__warps_active.avg.per_cycle_active"),
                 "warps_eligible_per_scheduler": g("smsp__warps_eligible.avg.per_cycle_active"),
-                "source": "profiles/r01c_tabucol_warp_ncu_raw.csv"}
+                "source": "profiles/" + os.path.basename(path)}
     except (OSError, ValueError, KeyError, IndexError):
         return None
 
@@ -388,7 +397,7 @@ def ncu_traffic(individuals):
     committed `ncu --set full` capture (profiles/r01c_tabucol_warp_ncu_raw.csv:
     one wave of 1184 individuals x 50k iterations, same kernel variant), scaled
     to this launch's individuals; (None, reason) when the capture is absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01c_tabucol_warp_ncu_raw.csv")
+    path = _ncu_capture()
     try:
         import csv
 
@@ -396,8 +405,8 @@ def ncu_traffic(individuals):
         h, u, v = rows[0], rows[1], rows[2]
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         tot = sum(float(v[h.index(m)]) * scale[u[h.index(m)]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        return tot * individuals / 1184.0, ("ncu --set full of the same kernel variant (profiles/r01c_tabucol_warp_ncu_raw"
-                                            ".csv, D=1184), dram read+write scaled per individual; the state stays on chip")
+        return tot * individuals / 1184.0, ("ncu --set full of the same kernel variant (profiles/" + os.path.basename(path)
+                                            + ", D=1184), dram read+write scaled per individual; the state stays on chip")
     except (OSError, ValueError, KeyError, IndexError):
         return None, "no ncu capture in profiles/"
 
