@@ -1013,16 +1013,41 @@ static size_t smem_bytes(int n, int kp) {
     return s;
 }
 
+// threads per individual: 256 when every individual is resident at 256
+// threads (pass 1's conflicting rows spread over twice the lanes; config 4 at
+// its 256 individuals per GPU: 3.6e6 -> 5.8e6 moves/s), else 128 so that more
+// individuals are resident.  MCB_TC_NT=128|256 overrides.
+static int pick_nt(int slots256, int p_hint) {
+    if (const char *e = getenv("MCB_TC_NT")) {
+        const int v = atoi(e);
+        if (v == 128 || v == 256) return v;
+    }
+    return p_hint <= slots256 ? 256 : TC_NT;
+}
+
+template <typename G, typename S, bool GSM, int NT>
+static auto kernel_for(int kp) {
+    return (GSM && kp <= 64) ? tabucol_kernel<G, S, GSM, 1, NT> : tabucol_kernel<G, S, GSM, 4, NT>;
+}
+
 template <typename G, typename S, bool GSM>
 static int launch_variant(TabuParams P, int max_grid, int p_hint, cudaStream_t st, int *grid_out,
                           bool query_only) {
     const size_t smem = smem_bytes<G, S, GSM>(P.n, P.kp);
-    auto kern = (GSM && P.kp <= 64) ? tabucol_kernel<G, S, GSM, 1, TC_NT> : tabucol_kernel<G, S, GSM, 4, TC_NT>;
+    int nt = TC_NT;
+    if (sizeof(S) == 2) {  // narrow pass (the wide re-run keeps 128)
+        auto k256 = kernel_for<G, S, GSM, 256>(P.kp);
+        int nb256 = 0;
+        if (cudaFuncSetAttribute(k256, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb256, k256, 256, smem) == cudaSuccess && nb256 > 0)
+            nt = pick_nt(nb256 * num_sms(), p_hint);
+    }
+    auto kern = nt == 256 ? kernel_for<G, S, GSM, 256>(P.kp) : kernel_for<G, S, GSM, TC_NT>(P.kp);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return set_error(MCB_ERR_CUDA, "cudaFuncSetAttribute(smem=%zu) failed", smem);
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TC_NT, smem) != cudaSuccess || nb < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, nt, smem) != cudaSuccess || nb < 1)
         return set_error(MCB_ERR_CUDA, "tabucol: no occupancy for smem=%zu", smem);
     int grid = std::min(p_hint, nb * num_sms());
     if (max_grid > 0) grid = std::min(grid, max_grid);
@@ -1030,10 +1055,10 @@ static int launch_variant(TabuParams P, int max_grid, int p_hint, cudaStream_t s
     *grid_out = grid;
     if (query_only) return MCB_OK;
     if (getenv("MCB_VERBOSE"))
-        fprintf(stderr, "[mcb] tabucol<%s,%s,gsm=%d,kq=%d> grid=%d (%d/SM) smem=%zu\n",
+        fprintf(stderr, "[mcb] tabucol<%s,%s,gsm=%d,kq=%d,nt=%d> grid=%d (%d/SM) smem=%zu\n",
                 sizeof(G) == 1 ? "u8" : "u16", sizeof(S) == 2 ? "u16" : "u32", (int)GSM,
-                (GSM && P.kp <= 64) ? 1 : 4, grid, nb, smem);
-    kern<<<grid, TC_NT, smem, st>>>(P);
+                (GSM && P.kp <= 64) ? 1 : 4, nt, grid, nb, smem);
+    kern<<<grid, nt, smem, st>>>(P);
     if (cudaGetLastError() != cudaSuccess) return set_error(MCB_ERR_CUDA, "tabucol launch failed");
     return MCB_OK;
 }
