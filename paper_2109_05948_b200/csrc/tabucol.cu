@@ -1013,10 +1013,11 @@ static size_t smem_bytes(int n, int kp) {
     return s;
 }
 
-// threads per individual: 256 when every individual is resident at 256
-// threads (pass 1's conflicting rows spread over twice the lanes; config 4 at
-// its 256 individuals per GPU: 3.6e6 -> 5.8e6 moves/s), else 128 so that more
-// individuals are resident.  MCB_TC_NT=128|256 overrides.
+// threads per individual (gamma-in-L2 shapes): 256 when every individual is
+// resident at 256 threads (pass 1's conflicting rows, read from L2, spread
+// over twice the lanes; config 4 at its 256 individuals per GPU: 3.6e6 -> 5.7e6
+// moves/s), else 128 so that more individuals are resident.  With gamma in
+// shared memory 128 measured slightly better (C3 shape).  MCB_TC_NT overrides.
 static int pick_nt(int slots256, int p_hint) {
     if (const char *e = getenv("MCB_TC_NT")) {
         const int v = atoi(e);
@@ -1035,7 +1036,7 @@ static int launch_variant(TabuParams P, int max_grid, int p_hint, cudaStream_t s
                           bool query_only) {
     const size_t smem = smem_bytes<G, S, GSM>(P.n, P.kp);
     int nt = TC_NT;
-    if (sizeof(S) == 2) {  // narrow pass (the wide re-run keeps 128)
+    if (sizeof(S) == 2 && !GSM) {  // narrow pass, gamma in L2 (the L2 latency is what more lanes hide)
         auto k256 = kernel_for<G, S, GSM, 256>(P.kp);
         int nb256 = 0;
         if (cudaFuncSetAttribute(k256, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
