@@ -292,7 +292,9 @@ struct RowEval {
         } else if constexpr (NARROW) {
             const int W = kp >> 2;
             int m = 0xFF, c = 0;
-#pragma unroll 4
+            // 16 words in flight: with gamma in L2 a row is a few round trips,
+            // not one per 4 words
+#pragma unroll 16
             for (int w = 0; w < W; w++) {
                 const uint32_t x = word(w);
                 const int wm = (int)min_bytes(x);
