@@ -1038,14 +1038,17 @@ static int launch_variant(TabuParams P, int max_grid, int p_hint, cudaStream_t s
                           bool query_only) {
     const size_t smem = smem_bytes<G, S, GSM>(P.n, P.kp);
     int nt = TC_NT;
-    if (sizeof(S) == 2 && !GSM) {  // narrow pass, gamma in L2 (the L2 latency is what more lanes hide)
+    auto kern = kernel_for<G, S, GSM, TC_NT>(P.kp);
+    if constexpr (sizeof(S) == 2 && !GSM) {  // narrow pass, gamma in L2 (the L2 latency is what more lanes hide)
         auto k256 = kernel_for<G, S, GSM, 256>(P.kp);
         int nb256 = 0;
         if (cudaFuncSetAttribute(k256, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb256, k256, 256, smem) == cudaSuccess && nb256 > 0)
-            nt = pick_nt(nb256 * num_sms(), p_hint);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb256, k256, 256, smem) == cudaSuccess && nb256 > 0 &&
+            pick_nt(nb256 * num_sms(), p_hint) == 256) {
+            nt = 256;
+            kern = k256;
+        }
     }
-    auto kern = nt == 256 ? kernel_for<G, S, GSM, 256>(P.kp) : kernel_for<G, S, GSM, TC_NT>(P.kp);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return set_error(MCB_ERR_CUDA, "cudaFuncSetAttribute(smem=%zu) failed", smem);
