@@ -36,7 +36,7 @@ constexpr int PD_WARPS = 4;
 // per-level row -> column and column -> row bitmasks, the explicit list of
 // entries >= 32 and the level counters.
 struct PdLayout {
-    size_t hist_words, list_words, big, cmask, per;
+    size_t hist_words, list_words, big, cmask, uni, per;
 };
 
 __host__ __device__ inline PdLayout pd_layout(int n, int k, bool wide) {
@@ -46,8 +46,11 @@ __host__ __device__ inline PdLayout pd_layout(int n, int k, bool wide) {
     L.list_words = ((size_t)n + 1) / 2;        // u16 (r << 8 | c) per cell
     L.big = (size_t)n / 32 + 2;
     L.cmask = (size_t)k * ((k + 31) / 32);
-    // hist + list + bucket + big + cmask + rmask + lvbeg[32] + lvcur[32] + rowused/colused[16] + bigcnt
-    L.per = (L.hist_words + 2 * L.list_words + L.big + 2 * L.cmask + 32 + 32 + 16 + 4) * 4;
+    // the first-touch list is dead once the cells are bucketed; the level
+    // masks are live only after that: one region for both
+    L.uni = L.list_words > 2 * L.cmask ? L.list_words : 2 * L.cmask;
+    // hist + (list | cmask + rmask) + bucket + big + lvbeg[32] + lvcur[32] + rowused/colused[16] + bigcnt
+    L.per = (L.hist_words + L.uni + L.list_words + L.big + 32 + 32 + 16 + 4) * 4;
     L.per = (L.per + 15) & ~(size_t)15;
     return L;
 }
@@ -92,19 +95,18 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const PdLayout L = pd_layout(n, k, WIDE);
     uint32_t *hist = reinterpret_cast<uint32_t *>(smem + warp * L.per);
-    uint16_t *list = reinterpret_cast<uint16_t *>(hist + L.hist_words);
-    uint16_t *bucket = list + 2 * L.list_words;
+    uint16_t *list = reinterpret_cast<uint16_t *>(hist + L.hist_words);  // shares with cmask / rmask
+    uint32_t *cmask = hist + L.hist_words;  // [k][KWD]: row r -> columns holding the level
+    uint32_t *rmask = cmask + L.cmask;      // [k][KWD]: column c -> rows holding the level
+    uint16_t *bucket = reinterpret_cast<uint16_t *>(hist + L.hist_words + L.uni);
     uint32_t *big = reinterpret_cast<uint32_t *>(bucket + 2 * L.list_words);
-    uint32_t *cmask = big + L.big;   // [k][KWD]: row r -> columns holding the level
-    uint32_t *rmask = cmask + L.cmask;  // [k][KWD]: column c -> rows holding the level
-    uint32_t *lvbeg = rmask + L.cmask;
+    uint32_t *lvbeg = big + L.big;
     uint32_t *lvcur = lvbeg + 32;
     uint32_t *s_used = lvcur + 32;   // rowused[8], colused[8] (entries >= 32 only)
     uint32_t *bigcnt = s_used + 16;
     const uint32_t lt_mask = (1u << lane) - 1u;
 
     for (size_t i = lane; i < L.hist_words; i += 32) hist[i] = 0u;
-    for (size_t i = lane; i < 2 * L.cmask; i += 32) cmask[i] = 0u;
     __syncwarp();
 
     const int64_t pq = p * q;
@@ -205,6 +207,10 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
             const uint32_t val = hist_get<WIDE>(hist, (int)(e >> 8) * k + (int)(e & 0xFFu));
             if (val < 32) bucket[atomicAdd(&lvcur[val], 1u)] = (uint16_t)e;
         }
+        // the list is dead: its region becomes the (zeroed) level masks
+        __syncwarp();
+        for (size_t i = lane; i < 2 * L.cmask; i += 32) cmask[i] = 0u;
+        __syncwarp();
         uint32_t rowused[KWD], colused[KWD];
 #pragma unroll
         for (int w = 0; w < KWD; w++) rowused[w] = colused[w] = 0u;
@@ -329,10 +335,16 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
                 within[oj * q + oi] = d;
             }
         }
-        // reset the warp's histogram for the next pair: only its nonzero cells
-        for (int i = lane; i < m; i += 32) {
-            const uint32_t e = list[i];
+        // reset the warp's histogram for the next pair: only its nonzero cells,
+        // i.e. the level buckets and the entries >= 32
+        const int nbk = (int)lvcur[31], nbig = (int)*bigcnt;
+        for (int i = lane; i < nbk; i += 32) {
+            const uint32_t e = bucket[i];
             const int flat = (int)(e >> 8) * k + (int)(e & 0xFFu);
+            hist[WIDE ? flat >> 1 : flat >> 2] = 0u;
+        }
+        for (int i = lane; i < nbig; i += 32) {
+            const int flat = 0xFFFF - (int)(big[i] & 0xFFFFu);
             hist[WIDE ? flat >> 1 : flat >> 2] = 0u;
         }
         __syncwarp();
