@@ -62,12 +62,18 @@ int mcb_device_count(void);
  * (GB/s), measured with a conflict-free LDS.128 stream; the roofline
  * denominator of the shared-memory-bound kernels. */
 int mcb_probe_smem_bandwidth(double *gbs, double *ms);
+/* L2 read bandwidth (16-byte loads, L1 bypassed, 48 MB resident buffer): the
+ * roofline denominator of the out-of-shared-memory TabuCol shapes. */
+int mcb_probe_l2_bandwidth(double *gbs, double *ms);
 /* Diagnostics: per-phase cycle totals of the TabuCol iteration accumulated
  * by runs with MCB_FLAG_PROFILE (out: 16 counters; [10] = iterations). */
 int mcb_debug_phase_cycles(unsigned long long *out, int reset);
 /* Diagnostics: counters of the last warp-kernel TabuCol launch made with
  * MCB_FLAG_WSTATS (out: 40 counters, see tabucol_warp.cu WS_*). */
 int mcb_debug_warp_stats(unsigned long long *out);
+/* Group-of-warps TabuCol kernel run with MCB_GSTATS=1 in the environment:
+ * thread 0's cycles per phase (out: 32 counters; [15] = iterations). */
+int mcb_debug_group_stats(unsigned long long *out);
 /* WVCP kernel under MCB_FLAG_WSTATS: out[0] iterations, out[1..8] thread 0's
  * cycles per phase (pass 1, chunk minima, prefix + walks, warp-0 section,
  * gamma update, class refresh, best copy, tail); reset != 0 clears them. */

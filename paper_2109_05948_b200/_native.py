@@ -27,7 +27,7 @@ EXPORTS = [
     "mcb_version", "mcb_last_error", "mcb_device_count", "mcb_stream_values",
     "mcb_tabucol_batch", "mcb_tabucol_batch_host", "mcb_wvcp_batch", "mcb_wvcp_batch_host",
     "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_gpx_rows", "mcb_pairwise", "mcb_pairwise_host",
-    "mcb_probe_smem_bandwidth", "mcb_debug_phase_cycles", "mcb_debug_warp_stats", "mcb_debug_wvcp_stats",
+    "mcb_probe_smem_bandwidth", "mcb_probe_l2_bandwidth", "mcb_debug_phase_cycles", "mcb_debug_warp_stats", "mcb_debug_group_stats", "mcb_debug_wvcp_stats",
     "mcb_debug_modcheck", "mcb_tabucol_describe",
     "mcb_update_population", "mcb_update_population_host", "mcb_match_parents", "mcb_match_parents_host",
     "mcb_greedy_wvcp_init", "mcb_greedy_wvcp_init_host", "mcb_segsum", "mcb_segsum_async",
@@ -62,8 +62,10 @@ def _declare(L):
     L.mcb_pairwise.argtypes = pw
     L.mcb_pairwise_host.argtypes = pw
     L.mcb_probe_smem_bandwidth.argtypes = [P, P]
+    L.mcb_probe_l2_bandwidth.argtypes = [P, P]
     L.mcb_debug_phase_cycles.argtypes = [P, C.c_int]
     L.mcb_debug_warp_stats.argtypes = [P]
+    L.mcb_debug_group_stats.argtypes = [P]
     L.mcb_debug_wvcp_stats.argtypes = [P, C.c_int]
     L.mcb_debug_modcheck.argtypes = [I64, P]
     L.mcb_tabucol_describe.argtypes = [I64, I64, I64, C.c_char_p, C.c_int]

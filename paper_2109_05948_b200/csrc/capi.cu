@@ -63,6 +63,15 @@ void *workspace3(size_t bytes) {
     return grow_buffer(&buf[d], &cap[d], bytes);
 }
 
+// fourth: the group TabuCol kernel's adjacency bitset (alive while the
+// warp/CTA fallbacks of the same call use workspace / workspace2)
+void *workspace4(size_t bytes) {
+    static void *buf[64] = {nullptr};
+    static size_t cap[64] = {0};
+    const int d = cur_dev();
+    return grow_buffer(&buf[d], &cap[d], bytes);
+}
+
 // second independent scratch (kernels that need their own tables while the
 // first holds control words of the same call)
 void *workspace2(size_t bytes) {

@@ -15,6 +15,7 @@ int max_smem_optin();
 void *workspace(size_t bytes);
 void *workspace2(size_t bytes);
 void *workspace3(size_t bytes);
+void *workspace4(size_t bytes);
 
 struct TabucolArgs {
     int32_t *assigns;
@@ -38,6 +39,11 @@ int tabucol_run(const TabucolArgs &a, cudaStream_t st);
 int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *work_counter, int32_t *ovf_list,
                         int32_t *ovf_count, int32_t *err_flag, const int32_t *work_list = nullptr,
                         int64_t nwork = -1, bool spill = false);
+// group-of-warps kernel (tabucol_group.cu); -1 = shape outside its envelope
+int tabucol_group_launch(const TabucolArgs &A, cudaStream_t st, int32_t *work_counter, int32_t *ovf_list,
+                         int32_t *ovf_count, int32_t *err_flag);
+int tabucol_group_describe(int64_t n, int64_t k, int64_t p, char *buf, int len);
+int tabucol_group_stats(unsigned long long *out);
 int tabucol_phase_cycles(unsigned long long *out, int reset);
 int tabucol_warp_stats(unsigned long long *out);
 

@@ -49,7 +49,48 @@ int smem_probe(double *gbs, double *ms) {
     return MCB_OK;
 }
 
+// L2 read bandwidth: every thread streams 16-byte loads (L1 bypassed) over a
+// buffer that fits in L2, several passes after one warm-up pass
+__global__ void __launch_bounds__(512) l2_probe_kernel(const uint4 *buf, size_t n16, int passes, uint32_t *sink) {
+    uint32_t acc = 0;
+    const size_t st = (size_t)gridDim.x * blockDim.x;
+    for (int p = 0; p < passes; p++)
+        for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += st) {
+            uint4 v;
+            asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(buf + i));
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
+int l2_probe(double *gbs, double *ms) {
+    const size_t bytes = (size_t)48 << 20;  // well inside the 126 MB L2
+    uint8_t *buf = (uint8_t *)workspace2(bytes + 256);
+    if (!buf) return set_error(MCB_ERR_CUDA, "l2 probe: allocation failed");
+    cudaMemset(buf, 1, bytes + 256);
+    uint32_t *sink = reinterpret_cast<uint32_t *>(buf + bytes);
+    const int grid = 4 * num_sms(), passes = 16;
+    const uint4 *b4 = reinterpret_cast<const uint4 *>(buf);
+    l2_probe_kernel<<<grid, 512>>>(b4, bytes / 16, 1, sink);  // warm-up: the buffer into L2
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    l2_probe_kernel<<<grid, 512>>>(b4, bytes / 16, passes, sink);
+    cudaEventRecord(e1);
+    if (cudaEventSynchronize(e1) != cudaSuccess) return set_error(MCB_ERR_CUDA, "l2 probe failed");
+    float t = 0;
+    cudaEventElapsedTime(&t, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms = t;
+    *gbs = (double)bytes * passes / (t * 1e-3) / 1e9;
+    return MCB_OK;
+}
+
 }  // namespace mcb
+
+extern "C" int mcb_probe_l2_bandwidth(double *gbs, double *ms) { return mcb::l2_probe(gbs, ms); }
 
 extern "C" int mcb_probe_smem_bandwidth(double *gbs, double *ms) { return mcb::smem_probe(gbs, ms); }
 
@@ -58,6 +99,7 @@ extern "C" int mcb_debug_phase_cycles(unsigned long long *out, int reset) {
 }
 
 extern "C" int mcb_debug_warp_stats(unsigned long long *out) { return mcb::tabucol_warp_stats(out); }
+extern "C" int mcb_debug_group_stats(unsigned long long *out) { return mcb::tabucol_group_stats(out); }
 extern "C" int mcb_debug_wvcp_stats(unsigned long long *out, int reset) { return mcb::wvcp_stats(out, reset); }
 
 // Diagnostics: mod_is_zero (common.cuh) against the 64-bit % on `count`
@@ -96,5 +138,6 @@ namespace mcb {
 int tabucol_warp_describe(int64_t n, int64_t k, int64_t p, char *buf, int len);
 }
 extern "C" int mcb_tabucol_describe(int64_t n, int64_t k, int64_t p, char *buf, int len) {
+    if (mcb::tabucol_group_describe(n, k, p, buf, len) == 0) return 0;
     return mcb::tabucol_warp_describe(n, k, p, buf, len);
 }

@@ -1181,7 +1181,9 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     int32_t *ovf_warp = ctl32 + 64 + 256, *ovf_spill = ovf_warp + A.p;
     int32_t *ovf_final = ovf_warp, *ovf_final_count = ctl32 + 2;
     if (variant == 0) {
-        rc = tabucol_warp_launch(A, st, ctl32 + 0, ovf_warp, ctl32 + 2, ctl32 + 3);
+        // group of warps per individual first (tabucol_group.cu), else one warp
+        rc = tabucol_group_launch(A, st, ctl32 + 0, ovf_warp, ctl32 + 2, ctl32 + 3);
+        if (rc < 0) rc = tabucol_warp_launch(A, st, ctl32 + 0, ovf_warp, ctl32 + 2, ctl32 + 3);
         if (rc > 0) return rc;
         warp_done = rc == MCB_OK;
     }

@@ -125,3 +125,22 @@ def test_describe_reports_the_warp_kernel():
     buf = ctypes.create_string_buffer(256)
     N.check(N.lib().mcb_tabucol_describe(500, 48, 8192, buf, 256))
     assert b"tabucol_warp_kernel<KV=3,bitset CH=16>" in buf.value
+
+
+@pytest.mark.parametrize("nw", ["1", "2", "4"])
+@pytest.mark.parametrize("shape", SHAPES + FALLBACK,
+                         ids=[f"n{s[1]}k{s[3]}p{s[2]}" for s in SHAPES + FALLBACK])
+def test_group_kernel_vs_oracle(shape, nw, monkeypatch, oracle_lib):
+    """The opt-in group-of-warps kernel (csrc/tabucol_group.cu, MCB_GROUP_NW):
+    row summaries + NW warps per individual, bit-exact including move logs and
+    its hand-off of overflowing individuals to the warp SPILL / CTA kernels."""
+    seed, n, pe, k, pop, depth = shape
+    g = rand_graph(seed, n, pe)
+    A = random_col_assigns(n, k, pop, seed)
+    keys = stream_keys(seed, TAG_LS, 0, pop)
+    ref = oracle_lib.tabucol_batch(g, A.copy(), k, keys, depth, log_moves=True, counters=True)
+    monkeypatch.setenv("MCB_GROUP_NW", nw)
+    buf = ctypes.create_string_buffer(256)
+    N.check(N.lib().mcb_tabucol_describe(n, k, pop, buf, 256))
+    assert b"tabucol_group_kernel" in buf.value
+    _check(_run(g, A, k, keys, depth, monkeypatch, "auto"), ref, f"{shape}/group{nw}")

@@ -84,6 +84,14 @@ for spec in variants:
                                                            "cy_draw", "cy_locrows", "ncl", "ncl_gt32", "ncl_gt144"]
         it_ = max(buf[0], 1)
         print(json.dumps({nm: round(buf[i] / it_, 3) for i, nm in enumerate(names) if nm}), flush=True)
+    if os.environ.get("MCB_GSTATS"):
+        import ctypes
+        buf = (ctypes.c_ulonglong * 32)()
+        N.lib().mcb_debug_group_stats(ctypes.addressof(buf))
+        it_ = max(buf[15], 1)
+        names = ["scan", "wscan+B1", "events", "cx+B2", "draws", "locate", "B4", "move", "update", "B5+list",
+                 "expiry", "B6", "tail"]
+        print(json.dumps({"gstats_" + nm: round(buf[i] / it_, 1) for i, nm in enumerate(names)}), flush=True)
     print(json.dumps({"variant": name, "moves_per_s": best, "ms": ms, "moves": moves,
                       "mean_C": float(c[0] / max(moves, 1)), "mean_deg": float(c[1] / max(moves, 1)),
                       "same_as_first": same}), flush=True)
