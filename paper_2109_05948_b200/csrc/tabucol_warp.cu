@@ -55,6 +55,10 @@
 #include "launch.h"
 #include "tw_helpers.cuh"
 
+#ifndef TW_DIVREG
+#define TW_DIVREG 1  // first-round reservoir divisor entries in registers
+#endif
+
 namespace mcb {
 
 using namespace tw;
@@ -198,6 +202,11 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
     if (stats)
         for (int i = 0; i < WS_N; i++) st[i] = 0;
     const int g_lane = S::g(lane);  // rotation of every row this lane owns (u = lane + 32q)
+    // this lane's first-round reservoir divisor s = 2 + lane (< 64): its table
+    // entry in registers, off the draw chain (the table sits in L2 otherwise)
+    const int dv_t = __ffs(2 + lane) - 1;
+    const ulonglong2 dv_e = g_divtab[((2 + lane) >> dv_t) >> 1];
+    constexpr int s_first = TW_DIVREG ? 34 : 2;
 
     for (;;) {
         int wi = 0;
@@ -610,7 +619,12 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             const unsigned long long c0 = ctr + (unsigned long long)(tot - (T - 1));
                             int smax = 1;
                             WST(WS_DRAW_ROUNDS, (T + 30) / 32);
-                            for (int s = 2 + lane; s <= T; s += 32)
+                            if (TW_DIVREG && 2 + lane <= T) {
+                                const uint64_t x = stream_value(key, c0 + (unsigned long long)lane);
+                                if ((x & ((1ull << dv_t) - 1ull)) == 0ull && (x >> dv_t) * dv_e.x <= dv_e.y)
+                                    smax = 2 + lane;
+                            }
+                            for (int s = s_first + lane; s <= T; s += 32)
                                 if (divisible(stream_value(key, c0 + (unsigned long long)(s - 2)), (uint32_t)s))
                                     smax = s;
                             sstar = __reduce_max_sync(FULLM, smax);

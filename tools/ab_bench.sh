@@ -1,10 +1,11 @@
-# A/B throughput check of two builds of the library on one GPU box:
-#   cp <lib A> ab/libA.so; cp <lib B> ab/libB.so; gpurun -- 'bash tools/ab_bench.sh'
-set -e
-for i in 1 2 3; do
- for v in A B; do
-  cp ab/lib$v.so paper_2109_05948_b200/libmemcolor_b200.so
-  touch paper_2109_05948_b200/libmemcolor_b200.so
-  echo "$v $(timeout 300 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e 2>/dev/null | python -c 'import json,sys; print(json.loads(sys.stdin.read())["value"])')"
+# A/B throughput of library builds on one GPU box, each loaded through
+# MCB_LIB (the in-tree library is never touched):
+#   python tools/build_variants.py a=-DX=0 b=-DX=1
+#   gpurun -- 'bash tools/ab_bench.sh ab/lib_a.so ab/lib_b.so'
+# extra warp_probe arguments via PROBE_ARGS (default: one wave at depth 50k)
+ARGS=${PROBE_ARGS:---pop 1184 --depth 50000 --reps 3}
+for i in 1 2; do
+ for lib in "$@"; do
+  echo "$lib $(MCB_LIB=$lib timeout 300 python tools/warp_probe.py $ARGS 2>/dev/null | tail -1)"
  done
 done

@@ -1,6 +1,8 @@
-"""Build A/B variants of the warp TabuCol kernel: each variant is the whole
-library compiled with extra -D flags into ab/lib_<name>.so (load one with
-MCB_LIB=ab/lib_<name>.so).
+"""Build A/B variants of the library: each variant is compiled with extra -D
+flags into ab/lib_<name>.so (load one with MCB_LIB=ab/lib_<name>.so).  Only
+the files named by VARIANT_FILES (default: tabucol_warp.cu) are recompiled;
+the others are linked from the in-tree build (python -m
+paper_2109_05948_b200._build first).
     python tools/build_variants.py name=-DFOO=1,-DBAR=0 other=..."""
 import os
 import subprocess
@@ -20,8 +22,13 @@ def build(name, defs):
     ccbin = ["-ccbin", "/usr/bin/g++"] if os.path.exists("/usr/bin/g++") else []
     comp = [f for f in B.NVCC_FLAGS if f != "-shared"]
     objs = []
+    files = os.environ.get("VARIANT_FILES", "tabucol_warp.cu").split(",")
     for src in B.sources():
-        obj = os.path.join(odir, os.path.basename(src)[:-3] + ".o")
+        base = os.path.basename(src)
+        if base not in files:
+            objs.append(os.path.join(B.PKG, "build", base[:-3] + ".o"))
+            continue
+        obj = os.path.join(odir, base[:-3] + ".o")
         cmd = [B.nvcc(), *ccbin, *B.ARCH, *comp, *defs, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         subprocess.run(cmd, check=True, capture_output=True)
         objs.append(obj)
