@@ -25,10 +25,13 @@ def test_tabucol_golden_bit_exact(name):
     check_tabucol(TAB, name, out)
 
 
+@pytest.mark.parametrize("nt", ["128", "256"])
 @pytest.mark.parametrize("flags", [N.FLAG_FORCE_WIDE, N.FLAG_FORCE_GLOBAL])
 @pytest.mark.parametrize("name", ["c1", "c2w", "k70", "k3", "tenure"])
-def test_tabucol_table_variants_bit_exact(name, flags):
-    """int16/u32 tables and the L2-resident (global) tables give identical results."""
+def test_tabucol_table_variants_bit_exact(name, flags, nt, monkeypatch):
+    """int16/u32 tables and the L2-resident (global) tables give identical
+    results, with 128 and with 256 threads per individual (MCB_TC_NT)."""
+    monkeypatch.setenv("MCB_TC_NT", nt)
     g, A, k, keys, depth, cap = tabucol_case(TAB, name)
     out = LS._run_tabucol_batch(g, A.copy(), k, keys, depth, log_moves=cap > 0, flags=flags)
     check_tabucol(TAB, name, out)
