@@ -53,6 +53,9 @@ extern "C" {
 #define MCB_FLAG_FORCE_GLOBAL 0x8u /* gamma/tabu tables in global memory (L2-resident path, tests) */
 #define MCB_FLAG_PROFILE 0x100u    /* accumulate per-phase clock64 cycles (mcb_debug_phase_cycles) */
 #define MCB_FLAG_WSTATS 0x200u     /* warp kernel: event counters + phase cycles (mcb_debug_warp_stats) */
+#define MCB_FLAG_ASYNC 0x400u      /* mcb_tabucol_batch: no host synchronisation (per-stream scratch, every
+                                      fallback pass enqueued with device-side counts; CUDA-graph capturable
+                                      after one warm-up call); errors via mcb_tabucol_async_status */
 
 const char *mcb_version(void);
 const char *mcb_last_error(void);
@@ -103,6 +106,9 @@ int mcb_tabucol_batch(int32_t *assigns, int64_t p, int64_t n, int64_t k,
                       int64_t *iters_used, int64_t *diag,
                       int64_t log_cap, int32_t *log_v, int64_t *log_iter, int64_t *log_tt,
                       int64_t *log_cnt, int64_t *counters, uint32_t flags, void *stream);
+/* Status of the last MCB_FLAG_ASYNC mcb_tabucol_batch on `stream`
+ * (synchronises the stream; MCB_ERR_RANGE for colours outside [0, k)). */
+int mcb_tabucol_async_status(void *stream);
 int mcb_tabucol_batch_host(int32_t *assigns, int64_t p, int64_t n, int64_t k,
                            const int64_t *adj_indptr, const int32_t *adj_indices,
                            const int32_t *edges_u, const int32_t *edges_v, int64_t m,
@@ -169,6 +175,20 @@ int mcb_pairwise(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, i
 int mcb_pairwise_host(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n,
                       int64_t k, int32_t *cross, int32_t *within, int64_t job_begin,
                       int64_t job_end, uint32_t flags, void *stream);
+/*
+ * Sharded distances: a rank computes the job range
+ * [job_begin, job_end) of the same job space and writes the distances
+ * compactly, jobs16[j - job_begin] (int16: distances are <= n <= 32767);
+ * the ranks all-gather those vectors and mcb_pairwise_scatter expands the
+ * whole job space's vector into cross (p x q) and within (q x q, symmetric,
+ * zero diagonal).  Device pointers, asynchronous on `stream` except
+ * mcb_pairwise_jobs' range check of the colours (one flag read).
+ */
+int mcb_pairwise_jobs(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n,
+                      int64_t k, int16_t *jobs16, int64_t job_begin, int64_t job_end, uint32_t flags,
+                      void *stream);
+int mcb_pairwise_scatter(const int16_t *jobs16, int64_t p, int64_t q, int32_t *cross, int32_t *within,
+                         void *stream);
 
 /*
  * Population update (mc/population.py:59-127): merge p incumbents (pdist

@@ -22,11 +22,12 @@ FLAG_FORCE_WIDE = 0x4
 FLAG_FORCE_GLOBAL = 0x8
 FLAG_PROFILE = 0x100
 FLAG_WSTATS = 0x200
+FLAG_ASYNC = 0x400
 
 EXPORTS = [
     "mcb_version", "mcb_last_error", "mcb_device_count", "mcb_stream_values",
-    "mcb_tabucol_batch", "mcb_tabucol_batch_host", "mcb_wvcp_batch", "mcb_wvcp_batch_host",
-    "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_gpx_rows", "mcb_pairwise", "mcb_pairwise_host",
+    "mcb_tabucol_batch", "mcb_tabucol_batch_host", "mcb_tabucol_async_status", "mcb_wvcp_batch", "mcb_wvcp_batch_host",
+    "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_gpx_rows", "mcb_pairwise", "mcb_pairwise_host", "mcb_pairwise_jobs", "mcb_pairwise_scatter",
     "mcb_probe_smem_bandwidth", "mcb_probe_l2_bandwidth", "mcb_debug_phase_cycles", "mcb_debug_warp_stats", "mcb_debug_group_stats", "mcb_debug_wvcp_stats",
     "mcb_debug_modcheck", "mcb_tabucol_describe",
     "mcb_update_population", "mcb_update_population_host", "mcb_match_parents", "mcb_match_parents_host",
@@ -50,6 +51,7 @@ def _declare(L):
     tab = [P, I64, I64, I64, P, P, P, P, I64, I64, P, P, P, P, P, P, I64, P, P, P, P, P, U32, P]
     L.mcb_tabucol_batch.argtypes = tab
     L.mcb_tabucol_batch_host.argtypes = tab
+    L.mcb_tabucol_async_status.argtypes = [P]
     wv = [P, I64, I64, I64, P, P, P, P, I64, P, P, I64, P, I64, I64, I32, P, C.c_double, I64, P,
           P, P, P, P, P, P, I64, P, P, P, P, P, U32, P]
     L.mcb_wvcp_batch.argtypes = wv
@@ -61,6 +63,8 @@ def _declare(L):
     pw = [P, I64, P, I64, I64, I64, P, P, I64, I64, U32, P]
     L.mcb_pairwise.argtypes = pw
     L.mcb_pairwise_host.argtypes = pw
+    L.mcb_pairwise_jobs.argtypes = [P, I64, P, I64, I64, I64, P, I64, I64, U32, P]
+    L.mcb_pairwise_scatter.argtypes = [P, I64, I64, P, P, P]
     L.mcb_probe_smem_bandwidth.argtypes = [P, P]
     L.mcb_probe_l2_bandwidth.argtypes = [P, P]
     L.mcb_debug_phase_cycles.argtypes = [P, C.c_int]

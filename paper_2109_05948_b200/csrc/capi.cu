@@ -7,7 +7,9 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -48,7 +50,27 @@ int max_smem_optin() {
 
 static void *grow_buffer(void **buf, size_t *cap, size_t bytes);
 
+// MCB_FLAG_ASYNC calls key their scratch by stream (WsStreamKey), so calls
+// on different streams may overlap on the device and a stream's calls can be
+// captured into a CUDA graph (after one warm-up call has sized the buffers)
+static thread_local bool t_ws_keyed = false;
+static thread_local cudaStream_t t_ws_stream = nullptr;
+WsStreamKey::WsStreamKey(cudaStream_t s) : prev_keyed(t_ws_keyed), prev_stream(t_ws_stream) {
+    t_ws_keyed = true;
+    t_ws_stream = s;
+}
+WsStreamKey::~WsStreamKey() {
+    t_ws_keyed = prev_keyed;
+    t_ws_stream = (cudaStream_t)prev_stream;
+}
+static void *keyed_workspace(int slot, size_t bytes) {
+    static std::map<std::tuple<int, int, void *>, std::pair<void *, size_t>> bufs;
+    auto &e = bufs[std::make_tuple(cur_dev(), slot, (void *)t_ws_stream)];
+    return grow_buffer(&e.first, &e.second, bytes);
+}
+
 void *workspace(size_t bytes) {
+    if (t_ws_keyed) return keyed_workspace(1, bytes);
     static void *buf[64] = {nullptr};
     static size_t cap[64] = {0};
     const int d = cur_dev();
@@ -66,6 +88,7 @@ void *workspace3(size_t bytes) {
 // fourth: the group TabuCol kernel's adjacency bitset (alive while the
 // warp/CTA fallbacks of the same call use workspace / workspace2)
 void *workspace4(size_t bytes) {
+    if (t_ws_keyed) return keyed_workspace(4, bytes);
     static void *buf[64] = {nullptr};
     static size_t cap[64] = {0};
     const int d = cur_dev();
@@ -75,6 +98,7 @@ void *workspace4(size_t bytes) {
 // second independent scratch (kernels that need their own tables while the
 // first holds control words of the same call)
 void *workspace2(size_t bytes) {
+    if (t_ws_keyed) return keyed_workspace(2, bytes);
     static void *buf[64] = {nullptr};
     static size_t cap[64] = {0};
     const int d = cur_dev();
@@ -388,6 +412,26 @@ int mcb_pairwise(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, i
     std::lock_guard<std::mutex> lk(g_mu);
     return pairwise_run(pop, p, off, q, n, k, cross, within, job_begin, job_end, flags,
                         (cudaStream_t)stream);
+}
+
+int mcb_tabucol_async_status(void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return tabucol_async_status((cudaStream_t)stream);
+}
+
+int mcb_pairwise_jobs(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n,
+                      int64_t k, int16_t *jobs16, int64_t job_begin, int64_t job_end, uint32_t flags,
+                      void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!jobs16) return set_error(MCB_ERR_VALUE, "pairwise_jobs: jobs16 is null");
+    return pairwise_run(pop, p, off, q, n, k, nullptr, nullptr, job_begin, job_end, flags, (cudaStream_t)stream,
+                        jobs16);
+}
+
+int mcb_pairwise_scatter(const int16_t *jobs16, int64_t p, int64_t q, int32_t *cross, int32_t *within,
+                         void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return pairwise_scatter_run(jobs16, p, q, cross, within, (cudaStream_t)stream);
 }
 
 int mcb_pairwise_host(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n,

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
     pairwise_kernel(const uint8_t *__restrict__ pop, int64_t p, const uint8_t *__restrict__ off,
                     int64_t q, int n, int nb, int k, int32_t *__restrict__ cross,
                     int32_t *__restrict__ within, int64_t job_begin, int64_t job_end,
-                    int32_t *err) {
+                    int16_t *__restrict__ jobs16, int32_t *err) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const PdLayout L = pd_layout(n, k, WIDE);
@@ -328,7 +328,9 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
         }
         const int d = n - (int)total;
         if (lane == 0) {
-            if (is_cross) {
+            if (jobs16) {
+                jobs16[job - job_begin] = (int16_t)d;  // compact job-range output (sharding)
+            } else if (is_cross) {
                 cross[oi * q + oj] = d;
             } else {
                 within[oi * q + oj] = d;
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
 namespace {
 
 using PdKernel = void (*)(const uint8_t *, int64_t, const uint8_t *, int64_t, int, int, int, int32_t *,
-                          int32_t *, int64_t, int64_t, int32_t *);
+                          int32_t *, int64_t, int64_t, int16_t *, int32_t *);
 
 template <bool WIDE>
 PdKernel pd_pick(int kwd) {
@@ -374,7 +376,7 @@ PdKernel pd_pick(int kwd) {
 
 int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n, int64_t k,
                  int32_t *cross, int32_t *within, int64_t job_begin, int64_t job_end,
-                 uint32_t flags, cudaStream_t st) {
+                 uint32_t flags, cudaStream_t st, int16_t *jobs16) {
     if (p < 0 || q < 0 || n < 0 || k < 0) return set_error(MCB_ERR_VALUE, "pairwise: bad shape");
     const int64_t total = p * q + q * (q - 1) / 2;
     if (job_end < 0 || job_end > total) job_end = total;
@@ -415,7 +417,7 @@ int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, i
         const int64_t jobs = job_end - job_begin;
         const int grid = (int)std::min<int64_t>((jobs + warps - 1) / warps, (int64_t)per_sm * num_sms());
         kern<<<grid, warps * 32, smem, st>>>(pop8, p, off8, q, (int)n, nb, (int)k, cross, within, job_begin,
-                                             job_end, err);
+                                             job_end, jobs16, err);
         int32_t herr = 0;
         if (cudaGetLastError() != cudaSuccess ||
             cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
@@ -427,6 +429,45 @@ int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, i
         cudaMemsetAsync(err, 0, 4, st);
     }
     (void)flags;
+    return MCB_OK;
+}
+
+// the whole job space's results (int16, job order: cross row-major, then the
+// within pairs i < j) -> the cross matrix and the symmetric within matrix
+__global__ void pd_scatter_kernel(const int16_t *__restrict__ jobs, int64_t p, int64_t q, int32_t *__restrict__ cross,
+                                  int32_t *__restrict__ within) {
+    const int64_t pq = p * q;
+    const int64_t total = pq + q * (q - 1) / 2;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total; j += (int64_t)gridDim.x * blockDim.x) {
+        const int d = jobs[j];
+        if (j < pq) {
+            cross[j] = d;
+        } else {
+            // row i of the upper triangle holds q-1-i pairs (distance.py:106-112)
+            const int64_t r = j - pq;
+            const double b = 2.0 * (double)q - 1.0;
+            int64_t i = (int64_t)floor((b - sqrt(fmax(b * b - 8.0 * (double)r, 0.0))) / 2.0);
+            i = max((int64_t)0, min(i, q - 2));
+            auto S = [&](int64_t t) { return t * (2 * q - t - 1) / 2; };
+            while (i > 0 && S(i) > r) i--;
+            while (i + 1 <= q - 2 && S(i + 1) <= r) i++;
+            const int64_t jj = i + 1 + (r - S(i));
+            within[i * q + jj] = d;
+            within[jj * q + i] = d;
+        }
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q; i += (int64_t)gridDim.x * blockDim.x)
+        within[i * q + i] = 0;
+}
+
+int pairwise_scatter_run(const int16_t *jobs, int64_t p, int64_t q, int32_t *cross, int32_t *within,
+                         cudaStream_t st) {
+    if (p < 0 || q < 0) return set_error(MCB_ERR_VALUE, "pairwise_scatter: bad shape");
+    const int64_t total = p * q + q * (q - 1) / 2;
+    if (total == 0 && q == 0) return MCB_OK;
+    const int grid = (int)std::min<int64_t>((std::max<int64_t>(total, q) + 255) / 256, 8 * (int64_t)num_sms());
+    pd_scatter_kernel<<<std::max(grid, 1), 256, 0, st>>>(jobs, p, q, cross, within);
+    if (cudaGetLastError() != cudaSuccess) return set_error(MCB_ERR_CUDA, "pairwise_scatter launch failed");
     return MCB_OK;
 }
 

@@ -16,6 +16,15 @@ void *workspace(size_t bytes);
 void *workspace2(size_t bytes);
 void *workspace3(size_t bytes);
 void *workspace4(size_t bytes);
+// scope in which workspace / workspace2 / workspace4 are per-stream buffers
+struct WsStreamKey {
+    explicit WsStreamKey(cudaStream_t s);
+    ~WsStreamKey();
+    bool prev_keyed;
+    void *prev_stream;
+};
+// device-side error word of the last MCB_FLAG_ASYNC TabuCol call on a stream
+int tabucol_async_status(cudaStream_t st);
 
 struct TabucolArgs {
     int32_t *assigns;
@@ -38,7 +47,7 @@ int tabucol_run(const TabucolArgs &a, cudaStream_t st);
 // variant whose tabu ring continues in global memory (no 1024-entry limit)
 int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *work_counter, int32_t *ovf_list,
                         int32_t *ovf_count, int32_t *err_flag, const int32_t *work_list = nullptr,
-                        int64_t nwork = -1, bool spill = false);
+                        int64_t nwork = -1, bool spill = false, const int32_t *nwork_dev = nullptr);
 // group-of-warps kernel (tabucol_group.cu); -1 = shape outside its envelope
 int tabucol_group_launch(const TabucolArgs &A, cudaStream_t st, int32_t *work_counter, int32_t *ovf_list,
                          int32_t *ovf_count, int32_t *err_flag);
@@ -84,7 +93,9 @@ int gpx_rows_run(const int32_t *pop, int64_t p, int64_t n, const int64_t *matche
                  uint32_t flags, cudaStream_t st);
 int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, int64_t n, int64_t k,
                  int32_t *cross, int32_t *within, int64_t job_begin, int64_t job_end,
-                 uint32_t flags, cudaStream_t st);
+                 uint32_t flags, cudaStream_t st, int16_t *jobs16 = nullptr);
+int pairwise_scatter_run(const int16_t *jobs, int64_t p, int64_t q, int32_t *cross, int32_t *within,
+                         cudaStream_t st);
 int update_population_run(const int32_t *pdist, const int32_t *cross, const int32_t *within,
                           const int64_t *fit_pop, const int64_t *fit_new, int64_t p, int64_t q, int64_t ms,
                           const int32_t *pop_assigns, const int32_t *new_assigns, int64_t n,

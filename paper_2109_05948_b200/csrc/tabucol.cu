@@ -42,6 +42,8 @@
 // (u16 gamma / u32 expiry) instantiation; results are identical by
 // construction (same arithmetic, wider storage).
 #include <algorithm>
+#include <map>
+#include <memory>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -1081,6 +1083,25 @@ int tabucol_phase_cycles(unsigned long long *out, int reset) {
     return MCB_OK;
 }
 
+static const int32_t *&async_err_slot(cudaStream_t st) {
+    static std::map<std::pair<int, void *>, const int32_t *> slots;
+    int d = 0;
+    cudaGetDevice(&d);
+    return slots[std::make_pair(d, (void *)st)];
+}
+
+int tabucol_async_status(cudaStream_t st) {
+    const int32_t *e = async_err_slot(st);
+    if (!e) return MCB_OK;
+    int32_t h = 0;
+    if (cudaMemcpyAsync(&h, e, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "tabucol: kernel failed: %s", cudaGetErrorString(cudaGetLastError()));
+    if (h == 1) return set_error(MCB_ERR_RANGE, "color id out of range [0, k)");
+    if (h == 2) return set_error(MCB_ERR_UNSUPPORTED, "tabucol: wide tables overflowed");
+    return MCB_OK;
+}
+
 int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     if (A.p < 0 || A.n < 1 || A.k < 1 || A.depth < 0 || A.m < 0)
         return set_error(MCB_ERR_VALUE, "tabucol: bad shape p=%lld n=%lld k=%lld depth=%lld",
@@ -1088,6 +1109,11 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     if (A.n > 32767 || A.k > 255)
         return set_error(MCB_ERR_UNSUPPORTED, "tabucol: n<=32767 and k<=255 required");
     if (A.p == 0) return MCB_OK;
+    // MCB_FLAG_ASYNC: no host synchronisation at all -- per-stream scratch, the
+    // fallback passes always enqueued with device-side work counts, errors left
+    // in the device word mcb_tabucol_async_status reads (graph-capturable)
+    const bool async = (A.flags & MCB_FLAG_ASYNC) != 0;
+    std::unique_ptr<WsStreamKey> wskey(async ? new WsStreamKey(st) : nullptr);
     const int n = (int)A.n, k = (int)A.k, kp = (k + 3) & ~3;
     // every shape must be able to fall back to the wide CTA pass, whose
     // per-vertex state (u32 expiries, scan records, lists) lives in shared
@@ -1187,7 +1213,15 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
         if (rc > 0) return rc;
         warp_done = rc == MCB_OK;
     }
-    if (warp_done) {
+    if (warp_done && async) {
+        // the SPILL pass over the warp pass's overflow list, then the wide pass
+        // over the SPILL pass's list, both sized for the worst case
+        rc = tabucol_warp_launch(A, st, ctl32 + 4, ovf_spill, ctl32 + 5, ctl32 + 3, ovf_warp, A.p, true,
+                                 ctl32 + 2);
+        if (rc > 0) return rc;
+        ovf_final = rc == MCB_OK ? ovf_spill : ovf_warp;
+        ovf_final_count = rc == MCB_OK ? ctl32 + 5 : ctl32 + 2;
+    } else if (warp_done) {
         int32_t h[2] = {0, 0};  // [0] = overflowed individuals, [1] = error flag
         if (cudaMemcpyAsync(h, ctl32 + 2, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
             cudaStreamSynchronize(st) != cudaSuccess)
@@ -1252,6 +1286,10 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
     int g2 = 1;
     rc = launch_variant<uint16_t, uint32_t, false>(Q, wide_grid, (int)A.p, st, &g2, false);
     if (rc) return rc;
+    if (async) {
+        async_err_slot(st) = ctl32 + 3;
+        return MCB_OK;
+    }
 
     int32_t err = 0;
     if (cudaMemcpyAsync(&err, ctl32 + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||

@@ -82,6 +82,7 @@ struct WarpTabuParams {
     int64_t *log_iter, *log_tt, *log_cnt;
     int64_t *counters;
     int nwork;
+    const int32_t *nwork_dev;  // device-side count (overrides nwork when set)
     const int32_t *work_list;  // individual ids (nullptr: 0 .. nwork-1)
     uint32_t *spill;           // SPILL variant: per-warp ring rows in global memory
     int spill_rows;            // rows per warp (power of two)
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
         int wi = 0;
         if (lane == 0) wi = atomicAdd(P.work_counter, 1);
         wi = __shfl_sync(FULLM, wi, 0);
-        if (wi >= P.nwork) break;
+        if (wi >= (P.nwork_dev ? *P.nwork_dev : P.nwork)) break;
         const int ind = P.work_list ? P.work_list[wi] : wi;
         const uint64_t key = P.keys[ind];
         int32_t *a_io = P.assigns + (size_t)ind * n;
@@ -1139,7 +1140,7 @@ static int upload_divtab(cudaStream_t st) {
 
 int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, int32_t *ovf_list,
                         int32_t *ovf_count, int32_t *err_flag, const int32_t *work_list, int64_t nwork,
-                        bool spill) {
+                        bool spill, const int32_t *nwork_dev) {
     if (A.flags & (MCB_FLAG_FORCE_WIDE | MCB_FLAG_FORCE_GLOBAL | MCB_FLAG_PROFILE)) return -1;
     if (A.flags & MCB_FLAG_WSTATS) {
         // reset the counters of this launch
@@ -1161,10 +1162,7 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
     constexpr int SPILL_ROWS = 256;
     const size_t spill_bytes = spill ? (size_t)pl.grid * pl.warps * SPILL_ROWS * 32 * 4 : 0;
     (void)kp;
-    int64_t nnz_h = 0;
-    if (cudaMemcpyAsync(&nnz_h, A.indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess)
-        return set_error(MCB_ERR_CUDA, "tabucol_warp: indptr read failed");
+    const int64_t nnz_h = 2 * A.m;  // CSR of an undirected graph (no host read of indptr[n])
     const size_t graph_bytes = pl.ch ? pl.bitset_global : (4 * (size_t)(n + 1) + 2 * (size_t)nnz_h + 256);
     uint8_t *ws = (uint8_t *)workspace2(spill_bytes + graph_bytes + 512);
     if (!ws) return set_error(MCB_ERR_CUDA, "tabucol_warp: workspace allocation failed");
@@ -1206,6 +1204,7 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
     P.log_cnt = A.log_cnt;
     P.counters = A.counters;
     P.nwork = (int)nwork;
+    P.nwork_dev = nwork_dev;
     P.work_counter = ctl32;
     P.ovf_list = ovf_list;
     P.ovf_count = ovf_count;

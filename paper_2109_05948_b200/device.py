@@ -71,6 +71,12 @@ def tabucol_batch(dg, assigns, k, keys, depth, *, flags=N.FLAG_DIAG, counters=Fa
     return out
 
 
+def tabucol_async_status():
+    """Raise for the last asynchronous (FLAG_ASYNC) TabuCol call on the current
+    stream (synchronises it): ValueError for colours outside [0, k)."""
+    N.check(N.lib().mcb_tabucol_async_status(_stream_handle()))
+
+
 def wvcp_batch(dg, assigns, k, keys, depth, rounds, schedule_on, phi0, *, flags=N.FLAG_DIAG):
     assert assigns.is_cuda and assigns.dtype == torch.int32 and assigns.is_contiguous()
     p, n = assigns.shape
@@ -118,6 +124,26 @@ def pairwise(pop, off, k, job_begin=0, job_end=-1, cross=None, within=None):
         within = torch.zeros((q, q), dtype=torch.int32, device=dev)
     N.check(N.lib().mcb_pairwise(N.ptr(pop), p, N.ptr(off), q, n, int(k), N.ptr(cross),
                                  N.ptr(within), int(job_begin), int(job_end), 0, _stream_handle()))
+    return cross, within
+
+
+def pairwise_jobs(pop, off, k, job_begin, job_end, out=None):
+    """Distances of the job range [job_begin, job_end) of the (pop, off) job
+    space as a compact int16 vector (`mcb_pairwise_jobs`, the sharded path)."""
+    p, q = pop.shape[0], off.shape[0]
+    n = off.shape[1]
+    if out is None:
+        out = torch.empty(max(job_end - job_begin, 0), dtype=torch.int16, device=off.device)
+    N.check(N.lib().mcb_pairwise_jobs(N.ptr(pop), p, N.ptr(off), q, n, int(k), N.ptr(out), int(job_begin),
+                                      int(job_end), 0, _stream_handle()))
+    return out
+
+
+def pairwise_scatter(jobs, p, q, device):
+    """The whole job space's int16 vector -> (cross p x q, within q x q) int32."""
+    cross = torch.empty((p, q), dtype=torch.int32, device=device)
+    within = torch.empty((q, q), dtype=torch.int32, device=device)
+    N.check(N.lib().mcb_pairwise_scatter(N.ptr(jobs), p, q, N.ptr(cross), N.ptr(within), _stream_handle()))
     return cross, within
 
 

@@ -106,9 +106,29 @@ def col_generation(dg, st, *, seed, depth, K, ms=None, timings=None):
     return generation(dg, st, seed=seed, depth=depth, K=K, ms=ms, timings=timings)
 
 
+def _all_gather_blocks(pad, group):
+    """Equal-size blocks of every rank, concatenated in rank order: NCCL
+    all-gather into one tensor; other backends (gloo, e.g. the world-2 test
+    on one GPU) through host staging."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    short = pad.dtype == torch.int16  # neither torch's NCCL nor gloo group takes int16: move its bytes
+    wire = pad.view(torch.uint8) if short else pad
+    if dist.get_backend(group) == "nccl":
+        buf = torch.empty((world * wire.shape[0],) + tuple(wire.shape[1:]), dtype=wire.dtype, device=wire.device)
+        dist.all_gather_into_tensor(buf, wire, group=group)
+    else:
+        host = wire.cpu()
+        parts = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(parts, host, group=group)
+        buf = torch.cat(parts, 0).to(pad.device)
+    return buf.view(torch.int16) if short else buf
+
+
 def _gather_rows(local, total, world, rank, group):
     """Rows [lo_r, hi_r) of every rank -> the whole (total, ...) tensor on this
-    device (NCCL all-gather of equal-size padded blocks)."""
+    device (all-gather of equal-size padded blocks)."""
     import torch.distributed as dist
 
     from .shard import shard_range
@@ -118,8 +138,7 @@ def _gather_rows(local, total, world, rank, group):
     cap = -(-total // world)
     pad = torch.zeros((cap,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     pad[: local.shape[0]] = local
-    buf = torch.empty((world * cap,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(buf, pad, group=group)
+    buf = _all_gather_blocks(pad, group)
     parts = []
     for r in range(world):
         lo, hi = shard_range(total, world, r)
@@ -146,8 +165,9 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
     Multi-GPU (`group`, one process per GPU, NCCL): every rank
     holds the whole population; the LS runs on this rank's individuals
     [lo, hi) with their global stream keys, the improved colourings and
-    fitness are all-gathered, the distance job space is split and the partial
-    matrices SUM-all-reduced, the pool update / matching / surrogate training
+    fitness are all-gathered, the distance job space is split and each rank's
+    results all-gathered as compact int16 vectors (`mcb_pairwise_jobs`,
+    expanded by `mcb_pairwise_scatter`), the pool update / matching / surrogate training
     run replicated (deterministic), GPX and selection run on this rank's rows
     and the offspring are all-gathered -- the same results on every rank as
     one process (`shard.col_generation_sharded` is the host-level twin, tested
@@ -159,7 +179,7 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
     if world > 1 or force_shard:
         return _generation_sharded(dg, st, seed=seed, depth=depth, K=K, ms=ms, max_rounds=max_rounds, phi0=phi0,
                                    net=net, epochs=epochs, batch_size=batch_size, group=group, world=world,
-                                   rank=rank)
+                                   rank=rank, timings=timings)
     p, n, k, t = st.p, st.n, st.k, st.generation
     dev = st.pop_assigns.device
     ms = min_spacing(n) if ms is None else ms
@@ -236,7 +256,7 @@ def generation(dg, st, *, seed, depth, K, ms=None, timings=None, max_rounds=10, 
 
 
 def _generation_sharded(dg, st, *, seed, depth, K, ms, max_rounds, phi0, net, epochs, batch_size, group, world,
-                        rank):
+                        rank, timings=None):
     import torch.distributed as dist
 
     from .shard import shard_range
@@ -244,6 +264,15 @@ def _generation_sharded(dg, st, *, seed, depth, K, ms, max_rounds, phi0, net, ep
     p, n, k, t = st.p, st.n, st.k, st.generation
     dev = st.pop_assigns.device
     ms = min_spacing(n) if ms is None else ms
+    marks = []
+
+    def mark(name):
+        if timings is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append((name, e))
+
+    mark(None)
     lo, hi = shard_range(p, world, rank)
     keys = Dv.keys_to_tensor(stream_keys(seed, TAG_LS, t, hi - lo, start=lo), dev)
     start = st.offspring[lo:hi].clone()
@@ -254,12 +283,17 @@ def _generation_sharded(dg, st, *, seed, depth, K, ms, max_rounds, phi0, net, ep
         legal = ls["best_scores"] < INF_SCORE
         imp_loc = torch.where(legal[:, None], ls["best_assigns"], start).contiguous()
         fit_loc = torch.where(legal, ls["best_scores"], torch.full_like(ls["best_scores"], INF_SCORE))
+        end_fit_loc = ls["end_scores"]
     else:
         ls = Dv.tabucol_batch(dg, start.clone(), k, keys, depth)
         imp_loc, fit_loc = ls["best_assigns"], ls["best_conflicts"]
+        end_fit_loc = ls["end_conflicts"]
+    mark("ls")
     # elites: the improved colourings (uint8 over NVLink) and their fitness
-    improved = _gather_rows(imp_loc.to(torch.uint8) if k <= 256 else imp_loc, p, world, rank, group).to(torch.int32)
+    as8 = (lambda a: a.to(torch.uint8)) if k <= 256 else (lambda a: a)  # noqa: E731
+    improved = _gather_rows(as8(imp_loc), p, world, rank, group).to(torch.int32)
     imp_fit = _gather_rows(fit_loc.contiguous(), p, world, rank, group)
+    mark("elite_allgather")
     st.best_score = min(st.best_score, int(imp_fit.min().item()))
     if net is not None:
         from .rng import TAG_TRAIN, Stream
@@ -268,15 +302,17 @@ def _generation_sharded(dg, st, *, seed, depth, K, ms, max_rounds, phi0, net, ep
         if int(mask.sum().item()) >= 2:
             net.train_generation(st.offspring[mask], imp_fit[mask].double().cpu().numpy(), k, epochs, batch_size,
                                  Stream.derive(seed, TAG_TRAIN, t))
-    # distances: this rank's slice of the job space, partial matrices summed
+        mark("surrogate_train")
+    # distances: this rank's slice of the reference's job space as compact
+    # int16 results, all-gathered, then expanded into cross / within
     total = p * p + p * (p - 1) // 2
     jlo, jhi = shard_range(total, world, rank)
-    cross = torch.zeros((p, p), dtype=torch.int32, device=dev)
-    within = torch.zeros((p, p), dtype=torch.int32, device=dev)
-    Dv.pairwise(st.pop_assigns, improved, k, jlo, jhi, cross=cross, within=within)
+    jobs = Dv.pairwise_jobs(st.pop_assigns, improved, k, jlo, jhi)
+    mark("distances")
     if dist.is_initialized():
-        dist.all_reduce(cross, group=group)
-        dist.all_reduce(within, group=group)
+        jobs = _gather_rows(jobs, total, world, rank, group)
+    mark("distance_allgather")
+    cross, within = Dv.pairwise_scatter(jobs, p, p, dev)
     # pool update and matching: replicated, identical on every rank
     adm = torch.empty(p, dtype=torch.int32, device=dev)
     rule = torch.empty(p, dtype=torch.uint8, device=dev)
@@ -289,8 +325,10 @@ def _generation_sharded(dg, st, *, seed, depth, K, ms, max_rounds, phi0, net, ep
         P(st.pop_assigns), P(improved), n, P(adm), P(rule), P(new_dist), P(new_assigns), P(new_fit),
         _stream()))
     st.pop_assigns, st.pop_fitness, st.pop_dist = new_assigns, new_fit, new_dist
+    mark("update_population")
     matches = torch.empty((p, K), dtype=torch.int64, device=dev)
     N.check(N.lib().mcb_match_parents(P(st.pop_dist), p, int(K), n, P(matches), _stream()))
+    mark("match_parents")
     # GPX and selection on this rank's rows, then the offspring all-gathered
     ck = Dv.keys_to_tensor(stream_keys(seed, TAG_CROSS, t, (hi - lo) * K, start=lo * K), dev)
     cands = Dv.gpx_rows(st.pop_assigns, matches[lo:hi].contiguous(), lo, k, ck)
@@ -305,13 +343,25 @@ def _generation_sharded(dg, st, *, seed, depth, K, ms, max_rounds, phi0, net, ep
         hi32, lo32 = (sv >> 32) & 0xFFFFFFFF, sv & 0xFFFFFFFF
         sel = ((hi32 % K) * ((1 << 32) % K) + lo32 % K) % K
     off_loc = cands[torch.arange(rows, device=dev), sel].contiguous()
-    st.offspring = _gather_rows(off_loc.to(torch.uint8) if k <= 256 else off_loc, p, world, rank, group).to(torch.int32)
+    mark("gpx_select")
+    st.offspring = _gather_rows(as8(off_loc), p, world, rank, group).to(torch.int32)
+    mark("offspring_allgather")
     st.generation = t + 1
-    out = dict(ls)
-    out["best_assigns"] = improved
+    # the LS outputs of the whole population (every entry gathered)
+    out = {"best_assigns": improved,
+           "end_assigns": _gather_rows(as8(ls["end_assigns"]), p, world, rank, group).to(torch.int32),
+           "diag": _gather_rows(ls["diag"].contiguous(), p, world, rank, group)}
     if st.mode == "wvcp":
         out["best_scores"] = imp_fit
+        out["end_scores"] = _gather_rows(end_fit_loc.contiguous(), p, world, rank, group)
+        out["end_conflicts"] = _gather_rows(ls["end_conflicts"].contiguous(), p, world, rank, group)
+        out["phi_used"] = _gather_rows(ls["phi_used"].contiguous(), p, world, rank, group)
     else:
         out["best_conflicts"] = imp_fit
+        out["end_conflicts"] = _gather_rows(end_fit_loc.contiguous(), p, world, rank, group)
+        out["iters_used"] = _gather_rows(ls["iters_used"].contiguous(), p, world, rank, group)
+    if timings is not None:
+        torch.cuda.synchronize()
+        for (_, e0), (name, e1) in zip(marks[:-1], marks[1:]):
+            timings[name] = timings.get(name, 0.0) + e0.elapsed_time(e1) / 1e3
     return out
-

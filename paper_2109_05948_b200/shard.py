@@ -11,9 +11,10 @@ the whole population for the next operator:
 
 * local search: shard by individual, then all-gather the elites;
 * pairwise distances: shard the reference's linear job space
-  [0, p*q + q(q-1)/2) (`distance.py:94-113`) into contiguous ranges; every job
-  writes distinct cells, so a SUM all-reduce of the partial matrices (zeros
-  elsewhere) reconstructs them;
+  [0, p*q + q(q-1)/2) (`distance.py:94-113`) into contiguous ranges; every
+  rank's results travel as one compact int16 vector of its job range
+  (distances are <= n), all-gathered and expanded into cross / within --
+  3 p q / 2 bytes per generation instead of all-reducing two int32 matrices;
 * GPX: shard by individual i (rows of `matches`); parents are read from the
   replicated population; then all-gather the offspring rows.
 
@@ -50,7 +51,12 @@ def _all_gather_rows(local, total_rows, group, device):
     world, rank = _world(group)
     if world == 1:
         return local
-    t = torch.as_tensor(np.ascontiguousarray(local)).to(device)
+    local = np.ascontiguousarray(local)
+    if local.dtype == np.int16 and dist.get_backend(group) == "gloo":
+        # gloo has no int16: move the same bytes as (rows, 2) uint8
+        return _all_gather_rows(local.view(np.uint8).reshape(-1, 2), total_rows, group, device).reshape(-1).view(
+            np.int16)
+    t = torch.as_tensor(local).to(device)
     shapes = [shard_range(total_rows, world, r) for r in range(world)]
     maxrows = max(hi - lo for lo, hi in shapes)
     pad = torch.zeros((maxrows,) + tuple(t.shape[1:]), dtype=t.dtype, device=device)
@@ -87,20 +93,27 @@ def pairwise_sharded(pop, off, k, pair_fn, group=None, device="cpu"):
     """`pairwise_distances` with the job space split over ranks.
 
     `pair_fn(pop, off, k, job_begin, job_end) -> (cross, within)` computes the
-    given job range (zeros elsewhere), e.g. `distance.pairwise_raw`.
+    given job range (zeros elsewhere), e.g. `distance.pairwise_raw`; the
+    range's distances are exchanged as int16 job vectors.
     """
     world, rank = _world(group)
     p, q = pop.shape[0], off.shape[0]
-    total = p * q + q * (q - 1) // 2
+    pq = p * q
+    total = pq + q * (q - 1) // 2
     lo, hi = shard_range(total, world, rank)
     cross, within = pair_fn(pop, off, k, lo, hi)
     if world == 1:
         return cross, within
-    c = torch.as_tensor(np.ascontiguousarray(cross)).to(device)
-    w = torch.as_tensor(np.ascontiguousarray(within)).to(device)
-    dist.all_reduce(c, group=group)
-    dist.all_reduce(w, group=group)
-    return c.cpu().numpy(), w.cpu().numpy()
+    iu, ju = np.triu_indices(q, 1)  # the within jobs in the reference's order (:103-113)
+    wl, wh = max(lo - pq, 0), max(hi - pq, 0)
+    vec = np.concatenate([np.asarray(cross).reshape(-1)[min(lo, pq):min(hi, pq)],
+                          np.asarray(within)[iu[wl:wh], ju[wl:wh]]]).astype(np.int16)
+    allv = _all_gather_rows(vec, total, group, device).astype(np.int32)
+    cross = allv[:pq].reshape(p, q).copy()
+    within = np.zeros((q, q), dtype=np.int32)
+    within[iu, ju] = allv[pq:]
+    within[ju, iu] = allv[pq:]
+    return cross, within
 
 
 def offspring_sharded(pop, matches, k, master_seed, generation, gpx_fn, group=None, device="cpu"):

@@ -172,3 +172,63 @@ def test_device_sharded_generation_nccl_world1():
                 np.testing.assert_array_equal(st.offspring.cpu().numpy(), ENG[pre + f"g{t}_offspring"])
     finally:
         dist.destroy_process_group()
+
+
+def _world2_worker(rank, port, out_path):
+    import os
+    import sys
+
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=2)
+    try:
+        eng = load_golden("engine")
+        res = {}
+        for name in [str(c) for c in eng["cases"]]:
+            pre = name + "__"
+            seed, n, pe, k, p, K, depth, G = (int(x) for x in eng[pre + "params"])
+            g = rand_graph(seed, n, pe / 1000.0)
+            dg = Dv.DeviceGraph(g, "cuda")
+            st = E.init_state(dg, eng[pre + "init"], k)
+            timings = {}
+            for t in range(G):
+                ls = E.generation(dg, st, seed=seed, depth=depth, K=K, timings=timings)
+                torch.cuda.synchronize()
+                res[f"{name}_g{t}_pop"] = st.pop_assigns.cpu().numpy()
+                res[f"{name}_g{t}_dist"] = st.pop_dist.cpu().numpy()
+                res[f"{name}_g{t}_offspring"] = st.offspring.cpu().numpy()
+                for key in ("best_assigns", "best_conflicts", "end_assigns", "end_conflicts", "iters_used"):
+                    res[f"{name}_g{t}_ls_{key}"] = ls[key].cpu().numpy()
+            res[f"{name}_timing_stages"] = np.array(sorted(timings))
+        if rank == 0:
+            np.savez(out_path, **res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_device_sharded_generation_world2(tmp_path):
+    """The device-resident sharded generation at world size 2 (two processes
+    on this GPU, gloo all-gathers with host staging -- the ranks' kernels never
+    wait on each other): the same state after every generation as the
+    reference chain, LS outputs gathered for the whole population, per-stage
+    timings reported."""
+    import torch.multiprocessing as mp
+
+    from test_shard import _free_port
+
+    out = str(tmp_path / "w2.npz")
+    mp.start_processes(_world2_worker, args=(_free_port(), out), nprocs=2, join=True, start_method="spawn")
+    res = np.load(out)
+    for name in [str(c) for c in ENG["cases"]]:
+        pre = name + "__"
+        seed, n, pe, k, p, K, depth, G = (int(x) for x in ENG[pre + "params"])
+        for t in range(G):
+            np.testing.assert_array_equal(res[f"{name}_g{t}_pop"], ENG[pre + f"g{t}_pop"], err_msg=f"{name} g{t}")
+            np.testing.assert_array_equal(res[f"{name}_g{t}_dist"], ENG[pre + f"g{t}_dist"])
+            np.testing.assert_array_equal(res[f"{name}_g{t}_offspring"], ENG[pre + f"g{t}_offspring"])
+            assert res[f"{name}_g{t}_ls_best_assigns"].shape == (p, n)
+            assert res[f"{name}_g{t}_ls_iters_used"].shape == (p,)
+        stages = set(res[f"{name}_timing_stages"].tolist())
+        assert {"ls", "elite_allgather", "distances", "distance_allgather", "update_population"} <= stages
