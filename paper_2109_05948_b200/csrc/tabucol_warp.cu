@@ -59,11 +59,13 @@
 #define TW_DIVREG 1  // first-round reservoir divisor entries in registers
 #endif
 
+#ifndef TW_STATS_TU
+#define TW_STATS_TU 0  // 1: the instrumented instantiations (tabucol_warp_stats.cu)
+#endif
+
 namespace mcb {
 
 using namespace tw;
-
-namespace {
 
 struct WarpTabuParams {
     int32_t *assigns;
@@ -92,6 +94,8 @@ struct WarpTabuParams {
     int warp_smem;     // bytes per warp region
     int bitset_bytes;  // bytes of the CTA-shared bitset copy (0: rows read from L2)
 };
+
+namespace {
 
 __device__ unsigned long long g_wstats[40];
 // divisibility by s = o * 2^t, odd o < 64: x % s == 0  <=>  low t bits of x are
@@ -139,9 +143,9 @@ enum {
     WS_N = 40
 };
 #define WST(i, x) \
-    if (stats) st[i] += (x)
+    if constexpr (stats) st[i] += (x)
 #define WPH(i)                          \
-    if (stats) {                        \
+    if constexpr (stats) {              \
         const long long _t = clock64(); \
         st[i] += _t - ph_t;             \
         ph_t = _t;                      \
@@ -160,9 +164,10 @@ enum {
 // bytes translate colours with phys().
 // ---------------------------------------------------------------------------
 
-template <int KV, int CH, bool BITSET, bool SPILL>
+template <int KV, int CH, bool BITSET, bool SPILL, bool STATS>
 __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(WarpTabuParams P) {
     constexpr int KP = 16 * KV, KW = 4 * KV;
+    constexpr int CBITS = KP <= 16 ? 4 : KP <= 32 ? 5 : KP <= 64 ? 6 : 7;  // a row's tie count < KP
     constexpr int RW = 2;  // conflicting rows per lane per scan round
     constexpr int SW = KW <= 4 ? 4 : KW <= 8 ? 8 : KW <= 16 ? 16 : 32;  // walk segment width
     static_assert(KW <= 32, "k <= 128");
@@ -198,9 +203,9 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
     const bool prod = (P.flags & MCB_FLAG_PRODUCTION) != 0;
     const bool diagf = (P.flags & MCB_FLAG_DIAG) != 0;
     const bool cnt_on = P.counters != nullptr;
-    const bool stats = (P.flags & MCB_FLAG_WSTATS) != 0;
-    long long st[WS_N];
-    if (stats)
+    constexpr bool stats = STATS;  // MCB_FLAG_WSTATS selects the instrumented instantiation
+    long long st[STATS ? WS_N : 1];
+    if constexpr (stats)
         for (int i = 0; i < WS_N; i++) st[i] = 0;
     const int g_lane = S::g(lane);  // rotation of every row this lane owns (u = lane + 32q)
     // this lane's first-round reservoir divisor s = 2 + lane (< 64): its table
@@ -325,7 +330,8 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
         if (k >= 2 && !bad) {
             for (long long step = 0; step < P.depth; step++) {
                 if (conflicts == 0) break;
-                long long ph_t = stats ? clock64() : 0;
+                long long ph_t = 0;
+                if constexpr (stats) ph_t = clock64();
                 WST(WS_IT, 1);
                 const uint32_t it32 = (uint32_t)it;
                 const int thr = (int)max(best - conflicts, (long long)-TW_BIG);
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                             if (m < (int)TABU) rm[h] = m - gva[h];
                         }
                     }
-                    if (stats) WST(WS_ASP_ROUNDS, __any_sync(FULLM, A[0] > 0));
+                    WST(WS_ASP_ROUNDS, __any_sync(FULLM, A[0] > 0));
                     WPH(WS_CY_ROWMIN);
                     // running minimum entering each row (RW interleaved scans)
                     int in[RW];
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                         e_v = v;
                         e_gv = gv;
                         e_cD = cD;
-                        e_ex = excl_sum_small<8>(cD, lt_mask);
+                        e_ex = excl_sum_small<CBITS>(cD, lt_mask);
                         T = __reduce_add_sync(FULLM, cD);
                         while (low) {
                             WST(WS_WALK_PASSES, 1);
@@ -959,10 +965,12 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
         }
         __syncwarp();
 
-        if (stats && lane == 0)
-            for (int i = 0; i < WS_N; i++)
-                if (st[i]) atomicAdd(&g_wstats[i], (unsigned long long)st[i]);
-        if (stats)
+        if constexpr (stats) {
+            if (lane == 0)
+                for (int i = 0; i < WS_N; i++)
+                    if (st[i]) atomicAdd(&g_wstats[i], (unsigned long long)st[i]);
+        }
+        if constexpr (stats)
             for (int i = 0; i < WS_N; i++) st[i] = 0;
         // ---------------- outputs (:407-410) ----------------
         if (!bad) {
@@ -986,6 +994,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
     }
 }
 
+#if !TW_STATS_TU
 // lane-interleaved bitset: row v = 32 chunks of CH bits, bit q of chunk L <->
 // vertex L + 32 q (bit index L*CH + q of the row)
 __global__ void tw_bitset_kernel(const int64_t *indptr, const int32_t *indices, int n, int ch,
@@ -1007,33 +1016,76 @@ __global__ void tw_csr16_kernel(const int64_t *indptr, const int32_t *indices, i
     for (int64_t i = t0; i < nnz; i += st) nb16[i] = (uint16_t)indices[i];
 }
 
+#endif  // !TW_STATS_TU
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 using KernT = void (*)(WarpTabuParams);
 
-template <int KV, bool SPILL>
+template <int KV, bool SPILL, bool STATS>
 static KernT pick_mode(int ch) {
     switch (ch) {
-        case 8: return tabucol_warp_kernel<KV, 8, true, SPILL>;
-        case 16: return tabucol_warp_kernel<KV, 16, true, SPILL>;
-        case 32: return tabucol_warp_kernel<KV, 32, true, SPILL>;
-        default: return tabucol_warp_kernel<KV, 32, false, SPILL>;  // CSR, n <= 1024
+        case 8: return tabucol_warp_kernel<KV, 8, true, SPILL, STATS>;
+        case 16: return tabucol_warp_kernel<KV, 16, true, SPILL, STATS>;
+        case 32: return tabucol_warp_kernel<KV, 32, true, SPILL, STATS>;
+        default: return tabucol_warp_kernel<KV, 32, false, SPILL, STATS>;  // CSR, n <= 1024
     }
 }
-template <bool SPILL>
+template <bool SPILL, bool STATS>
 static KernT pick_kernel(int kv, int ch) {
     switch (kv) {
-        case 1: return pick_mode<1, SPILL>(ch);
-        case 2: return pick_mode<2, SPILL>(ch);
-        case 3: return pick_mode<3, SPILL>(ch);
-        case 4: return pick_mode<4, SPILL>(ch);
-        case 6: return pick_mode<6, SPILL>(ch);
-        case 8: return pick_mode<8, SPILL>(ch);
+        case 1: return pick_mode<1, SPILL, STATS>(ch);
+        case 2: return pick_mode<2, SPILL, STATS>(ch);
+        case 3: return pick_mode<3, SPILL, STATS>(ch);
+        case 4: return pick_mode<4, SPILL, STATS>(ch);
+        case 6: return pick_mode<6, SPILL, STATS>(ch);
+        case 8: return pick_mode<8, SPILL, STATS>(ch);
         default: return nullptr;
     }
 }
 
+static int upload_divtab(cudaStream_t st) {
+    static bool done[64] = {false};
+    int d = 0;
+    cudaGetDevice(&d);
+    if (done[d & 63]) return MCB_OK;
+    ulonglong2 tab[32];
+    for (int i = 0; i < 32; i++) {
+        const uint64_t o = 2 * (uint64_t)i + 1;
+        uint64_t x = o;  // Newton: inverse of o modulo 2^64
+        for (int r = 0; r < 6; r++) x *= 2 - o * x;
+        tab[i] = make_ulonglong2(x, ~0ull / o);
+    }
+    if (cudaMemcpyToSymbolAsync(g_divtab, tab, sizeof(tab), 0, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "tabucol_warp: divisor table upload failed");
+    done[d & 63] = true;
+    return MCB_OK;
+}
+
+#if TW_STATS_TU
+// the instrumented instantiations and the counters they write (this TU's
+// g_wstats / g_divtab)
+KernT tw_stats_kernel(int kv, int ch, bool spill) {
+    return spill ? pick_kernel<true, true>(kv, ch) : pick_kernel<false, true>(kv, ch);
+}
+int tw_stats_prepare(cudaStream_t st) {
+    unsigned long long z[40] = {0};
+    cudaMemcpyToSymbolAsync(g_wstats, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+    return upload_divtab(st);
+}
+int tabucol_warp_stats(unsigned long long *out) {
+    if (cudaMemcpyFromSymbol(out, g_wstats, sizeof(unsigned long long) * 40) != cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "warp stats unavailable");
+    return MCB_OK;
+}
+#else
+KernT tw_stats_kernel(int kv, int ch, bool spill);
+int tw_stats_prepare(cudaStream_t st);
+#endif
+
+#if !TW_STATS_TU
 struct WarpPlan {
     int kv, ch;  // ch = 0: CSR
     int warps, grid;
@@ -1119,40 +1171,20 @@ static bool tw_plan(int n, int k, int64_t p, WarpPlan *pl) {
 // Launches the warp kernel; individuals it cannot finish (table overflow) are
 // appended to ovf_list for the wide CTA kernel.  Returns MCB_OK, or -1 when
 // the shape is outside the envelope (caller uses the CTA kernels).
-static int upload_divtab(cudaStream_t st) {
-    static bool done[64] = {false};
-    int d = 0;
-    cudaGetDevice(&d);
-    if (done[d & 63]) return MCB_OK;
-    ulonglong2 tab[32];
-    for (int i = 0; i < 32; i++) {
-        const uint64_t o = 2 * (uint64_t)i + 1;
-        uint64_t x = o;  // Newton: inverse of o modulo 2^64
-        for (int r = 0; r < 6; r++) x *= 2 - o * x;
-        tab[i] = make_ulonglong2(x, ~0ull / o);
-    }
-    if (cudaMemcpyToSymbolAsync(g_divtab, tab, sizeof(tab), 0, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess)
-        return set_error(MCB_ERR_CUDA, "tabucol_warp: divisor table upload failed");
-    done[d & 63] = true;
-    return MCB_OK;
-}
-
 int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, int32_t *ovf_list,
                         int32_t *ovf_count, int32_t *err_flag, const int32_t *work_list, int64_t nwork,
                         bool spill, const int32_t *nwork_dev) {
     if (A.flags & (MCB_FLAG_FORCE_WIDE | MCB_FLAG_FORCE_GLOBAL | MCB_FLAG_PROFILE)) return -1;
-    if (A.flags & MCB_FLAG_WSTATS) {
-        // reset the counters of this launch
-        unsigned long long z[40] = {0};
-        cudaMemcpyToSymbolAsync(g_wstats, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
-    }
     WarpPlan pl;
     if (nwork < 0) nwork = A.p;
     if (!tw_plan((int)A.n, (int)A.k, nwork, &pl)) return -1;
-    KernT kern = spill ? pick_kernel<true>(pl.kv, pl.ch) : pick_kernel<false>(pl.kv, pl.ch);
+    const bool stats = (A.flags & MCB_FLAG_WSTATS) != 0;
+    KernT kern = stats ? tw_stats_kernel(pl.kv, pl.ch, spill)
+                       : (spill ? pick_kernel<true, false>(pl.kv, pl.ch) : pick_kernel<false, false>(pl.kv, pl.ch));
     if (!kern) return -1;
     if (int rc = upload_divtab(st)) return rc;
+    if (stats)
+        if (int rc = tw_stats_prepare(st)) return rc;  // resets this launch's counters
     const int n = (int)A.n, kp = 16 * pl.kv;
     const size_t smem = pl.bitset_bytes + (size_t)pl.warps * pl.warp_smem;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -1223,13 +1255,6 @@ int tabucol_warp_launch(const TabucolArgs &A, cudaStream_t st, int32_t *ctl32, i
 
 }  // namespace mcb
 
-namespace mcb {
-int tabucol_warp_stats(unsigned long long *out) {
-    if (cudaMemcpyFromSymbol(out, g_wstats, sizeof(unsigned long long) * 40) != cudaSuccess)
-        return set_error(MCB_ERR_CUDA, "warp stats unavailable");
-    return MCB_OK;
-}
-}  // namespace mcb
 
 namespace mcb {
 // Diagnostics: the table divisibility test against the 64-bit %, s in [1, 63]
@@ -1268,3 +1293,9 @@ int tabucol_warp_describe(int64_t n, int64_t k, int64_t p, char *buf, int len) {
     return MCB_OK;
 }
 }  // namespace mcb
+
+#endif  // !TW_STATS_TU
+
+#if TW_STATS_TU
+}  // namespace mcb
+#endif

@@ -1,6 +1,6 @@
 """Build A/B variants of the library: each variant is compiled with extra -D
 flags into ab/lib_<name>.so (load one with MCB_LIB=ab/lib_<name>.so).  Only
-the files named by VARIANT_FILES (default: tabucol_warp.cu) are recompiled;
+the files named by VARIANT_FILES (default: the warp kernel's two files) are recompiled;
 the others are linked from the in-tree build (python -m
 paper_2109_05948_b200._build first).
     python tools/build_variants.py name=-DFOO=1,-DBAR=0 other=..."""
@@ -22,7 +22,7 @@ def build(name, defs):
     ccbin = ["-ccbin", "/usr/bin/g++"] if os.path.exists("/usr/bin/g++") else []
     comp = [f for f in B.NVCC_FLAGS if f != "-shared"]
     objs = []
-    files = os.environ.get("VARIANT_FILES", "tabucol_warp.cu").split(",")
+    files = os.environ.get("VARIANT_FILES", "tabucol_warp.cu,tabucol_warp_stats.cu").split(",")
     for src in B.sources():
         base = os.path.basename(src)
         if base not in files:
