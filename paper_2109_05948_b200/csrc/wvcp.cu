@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
     int64_t *max_val = reinterpret_cast<int64_t *>(take((size_t)k * 8));
     int64_t *uniq_drop = reinterpret_cast<int64_t *>(take((size_t)k * 8));
     int32_t *cmax = reinterpret_cast<int32_t *>(take((size_t)k * 4));  // scratch
+    int32_t *mx32 = reinterpret_cast<int32_t *>(take((size_t)k * 4));  // max_val as int32 (the scan's copy)
     int32_t *lowq = reinterpret_cast<int32_t *>(take((size_t)2 * n * 4));  // (row, pos in R table)
     double *lowR = reinterpret_cast<double *>(take((size_t)n * 8));
     uint16_t *wc = P.ws_wc + blockIdx.x * P.ws_wc_stride;
@@ -221,6 +222,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
         if (lane == 0) {
             max_rank[c] = mr;
             max_val[c] = mv;
+            mx32[c] = (int32_t)mv;  // class maxima are vertex weights (< 2^31)
             uniq_drop[c] = ud;
         }
     };
@@ -353,16 +355,37 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                         const int wv = wgt[v];
                         int m = INT_MAX, cnt = 0;
                         if (!frozen) {
-                            // branch-free: the own colour gets INT_MAX (never below a
-                            // real candidate; k >= 2 leaves one)
-                            for (int c = 0; c < k; c++) {
-                                const int dc = (int)row[c] - gva;
-                                const int ds = max(0, wv - (int)max_val[c]) - rem;
-                                const int G = (c == a) ? INT_MAX : (ds << S) + Tt * dc;
-                                cnt = (G < m) ? 1 : cnt + (G == m);
-                                m = min(m, G);
+                            // G = (ds << S) + t dc = H_c + K with the row constant
+                            // K = -(rem << S) - t gva and H_c = (max(0, w_v - M_c) << S)
+                            // + t gamma_c: min / multiplicity over H (the own colour
+                            // excluded), four colours per shared load of the row
+                            int mh = INT_MAX;
+                            if (NARROW && (k & 3) == 0) {
+                                const uint32_t *row32 = reinterpret_cast<const uint32_t *>(row);
+                                for (int c4 = 0; c4 < k; c4 += 4) {
+                                    const uint32_t g4 = row32[c4 >> 2];
+#pragma unroll
+                                    for (int j = 0; j < 4; j++) {
+                                        const int c = c4 + j;
+                                        const int H = (max(0, wv - mx32[c]) << S) + Tt * (int)((g4 >> (8 * j)) & 0xFFu);
+                                        const int Hx = (c == a) ? INT_MAX : H;
+                                        cnt = (Hx < mh) ? 1 : cnt + (Hx == mh);
+                                        mh = min(mh, Hx);
+                                    }
+                                }
+                            } else {
+                                for (int c = 0; c < k; c++) {
+                                    const int H = (max(0, wv - mx32[c]) << S) + Tt * (int)row[c];
+                                    const int Hx = (c == a) ? INT_MAX : H;
+                                    cnt = (Hx < mh) ? 1 : cnt + (Hx == mh);
+                                    mh = min(mh, Hx);
+                                }
                             }
-                        } else if (conflicts <= gva) {
+                            m = (mh == INT_MAX) ? INT_MAX : mh - (rem << S) - Tt * gva;
+                        } else if (conflicts <= gva && rem + min(best - score, (long long)INT_MAX) > 0) {
+                            // (a frozen row needs ds = max(0, w - M_c) - rem < best - score:
+                            // impossible when rem + best - score <= 0, e.g. every row
+                            // whose move cannot lower a class maximum at a legal state)
                             // frozen vertex: only legal moves (dc == -conflicts, reachable
                             // only if conflicts <= gva) that beat the best legal score
                             const int need_dc = -(int)conflicts;
@@ -782,7 +805,7 @@ static size_t wv_smem(int n, int k, int gbytes) {
     auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
     return a16((size_t)n * k * gbytes) + a16((size_t)n * 4) + a16((size_t)n * 4) + a16((size_t)n * 2) +
            a16((size_t)n) + a16((size_t)n * 8) + a16((size_t)n * 2) + a16((size_t)k * 4) +
-           2 * a16((size_t)k * 8) + a16((size_t)k * 4) + a16((size_t)2 * n * 4) + a16((size_t)n * 8);
+           2 * a16((size_t)k * 8) + 2 * a16((size_t)k * 4) + a16((size_t)2 * n * 4) + a16((size_t)n * 8);
 }
 
 template <typename GT, bool STATS>
