@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
     int64_t *uniq_drop = reinterpret_cast<int64_t *>(take((size_t)k * 8));
     int32_t *cmax = reinterpret_cast<int32_t *>(take((size_t)k * 4));  // scratch
     int32_t *mx32 = reinterpret_cast<int32_t *>(take((size_t)k * 4));  // max_val as int32 (the scan's copy)
-    int32_t *lowq = reinterpret_cast<int32_t *>(take((size_t)2 * n * 4));  // (row, pos in R table)
+    int32_t *lowq = reinterpret_cast<int32_t *>(take((size_t)(2 * n + 64) * 4));  // 32-bit path: chunk minima / counts, walk queue
     double *lowR = reinterpret_cast<double *>(take((size_t)n * 8));
     uint16_t *wc = P.ws_wc + blockIdx.x * P.ws_wc_stride;
 
@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
     const bool prod = (P.flags & MCB_FLAG_PRODUCTION) != 0;
 
     __shared__ int s_maxw;
+    __shared__ int s_nlow, s_wts[NW], s_wts2[NW];  // 32-bit path: walk queue length, warp event sums
     if (tid == 0) s_maxw = 0;
     __syncthreads();
     {
@@ -309,6 +310,41 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
         if (ctl.conflicts == 0)
             for (int v = tid; v < n; v += NT) b_out[v] = assign[v];
 
+        // the move's bookkeeping (:212-231), one thread: tenure draw on the
+        // stream after the scan's `total` tie events, tabu stamp, score /
+        // conflicts, log
+        auto wv_apply_move = [&](int v, int a, int b, long long mv_ds, long long mv_dc, bool mv_tabu, long long it,
+                                 int total, long long score, long long conflicts) {
+            unsigned long long c = ctl.ctr;
+            uint32_t ll;
+            if (!prod) {
+                c += (unsigned long long)total;
+                ll = u64_below32(key, c, 10u);
+                c += 1;
+            } else {
+                ll = philox_below(key, c + 1, 10u);
+                c += 2;
+            }
+            const long long tt = (long long)ll + P.tt_base;
+            tabu_until[v] = (uint32_t)(it + tt + 1);
+            ctl.ctr = c;
+            ctl.mv_v = v;
+            ctl.mv_a = a;
+            ctl.mv_b = b;
+            ctl.score = score + mv_ds;
+            ctl.conflicts = conflicts + mv_dc;
+            const long long nl = ctl.nlog;
+            if (nl < P.log_cap) {
+                const size_t o = (size_t)ind * P.log_cap + nl;
+                P.log_v[o] = v;
+                P.log_iter[o] = it;
+                P.log_tt[o] = tt;
+                P.log_asp[o] = mv_tabu ? 1 : 0;
+                ctl.nlog = nl + 1;
+            }
+            if (b < 0) atomicExch(P.err_flag, 3);
+        };
+
         // ---------------- rounds (:156-258) ----------------
         for (int64_t rnd = 0; rnd < P.rounds; rnd++) {
             if (NARROW && ctl.ovf) break;  // read after a barrier: uniform
@@ -344,66 +380,239 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                 const bool fast32 =
                     gm.fast && (long long)(gm.t < 0 ? -gm.t : gm.t) * n + ((long long)s_maxw << gm.s) < (1ll << 30);
                 // pass 1: (min g, count) per vertex row over admissible candidates
-                if (fast32) {
+                const int nch = (n + 31) >> 5;
+                if (fast32 && nch <= 32) {
+                    // ================= exact 32-bit path (all arrays int) =================
                     const int S = gm.s, Tt = (int)gm.t;
-                    for (int v = tid; v < n; v += NT) {
-                        const int a = assign[v];
-                        const int rem = (wrk[v] == max_rank[a]) ? (int)uniq_drop[a] : 0;
-                        const GT *row = gamma + (size_t)v * k;
-                        const int gva = row[a];
-                        const bool frozen = (uint64_t)it < tabu_until[v];
-                        const int wv = wgt[v];
+                    int32_t *r32 = reinterpret_cast<int32_t *>(rmin);  // row minima (numerators)
+                    int32_t *c_min = lowq;                           // [32] chunk minima
+                    int32_t *c_cnt = lowq + 32;                      // [32] multiplicity at the chunk minimum
+                    int32_t *q = lowq + 64;                          // walk queue (row, entering minimum)
+                    // pass 1, rows warp-uniform (chunk = warp + NW j): every row's
+                    // (min G, #candidates at it), then the chunk's minimum and multiplicity
+                    for (int v0 = warp * 32; v0 < n; v0 += NT) {
+                        const int v = v0 + lane;
                         int m = INT_MAX, cnt = 0;
-                        if (!frozen) {
-                            // G = (ds << S) + t dc = H_c + K with the row constant
-                            // K = -(rem << S) - t gva and H_c = (max(0, w_v - M_c) << S)
-                            // + t gamma_c: min / multiplicity over H (the own colour
-                            // excluded), four colours per shared load of the row
-                            int mh = INT_MAX;
-                            if (NARROW && (k & 3) == 0) {
-                                const uint32_t *row32 = reinterpret_cast<const uint32_t *>(row);
-                                for (int c4 = 0; c4 < k; c4 += 4) {
-                                    const uint32_t g4 = row32[c4 >> 2];
-#pragma unroll
-                                    for (int j = 0; j < 4; j++) {
-                                        const int c = c4 + j;
-                                        const int H = (max(0, wv - mx32[c]) << S) + Tt * (int)((g4 >> (8 * j)) & 0xFFu);
+                        if (v < n) {
+                            const int a = assign[v];
+                            const int rem = (wrk[v] == max_rank[a]) ? (int)uniq_drop[a] : 0;
+                            const GT *row = gamma + (size_t)v * k;
+                            const int gva = row[a];
+                            const bool frozen = (uint64_t)it < tabu_until[v];
+                            const int wv = wgt[v];
+                            if (!frozen) {
+                                // G = (ds << S) + t dc = H_c + K with the row constant
+                                // K = -(rem << S) - t gva and H_c = (max(0, w_v - M_c) << S)
+                                // + t gamma_c: min / multiplicity over H (the own colour
+                                // excluded), four colours per shared load of the row
+                                int mh = INT_MAX;
+                                if (NARROW && (k & 3) == 0) {
+                                    const uint32_t *row32 = reinterpret_cast<const uint32_t *>(row);
+                                    for (int c4 = 0; c4 < k; c4 += 4) {
+                                        const uint32_t g4 = row32[c4 >> 2];
+    #pragma unroll
+                                        for (int j = 0; j < 4; j++) {
+                                            const int c = c4 + j;
+                                            const int H = (max(0, wv - mx32[c]) << S) + Tt * (int)((g4 >> (8 * j)) & 0xFFu);
+                                            const int Hx = (c == a) ? INT_MAX : H;
+                                            cnt = (Hx < mh) ? 1 : cnt + (Hx == mh);
+                                            mh = min(mh, Hx);
+                                        }
+                                    }
+                                } else {
+                                    for (int c = 0; c < k; c++) {
+                                        const int H = (max(0, wv - mx32[c]) << S) + Tt * (int)row[c];
                                         const int Hx = (c == a) ? INT_MAX : H;
                                         cnt = (Hx < mh) ? 1 : cnt + (Hx == mh);
                                         mh = min(mh, Hx);
                                     }
                                 }
-                            } else {
+                                m = (mh == INT_MAX) ? INT_MAX : mh - (rem << S) - Tt * gva;
+                            } else if (conflicts <= gva && rem + min(best - score, (long long)INT_MAX) > 0) {
+                                // (a frozen row needs ds = max(0, w - M_c) - rem < best - score:
+                                // impossible when rem + best - score <= 0, e.g. every row
+                                // whose move cannot lower a class maximum at a legal state)
+                                // frozen vertex: only legal moves (dc == -conflicts, reachable
+                                // only if conflicts <= gva) that beat the best legal score
+                                const int need_dc = -(int)conflicts;
+                                const long long room = best - score;  // ds < room
+                                const int dsmax = room > INT_MAX ? INT_MAX : (room < INT_MIN ? INT_MIN : (int)room);
                                 for (int c = 0; c < k; c++) {
-                                    const int H = (max(0, wv - mx32[c]) << S) + Tt * (int)row[c];
-                                    const int Hx = (c == a) ? INT_MAX : H;
-                                    cnt = (Hx < mh) ? 1 : cnt + (Hx == mh);
-                                    mh = min(mh, Hx);
+                                    const int dc = (int)row[c] - gva;
+                                    const int ds = max(0, wv - (int)max_val[c]) - rem;
+                                    const bool ok = c != a && dc == need_dc && ds < dsmax;
+                                    const int G = ok ? (ds << S) + Tt * dc : INT_MAX;
+                                    cnt = (G < m) ? 1 : cnt + (G == m && ok);
+                                    m = min(m, G);
                                 }
                             }
-                            m = (mh == INT_MAX) ? INT_MAX : mh - (rem << S) - Tt * gva;
-                        } else if (conflicts <= gva && rem + min(best - score, (long long)INT_MAX) > 0) {
-                            // (a frozen row needs ds = max(0, w - M_c) - rem < best - score:
-                            // impossible when rem + best - score <= 0, e.g. every row
-                            // whose move cannot lower a class maximum at a legal state)
-                            // frozen vertex: only legal moves (dc == -conflicts, reachable
-                            // only if conflicts <= gva) that beat the best legal score
-                            const int need_dc = -(int)conflicts;
-                            const long long room = best - score;  // ds < room
-                            const int dsmax = room > INT_MAX ? INT_MAX : (room < INT_MIN ? INT_MIN : (int)room);
-                            for (int c = 0; c < k; c++) {
-                                const int dc = (int)row[c] - gva;
-                                const int ds = max(0, wv - (int)max_val[c]) - rem;
-                                const bool ok = c != a && dc == need_dc && ds < dsmax;
-                                const int G = ok ? (ds << S) + Tt * dc : INT_MAX;
-                                cnt = (G < m) ? 1 : cnt + (G == m && ok);
-                                m = min(m, G);
+                            r32[v] = m;
+                            rcnt[v] = (uint16_t)(m == INT_MAX ? 0 : cnt);
+                        }
+                        const int cm = __reduce_min_sync(FULL, m);
+                        const int cc = __reduce_add_sync(FULL, (m == cm && m != INT_MAX) ? cnt : 0);
+                        if (lane == 0) {
+                            c_min[v0 >> 5] = cm;
+                            c_cnt[v0 >> 5] = cc;
+                        }
+                    }
+                    if (tid == 0) s_nlow = 0;
+                    __syncthreads();
+                    WVPH(1);
+                    // prefix minimum over the rows in vertex order: every chunk's entering
+                    // minimum from one scan over the chunk minima; only chunks reaching
+                    // the running minimum hold tie events or rows that lower it
+                    const int cmv = lane < nch ? c_min[lane] : INT_MAX;
+                    int cin_all = cmv;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int t2 = __shfl_up_sync(FULL, cin_all, o);
+                        if (lane >= o) cin_all = min(cin_all, t2);
+                    }
+                    const int D = __shfl_sync(FULL, cin_all, 31);
+                    int cex = __shfl_up_sync(FULL, cin_all, 1);
+                    if (lane == 0) cex = INT_MAX;
+                    int tsum = 0;
+                    if (!prod && D != INT_MAX) {
+                        for (int cb = warp; cb < nch; cb += NW) {
+                            const int cin = __shfl_sync(FULL, cex, cb);
+                            if (__shfl_sync(FULL, cmv, cb) > cin) continue;  // no row at or below it
+                            const int v = cb * 32 + lane;
+                            const int x = v < n ? r32[v] : INT_MAX;
+                            const int nq = v < n ? rcnt[v] : 0;
+                            int incl = x;
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const int t2 = __shfl_up_sync(FULL, incl, o);
+                                if (lane >= o) incl = min(incl, t2);
+                            }
+                            int excl = __shfl_up_sync(FULL, incl, 1);
+                            if (lane == 0) excl = INT_MAX;
+                            const int RM = min(cin, excl);
+                            if (x != INT_MAX) {
+                                if (x == RM) {
+                                    tsum += nq;
+                                } else if (x < RM) {
+                                    const int pos = atomicAdd(&s_nlow, 1);
+                                    q[2 * pos] = v;
+                                    q[2 * pos + 1] = RM;
+                                }
                             }
                         }
-                        rmin[v] = (m == INT_MAX) ? INF : (double)m;
-                        rcnt[v] = (uint16_t)(m == INT_MAX ? 0 : cnt);
                     }
-                } else if (gm.fast) {
+                    {
+                        const int wts = __reduce_add_sync(FULL, tsum);
+                        if (lane == 0) s_wts[warp] = wts;
+                    }
+                    __syncthreads();
+                    WVPH(2);
+                    // walks of the rows that lower the running minimum (their tie
+                    // events in colour order, :194-210), spread over the warps
+                    {
+                        int tw = 0;
+                        const int nlow = s_nlow;
+                        for (int i = warp; i < nlow; i += NW) {
+                            const int wvx = q[2 * i], R = q[2 * i + 1];
+                            const int a = assign[wvx];
+                            const int rem = (wrk[wvx] == max_rank[a]) ? (int)uniq_drop[a] : 0;
+                            const GT *row = gamma + (size_t)wvx * k;
+                            const int gva = row[a];
+                            const bool frozen = (uint64_t)it < tabu_until[wvx];
+                            const int wv = wgt[wvx];
+                            int cr = R;
+                            for (int c0 = 0; c0 < k; c0 += 32) {
+                                const int c = c0 + lane;
+                                int G = INT_MAX;
+                                if (c < k && c != a) {
+                                    const int dc = (int)row[c] - gva;
+                                    const int ds = max(0, wv - mx32[c]) - rem;
+                                    if (!(frozen && (conflicts + dc != 0 || score + ds >= best))) G = (ds << S) + Tt * dc;
+                                }
+                                int inc2 = G;
+#pragma unroll
+                                for (int o = 1; o < 32; o <<= 1) {
+                                    const int t2 = __shfl_up_sync(FULL, inc2, o);
+                                    if (lane >= o) inc2 = min(inc2, t2);
+                                }
+                                int ex2 = __shfl_up_sync(FULL, inc2, 1);
+                                if (lane == 0) ex2 = INT_MAX;
+                                if (G != INT_MAX && G == min(cr, ex2)) tw++;
+                                cr = min(cr, __shfl_sync(FULL, inc2, 31));
+                            }
+                        }
+                        const int wtw = __reduce_add_sync(FULL, tw);
+                        if (lane == 0) s_wts2[warp] = wtw;
+                    }
+                    __syncthreads();
+                    WVPH(3);
+                    if (warp == 0) {
+                        const int total = __reduce_add_sync(FULL, lane < NW ? s_wts[lane] + s_wts2[lane] : 0);
+                        int mv_v = -1;
+                        if (D != INT_MAX) {
+                            const int cc = (lane < nch && cmv == D) ? c_cnt[lane] : 0;
+                            const int T = __reduce_add_sync(FULL, cc);
+                            const unsigned long long ctr = ctl.ctr;
+                            int sstar = 1;
+                            if (T > 1) {
+                                if (!prod) {
+                                    const unsigned long long c0 = ctr + (unsigned long long)(total - (T - 1));
+                                    int smax = 1;
+                                    for (int s2 = 2 + lane; s2 <= T; s2 += 32)
+                                        if (mod_is_zero(stream_value(key, c0 + (unsigned long long)(s2 - 2)), (uint32_t)s2))
+                                            smax = s2;
+                                    sstar = __reduce_max_sync(FULL, smax);
+                                } else {
+                                    sstar = 1 + (int)philox_below(key, ctr, (uint32_t)T);
+                                }
+                            }
+                            // the chunk, then the row holding the sstar-th D-candidate
+                            const int ci = warp_incl_sum(cc, lane);
+                            const int ch = __ffs(__ballot_sync(FULL, ci >= sstar)) - 1;
+                            const int before = __shfl_sync(FULL, ci - cc, ch);
+                            const int vv = ch * 32 + lane;
+                            const int c1 = (vv < n && r32[vv] == D) ? rcnt[vv] : 0;
+                            const int incl = warp_incl_sum(c1, lane);
+                            const int src = __ffs(__ballot_sync(FULL, before + incl >= sstar)) - 1;
+                            const int v = ch * 32 + src;
+                            const int need = sstar - before - __shfl_sync(FULL, incl - c1, src);
+                            // within the row: the need-th colour with G == D
+                            const int a = assign[v];
+                            const int rem = (wrk[v] == max_rank[a]) ? (int)uniq_drop[a] : 0;
+                            const GT *rw = gamma + (size_t)v * k;
+                            const int gva = rw[a];
+                            const bool frozen = (uint64_t)it < tabu_until[v];
+                            const int wv = wgt[v];
+                            int cum = 0, b = -1, bds = 0, bdc = 0;
+                            for (int c0 = 0; c0 < k && b < 0; c0 += 32) {
+                                const int c = c0 + lane;
+                                bool hit = false;
+                                int ds = 0, dc = 0;
+                                if (c < k && c != a) {
+                                    dc = (int)rw[c] - gva;
+                                    ds = max(0, wv - mx32[c]) - rem;
+                                    if (!(frozen && (conflicts + dc != 0 || score + ds >= best)))
+                                        hit = (ds << S) + Tt * dc == D;
+                                }
+                                const unsigned hm = __ballot_sync(FULL, hit);
+                                const int hc = __popc(hm);
+                                if (cum + hc >= need) {
+                                    unsigned mm = hm;
+                                    for (int q2 = 1; q2 < need - cum; q2++) mm &= mm - 1u;
+                                    const int sl = __ffs(mm) - 1;
+                                    b = c0 + sl;
+                                    bds = __shfl_sync(FULL, ds, sl);
+                                    bdc = __shfl_sync(FULL, dc, sl);
+                                }
+                                cum += hc;
+                            }
+                            mv_v = v;
+                            if (lane == 0) wv_apply_move(v, a, b, bds, bdc, frozen, it, total, score, conflicts);
+                        }
+                        if (lane == 0) ctl.has_move = (mv_v >= 0);
+                    }
+                } else {
+                // pass 1: (min g, count) per vertex row over admissible candidates
+                if (gm.fast) {
                     // exact integer numerators (see gv_mode)
                     for (int v = tid; v < n; v += NT) {
                         const int a = assign[v];
@@ -672,38 +881,10 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                         mv_ds = bds;
                         mv_dc = bdc;
                         mv_tabu = frozen;
-                        if (lane == 0) {
-                            unsigned long long c = ctr;
-                            uint32_t ll;
-                            if (!prod) {
-                                c += (unsigned long long)total;
-                                ll = u64_below32(key, c, 10u);
-                                c += 1;
-                            } else {
-                                ll = philox_below(key, c + 1, 10u);
-                                c += 2;
-                            }
-                            const long long tt = (long long)ll + P.tt_base;
-                            tabu_until[v] = (uint32_t)(it + tt + 1);
-                            ctl.ctr = c;
-                            ctl.mv_v = v;
-                            ctl.mv_a = a;
-                            ctl.mv_b = b;
-                            ctl.score = score + mv_ds;
-                            ctl.conflicts = conflicts + mv_dc;
-                            const long long nl = ctl.nlog;
-                            if (nl < P.log_cap) {
-                                const size_t o = (size_t)ind * P.log_cap + nl;
-                                P.log_v[o] = v;
-                                P.log_iter[o] = it;
-                                P.log_tt[o] = tt;
-                                P.log_asp[o] = mv_tabu ? 1 : 0;
-                                ctl.nlog = nl + 1;
-                            }
-                            if (b < 0) atomicExch(P.err_flag, 3);
-                        }
+                        if (lane == 0) wv_apply_move(v, a, b, mv_ds, mv_dc, mv_tabu, it, total, score, conflicts);
                     }
                     if (lane == 0) ctl.has_move = (mv_v >= 0);
+                }
                 }
                 __syncthreads();
                 WVPH(4);
@@ -805,7 +986,7 @@ static size_t wv_smem(int n, int k, int gbytes) {
     auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
     return a16((size_t)n * k * gbytes) + a16((size_t)n * 4) + a16((size_t)n * 4) + a16((size_t)n * 2) +
            a16((size_t)n) + a16((size_t)n * 8) + a16((size_t)n * 2) + a16((size_t)k * 4) +
-           2 * a16((size_t)k * 8) + 2 * a16((size_t)k * 4) + a16((size_t)2 * n * 4) + a16((size_t)n * 8);
+           2 * a16((size_t)k * 8) + 2 * a16((size_t)k * 4) + a16((size_t)(2 * n + 64) * 4) + a16((size_t)n * 8);
 }
 
 template <typename GT, bool STATS>
