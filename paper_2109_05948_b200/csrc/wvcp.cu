@@ -85,7 +85,7 @@ struct WvCtrl {
     long long it, score, conflicts, best, nlog, diag;
     unsigned long long ctr;
     double phi;
-    int work, mv_v, mv_a, mv_b, has_move, ovf;
+    int work, mv_v, mv_a, mv_b, has_move, ovf, copy, deg;
     long long red[WV_NT / 32];
     long long red2[WV_NT / 32];
 };
@@ -172,6 +172,8 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
     int32_t *cmax = reinterpret_cast<int32_t *>(take((size_t)k * 4));  // scratch
     int32_t *mx32 = reinterpret_cast<int32_t *>(take((size_t)k * 4));  // max_val as int32 (the scan's copy)
     int32_t *lowq = reinterpret_cast<int32_t *>(take((size_t)(2 * n + 64) * 4));  // 32-bit path: chunk minima / counts, walk queue
+    int32_t *ip32 = reinterpret_cast<int32_t *>(take((size_t)(n + 1) * 4));      // CSR row offsets
+    int32_t *nbuf = reinterpret_cast<int32_t *>(take((size_t)n * 4));            // the moved vertex's neighbours
     double *lowR = reinterpret_cast<double *>(take((size_t)n * 8));
     uint16_t *wc = P.ws_wc + blockIdx.x * P.ws_wc_stride;
 
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
     __syncthreads();
     {
         int mw = 0;
+        for (int v = tid; v <= n; v += NT) ip32[v] = (int32_t)P.indptr[v];  // 2m < 2^31 (host-checked)
         for (int v = tid; v < n; v += NT) {
             wgt[v] = (int32_t)P.weights[v];
             wrk[v] = (uint16_t)P.wranks[v];
@@ -333,6 +336,9 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
             ctl.mv_b = b;
             ctl.score = score + mv_ds;
             ctl.conflicts = conflicts + mv_dc;
+            // best legal score (:233-236); the colouring is copied after the move
+            ctl.copy = (ctl.conflicts == 0 && ctl.score < ctl.best);
+            if (ctl.copy) ctl.best = ctl.score;
             const long long nl = ctl.nlog;
             if (nl < P.log_cap) {
                 const size_t o = (size_t)ind * P.log_cap + nl;
@@ -343,6 +349,14 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                 ctl.nlog = nl + 1;
             }
             if (b < 0) atomicExch(P.err_flag, 3);
+        };
+
+        // warp 0, as soon as the moving vertex is known: its neighbour list into
+        // shared memory (the L2 round trip overlaps the colour locate)
+        auto fetch_nbrs = [&](int v) {
+            const int e0 = ip32[v], d = ip32[v + 1] - e0;
+            for (int i = lane; i < d; i += 32) nbuf[i] = __ldg(P.indices + e0 + i);
+            if (lane == 0) ctl.deg = d;
         };
 
         // ---------------- rounds (:156-258) ----------------
@@ -574,6 +588,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                             const int incl = warp_incl_sum(c1, lane);
                             const int src = __ffs(__ballot_sync(FULL, before + incl >= sstar)) - 1;
                             const int v = ch * 32 + src;
+                            fetch_nbrs(v);
                             const int need = sstar - before - __shfl_sync(FULL, incl - c1, src);
                             // within the row: the need-th colour with G == D
                             const int a = assign[v];
@@ -845,6 +860,7 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                         }
                         // within the row: the need-th colour with g == D
                         const int v = row;
+                        fetch_nbrs(v);
                         const int a = assign[v];
                         const long long rem = (wrk[v] == max_rank[a]) ? uniq_drop[a] : 0;
                         const GT *rw = gamma + (size_t)v * k;
@@ -888,40 +904,31 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                 }
                 __syncthreads();
                 WVPH(4);
-                if (ctl.has_move) {
-                    const int v = ctl.mv_v, a = ctl.mv_a, b = ctl.mv_b;
-                    // gamma over N(v) (:218-221)
-                    for (int64_t idx = P.indptr[v] + tid; idx < P.indptr[v + 1]; idx += NT) {
-                        const int u = __ldg(P.indices + idx);
+                const bool moved = ctl.has_move;
+                if (moved) {
+                    // gamma over N(v) (:218-221) by all threads; warp 0 / warp 1 move v
+                    // between the weight-rank counts of classes a / b and refresh them
+                    const int v = ctl.mv_v, a = ctl.mv_a, b = ctl.mv_b, deg = ctl.deg;
+                    for (int i = tid; i < deg; i += NT) {
+                        const int u = nbuf[i];
                         gamma[(size_t)u * k + a]--;
                         const GT old = gamma[(size_t)u * k + b];
                         if (NARROW && old == (GT)0xFF) ctl.ovf = 1;
                         gamma[(size_t)u * k + b] = (GT)(old + 1);
                     }
-                    if (tid == 0) {
-                        const int r = wrk[v];
-                        wc[(size_t)a * nranks + r]--;
-                        wc[(size_t)b * nranks + r]++;
-                        assign[v] = (uint8_t)b;
+                    if (warp <= 1) {
+                        const int c = warp == 0 ? a : b;
+                        if (lane == 0) wc[(size_t)c * nranks + wrk[v]] += (warp == 0) ? (uint16_t)0xFFFF : (uint16_t)1;
+                        __syncwarp();
+                        refresh_class(c);
+                        if (warp == 1 && lane == 0) assign[v] = (uint8_t)b;
                     }
-                    __syncthreads();
-                    WVPH(5);
-                    if (warp == 0) refresh_class(a);
-                    else if (warp == 1) refresh_class(b);
-                    __syncthreads();
-                    WVPH(6);
-                    if (tid == 0 && ctl.conflicts == 0 && ctl.score < ctl.best) {
-                        ctl.best = ctl.score;
-                        ctl.red[0] = 1;  // copy flag
-                    } else if (tid == 0) {
-                        ctl.red[0] = 0;
-                    }
-                    __syncthreads();
-                    WVPH(7);
-                    if (ctl.red[0])
-                        for (int u = tid; u < n; u += NT) b_out[u] = assign[u];
                 }
                 if (tid == 0) ctl.it = it + 1;
+                __syncthreads();
+                WVPH(5);
+                if (moved && ctl.copy)
+                    for (int u = tid; u < n; u += NT) b_out[u] = assign[u];
                 const long long itn = it + 1;
                 if (diagf && itn % 1024 == 0) {  // scratch check (:245-249)
                     for (int c = tid; c < k; c += NT) cmax[c] = -1;
@@ -948,7 +955,8 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                         if (s != ctl.score || f != ctl.conflicts) ctl.diag += 1;
                     }
                 }
-                __syncthreads();
+                // (no barrier here: the next iteration's first writes are ordered
+                // behind its pass-1 barrier, every read of this one's results is done)
                 WVPH(8);
                 if (NARROW && ctl.ovf) break;
             }
@@ -986,7 +994,8 @@ static size_t wv_smem(int n, int k, int gbytes) {
     auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
     return a16((size_t)n * k * gbytes) + a16((size_t)n * 4) + a16((size_t)n * 4) + a16((size_t)n * 2) +
            a16((size_t)n) + a16((size_t)n * 8) + a16((size_t)n * 2) + a16((size_t)k * 4) +
-           2 * a16((size_t)k * 8) + 2 * a16((size_t)k * 4) + a16((size_t)(2 * n + 64) * 4) + a16((size_t)n * 8);
+           2 * a16((size_t)k * 8) + 2 * a16((size_t)k * 4) + a16((size_t)(2 * n + 64) * 4) + a16((size_t)n * 8) +
+           a16((size_t)(n + 1) * 4) + a16((size_t)n * 4);
 }
 
 template <typename GT, bool STATS>
