@@ -307,6 +307,12 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
         }
         if (__any_sync(FULLM, rangeerr) && lane == 0) atomicExch(P.err_flag, 1);
         bad = __any_sync(FULLM, bad);
+        if constexpr (!SPILL) {
+            // tenures of U{0..9} + 0.6 conflicts beyond the register ring's 1024
+            // entries from the start (e.g. C3 from random colourings: ~1800):
+            // straight to the SPILL pass instead of overflowing after ~1000 moves
+            if (9 + (6 * conflicts) / 10 > 32 * KE) bad = true;
+        }
         __syncwarp();
 
         long long it = 0, nlog = 0, sum_c = 0, sum_deg = 0, diag = 0;
