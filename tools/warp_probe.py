@@ -32,6 +32,7 @@ ap.add_argument("--philox", action="store_true")
 ap.add_argument("--var", action="append", default=[])
 ap.add_argument("--stats", action="store_true")
 ap.add_argument("--modcheck", type=int, default=0)
+ap.add_argument("--warm", type=int, default=0, help="start from the end colourings of a WARM-iteration run")
 a = ap.parse_args()
 
 if a.modcheck:
@@ -43,6 +44,11 @@ g = rand_graph(1, a.n, a.p)
 A = random_col_assigns(a.n, a.k, a.pop, 1)
 dg = Dv.DeviceGraph(g, "cuda")
 keys = Dv.keys_to_tensor(stream_keys(1, TAG_LS, 0, a.pop), "cuda")
+if a.warm:
+    a_w = torch.from_numpy(A.copy()).cuda()
+    Dv.tabucol_batch(dg, a_w, a.k, keys, a.warm)
+    A = a_w.cpu().numpy()
+    keys = Dv.keys_to_tensor(stream_keys(1, TAG_LS, 1, a.pop), "cuda")
 flags = (N.FLAG_PRODUCTION if a.philox else 0) | (N.FLAG_WSTATS if a.stats else 0)
 variants = a.var or ["default:"]
 ref = None
