@@ -376,8 +376,11 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # communicator init lines (NVLS / NVLink use) visible, on stderr: rank 0's
+        # stdout carries exactly one JSON line
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     wl = args.workload
     kind, seed, n, pe, wmax, k, D, depth, rounds = WORKLOADS[wl]
