@@ -86,6 +86,10 @@ struct WvCtrl {
     unsigned long long ctr;
     double phi;
     int work, mv_v, mv_a, mv_b, has_move, ovf, copy, deg;
+    // 32-bit path's row caches: 0 = none valid, 1 = valid before the move
+    // (mv_v, mv_a, mv_b; class maxima of mv_a / mv_b before it: ma_old, mb_old),
+    // 2 = valid, no move since
+    int inc, ma_old, mb_old;
     long long red[WV_NT / 32];
     long long red2[WV_NT / 32];
 };
@@ -143,7 +147,7 @@ __device__ __forceinline__ double shfl_d(double x, int src) {
 __device__ unsigned long long g_wvstats[16];
 
 template <typename GT, bool STATS>
-__global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
+__global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
     constexpr bool NARROW = sizeof(GT) == 1;
     constexpr int NT = WV_NT, NW = NT / 32;
     constexpr unsigned FULL = 0xffffffffu;
@@ -334,6 +338,8 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
             ctl.mv_v = v;
             ctl.mv_a = a;
             ctl.mv_b = b;
+            ctl.ma_old = mx32[a];  // class maxima before the move (refreshed in the update phase)
+            ctl.mb_old = mx32[b];
             ctl.score = score + mv_ds;
             ctl.conflicts = conflicts + mv_dc;
             // best legal score (:233-236); the colouring is copied after the move
@@ -367,6 +373,11 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                 phis[P.rounds] = ctl.phi;
             }
             for (int v = tid; v < n; v += NT) tabu_until[v] = 0;
+            {
+                uint32_t *nbits = reinterpret_cast<uint32_t *>(lowR) + ((size_t)n + 1) / 2;  // after the u16 counts
+                for (int i = tid; i < 2 * ((n + 31) / 32); i += NT) nbits[i] = 0u;
+                if (tid == 0) ctl.inc = 0;
+            }
             __syncthreads();
             // phase counters live in shared memory (thread 0 only): no registers
             // held across the iteration when the flag is off
@@ -402,6 +413,12 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     int32_t *c_min = lowq;                           // [32] chunk minima
                     int32_t *c_cnt = lowq + 32;                      // [32] multiplicity at the chunk minimum
                     int32_t *q = lowq + 64;                          // walk queue (row, entering minimum)
+                    int32_t *hc_min = r32 + n;                       // row caches (rmin's second half)
+                    uint16_t *hc_cnt = reinterpret_cast<uint16_t *>(lowR);
+                    const uint32_t *nbr_bits = reinterpret_cast<const uint32_t *>(lowR) + ((size_t)n + 1) / 2 +
+                                               (size_t)((it - 1) & 1) * ((n + 31) / 32);
+                    const int inc = ctl.inc, mvv = ctl.mv_v, mva = ctl.mv_a, mvb = ctl.mv_b;
+                    const int mao = ctl.ma_old, mbo = ctl.mb_old;
                     // pass 1, rows warp-uniform (chunk = warp + NW j): every row's
                     // (min G, #candidates at it), then the chunk's minimum and multiplicity
                     for (int v0 = warp * 32; v0 < n; v0 += NT) {
@@ -418,9 +435,46 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                                 // G = (ds << S) + t dc = H_c + K with the row constant
                                 // K = -(rem << S) - t gva and H_c = (max(0, w_v - M_c) << S)
                                 // + t gamma_c: min / multiplicity over H (the own colour
-                                // excluded), four colours per shared load of the row
+                                // excluded), four colours per shared load of the row.
+                                // The (min, multiplicity) over H is cached per row: after a
+                                // move v*: a* -> b* only columns a* and b* change for any row
+                                // (gamma of v*'s neighbours, the two class maxima), so a
+                                // valid cache is updated with those two columns -- old
+                                // contributions out, new ones in -- and the row is rescanned
+                                // when its minimum group empties, after it was frozen, for
+                                // v* itself and at round start (ctl.inc == 0)
                                 int mh = INT_MAX;
-                                if (NARROW && (k & 3) == 0) {
+                                bool full = true;
+                                if (inc != 0 && hc_cnt[v] != 0xFFFFu && !(inc == 1 && v == mvv)) {
+                                    mh = hc_min[v];
+                                    cnt = hc_cnt[v];
+                                    full = false;
+                                    if (inc == 1) {
+                                        const int nb = (int)((nbr_bits[v >> 5] >> (v & 31)) & 1u);
+                                        int hn[2], nx = 0;
+#pragma unroll
+                                        for (int side = 0; side < 2; side++) {
+                                            const int x = side ? mvb : mva;
+                                            if (x == a) continue;  // the own colour is not a candidate
+                                            const int gnew = (int)row[x];
+                                            const int gold = gnew + (side ? -nb : nb);  // a*: -1, b*: +1 on N(v*)
+                                            const int hold = (max(0, wv - (side ? mbo : mao)) << S) + Tt * gold;
+                                            if (hold == mh) cnt--;
+                                            hn[nx++] = (max(0, wv - mx32[x]) << S) + Tt * gnew;
+                                        }
+                                        if (cnt == 0) {
+                                            full = true;  // the minimum group emptied: rescan
+                                            mh = INT_MAX;
+                                        } else {
+                                            for (int i2 = 0; i2 < nx; i2++) {
+                                                cnt = (hn[i2] < mh) ? 1 : cnt + (hn[i2] == mh);
+                                                mh = min(mh, hn[i2]);
+                                            }
+                                        }
+                                    }
+                                }
+                                if (!full) {
+                                } else if (NARROW && (k & 3) == 0) {
                                     const uint32_t *row32 = reinterpret_cast<const uint32_t *>(row);
                                     for (int c4 = 0; c4 < k; c4 += 4) {
                                         const uint32_t g4 = row32[c4 >> 2];
@@ -441,8 +495,11 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                                         mh = min(mh, Hx);
                                     }
                                 }
+                                hc_min[v] = mh;
+                                hc_cnt[v] = (uint16_t)cnt;
                                 m = (mh == INT_MAX) ? INT_MAX : mh - (rem << S) - Tt * gva;
-                            } else if (conflicts <= gva && rem + min(best - score, (long long)INT_MAX) > 0) {
+                            } else if ((hc_cnt[v] = 0xFFFFu, conflicts <= gva) &&
+                                       rem + min(best - score, (long long)INT_MAX) > 0) {
                                 // (a frozen row needs ds = max(0, w - M_c) - rem < best - score:
                                 // impossible when rem + best - score <= 0, e.g. every row
                                 // whose move cannot lower a class maximum at a legal state)
@@ -522,6 +579,11 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     WVPH(2);
                     // walks of the rows that lower the running minimum (their tie
                     // events in colour order, :194-210), spread over the warps
+                    {   // the neighbour flags pass 1 read are dead: clear them for the move after next
+                        uint32_t *nb_clear = reinterpret_cast<uint32_t *>(lowR) + ((size_t)n + 1) / 2 +
+                                             (size_t)((it - 1) & 1) * ((n + 31) / 32);
+                        for (int i = tid; i < (n + 31) / 32; i += NT) nb_clear[i] = 0u;
+                    }
                     {
                         int tw = 0;
                         const int nlow = s_nlow;
@@ -909,8 +971,11 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                     // gamma over N(v) (:218-221) by all threads; warp 0 / warp 1 move v
                     // between the weight-rank counts of classes a / b and refresh them
                     const int v = ctl.mv_v, a = ctl.mv_a, b = ctl.mv_b, deg = ctl.deg;
+                    uint32_t *nbw = reinterpret_cast<uint32_t *>(lowR) + ((size_t)n + 1) / 2 +
+                                    (size_t)(it & 1) * ((n + 31) / 32);
                     for (int i = tid; i < deg; i += NT) {
                         const int u = nbuf[i];
+                        atomicOr(&nbw[u >> 5], 1u << (u & 31));  // the 32-bit path's row caches read this
                         gamma[(size_t)u * k + a]--;
                         const GT old = gamma[(size_t)u * k + b];
                         if (NARROW && old == (GT)0xFF) ctl.ovf = 1;
@@ -924,7 +989,10 @@ __global__ void __launch_bounds__(WV_NT) wvcp_kernel(WvParams P) {
                         if (warp == 1 && lane == 0) assign[v] = (uint8_t)b;
                     }
                 }
-                if (tid == 0) ctl.it = it + 1;
+                if (tid == 0) {
+                    ctl.it = it + 1;
+                    ctl.inc = (fast32 && nch <= 32) ? (moved ? 1 : 2) : 0;  // row caches valid after a 32-bit pass 1
+                }
                 __syncthreads();
                 WVPH(5);
                 if (moved && ctl.copy)
