@@ -423,28 +423,28 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                     // (min G, #candidates at it), then the chunk's minimum and multiplicity
                     for (int v0 = warp * 32; v0 < n; v0 += NT) {
                         const int v = v0 + lane;
-                        int m = INT_MAX, cnt = 0;
+                        int m = INT_MAX, cnt = 0, mh = INT_MAX;
+                        int a = 0, rem = 0, gva = 0, wv = 0;
+                        bool full = false;
                         if (v < n) {
-                            const int a = assign[v];
-                            const int rem = (wrk[v] == max_rank[a]) ? (int)uniq_drop[a] : 0;
+                            a = assign[v];
+                            rem = (wrk[v] == max_rank[a]) ? (int)uniq_drop[a] : 0;
                             const GT *row = gamma + (size_t)v * k;
-                            const int gva = row[a];
+                            gva = row[a];
                             const bool frozen = (uint64_t)it < tabu_until[v];
-                            const int wv = wgt[v];
+                            wv = wgt[v];
                             if (!frozen) {
                                 // G = (ds << S) + t dc = H_c + K with the row constant
                                 // K = -(rem << S) - t gva and H_c = (max(0, w_v - M_c) << S)
-                                // + t gamma_c: min / multiplicity over H (the own colour
-                                // excluded), four colours per shared load of the row.
-                                // The (min, multiplicity) over H is cached per row: after a
-                                // move v*: a* -> b* only columns a* and b* change for any row
-                                // (gamma of v*'s neighbours, the two class maxima), so a
-                                // valid cache is updated with those two columns -- old
-                                // contributions out, new ones in -- and the row is rescanned
-                                // when its minimum group empties, after it was frozen, for
-                                // v* itself and at round start (ctl.inc == 0)
-                                int mh = INT_MAX;
-                                bool full = true;
+                                // + t gamma_c; the (min, multiplicity) over H (own colour
+                                // excluded) is cached per row: after a move v*: a* -> b*
+                                // only columns a* and b* change for any row (gamma of v*'s
+                                // neighbours, the two class maxima), so a valid cache is
+                                // updated with those two columns -- old contributions out,
+                                // new ones in -- and the row is rescanned (below, by the
+                                // whole warp) when its minimum group empties, after it was
+                                // frozen, for v* itself and at round start (ctl.inc == 0)
+                                full = true;
                                 if (inc != 0 && hc_cnt[v] != 0xFFFFu && !(inc == 1 && v == mvv)) {
                                     mh = hc_min[v];
                                     cnt = hc_cnt[v];
@@ -463,8 +463,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                             hn[nx++] = (max(0, wv - mx32[x]) << S) + Tt * gnew;
                                         }
                                         if (cnt == 0) {
-                                            full = true;  // the minimum group emptied: rescan
-                                            mh = INT_MAX;
+                                            full = true;  // the minimum group emptied
                                         } else {
                                             for (int i2 = 0; i2 < nx; i2++) {
                                                 cnt = (hn[i2] < mh) ? 1 : cnt + (hn[i2] == mh);
@@ -473,49 +472,56 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                         }
                                     }
                                 }
-                                if (!full) {
-                                } else if (NARROW && (k & 3) == 0) {
-                                    const uint32_t *row32 = reinterpret_cast<const uint32_t *>(row);
-                                    for (int c4 = 0; c4 < k; c4 += 4) {
-                                        const uint32_t g4 = row32[c4 >> 2];
-    #pragma unroll
-                                        for (int j = 0; j < 4; j++) {
-                                            const int c = c4 + j;
-                                            const int H = (max(0, wv - mx32[c]) << S) + Tt * (int)((g4 >> (8 * j)) & 0xFFu);
-                                            const int Hx = (c == a) ? INT_MAX : H;
-                                            cnt = (Hx < mh) ? 1 : cnt + (Hx == mh);
-                                            mh = min(mh, Hx);
-                                        }
-                                    }
-                                } else {
+                            } else {
+                                hc_cnt[v] = 0xFFFFu;
+                                if (conflicts <= gva && rem + min(best - score, (long long)INT_MAX) > 0) {
+                                    // (a frozen row needs ds = max(0, w - M_c) - rem < best - score:
+                                    // impossible when rem + best - score <= 0, e.g. every row
+                                    // whose move cannot lower a class maximum at a legal state)
+                                    // frozen vertex: only legal moves (dc == -conflicts, reachable
+                                    // only if conflicts <= gva) that beat the best legal score
+                                    const int need_dc = -(int)conflicts;
+                                    const long long room = best - score;  // ds < room
+                                    const int dsmax = room > INT_MAX ? INT_MAX : (room < INT_MIN ? INT_MIN : (int)room);
                                     for (int c = 0; c < k; c++) {
-                                        const int H = (max(0, wv - mx32[c]) << S) + Tt * (int)row[c];
-                                        const int Hx = (c == a) ? INT_MAX : H;
-                                        cnt = (Hx < mh) ? 1 : cnt + (Hx == mh);
-                                        mh = min(mh, Hx);
+                                        const int dc = (int)row[c] - gva;
+                                        const int ds = max(0, wv - (int)max_val[c]) - rem;
+                                        const bool ok = c != a && dc == need_dc && ds < dsmax;
+                                        const int G = ok ? (ds << S) + Tt * dc : INT_MAX;
+                                        cnt = (G < m) ? 1 : cnt + (G == m && ok);
+                                        m = min(m, G);
                                     }
                                 }
+                            }
+                        }
+                        // full rescans of this chunk's rows by the whole warp: lanes over
+                        // colours, minimum by REDUX, multiplicity by ballots
+                        for (unsigned rs = __ballot_sync(FULL, full); rs; rs &= rs - 1) {
+                            const int src = __ffs(rs) - 1;
+                            const int au = __shfl_sync(FULL, a, src), wu = __shfl_sync(FULL, wv, src);
+                            const GT *ru = gamma + (size_t)(v0 + src) * k;
+                            int lmin = INT_MAX;
+                            for (int cb = 0; cb < k; cb += 32) {
+                                const int c = cb + lane;
+                                if (c < k && c != au) lmin = min(lmin, (max(0, wu - mx32[c]) << S) + Tt * (int)ru[c]);
+                            }
+                            const int hm = __reduce_min_sync(FULL, lmin);
+                            int hcn = 0;
+                            for (int cb = 0; cb < k; cb += 32) {
+                                const int c = cb + lane;
+                                const bool eq = c < k && c != au && (max(0, wu - mx32[c]) << S) + Tt * (int)ru[c] == hm;
+                                hcn += __popc(__ballot_sync(FULL, eq));
+                            }
+                            if (lane == src) {
+                                mh = hm;
+                                cnt = hm == INT_MAX ? 0 : hcn;
+                            }
+                        }
+                        if (v < n) {
+                            if ((uint64_t)it >= tabu_until[v]) {  // not frozen: the cache and the row minimum
                                 hc_min[v] = mh;
                                 hc_cnt[v] = (uint16_t)cnt;
                                 m = (mh == INT_MAX) ? INT_MAX : mh - (rem << S) - Tt * gva;
-                            } else if ((hc_cnt[v] = 0xFFFFu, conflicts <= gva) &&
-                                       rem + min(best - score, (long long)INT_MAX) > 0) {
-                                // (a frozen row needs ds = max(0, w - M_c) - rem < best - score:
-                                // impossible when rem + best - score <= 0, e.g. every row
-                                // whose move cannot lower a class maximum at a legal state)
-                                // frozen vertex: only legal moves (dc == -conflicts, reachable
-                                // only if conflicts <= gva) that beat the best legal score
-                                const int need_dc = -(int)conflicts;
-                                const long long room = best - score;  // ds < room
-                                const int dsmax = room > INT_MAX ? INT_MAX : (room < INT_MIN ? INT_MIN : (int)room);
-                                for (int c = 0; c < k; c++) {
-                                    const int dc = (int)row[c] - gva;
-                                    const int ds = max(0, wv - (int)max_val[c]) - rem;
-                                    const bool ok = c != a && dc == need_dc && ds < dsmax;
-                                    const int G = ok ? (ds << S) + Tt * dc : INT_MAX;
-                                    cnt = (G < m) ? 1 : cnt + (G == m && ok);
-                                    m = min(m, G);
-                                }
                             }
                             r32[v] = m;
                             rcnt[v] = (uint16_t)(m == INT_MAX ? 0 : cnt);
