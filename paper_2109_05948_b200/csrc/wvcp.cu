@@ -94,6 +94,18 @@ struct WvCtrl {
     long long red2[WV_NT / 32];
 };
 
+// x % s == 0 for the reservoir draws: s < 64 by a table (inverse of the odd
+// part mod 2^64 and floor((2^64 - 1) / odd)), larger s by the fp64 test
+__device__ ulonglong2 g_divtab_wv[32];
+__device__ __forceinline__ bool divisible_wv(uint64_t x, uint32_t s) {
+    if (s < 64u) {
+        const int t = __ffs(s) - 1;
+        const ulonglong2 e = g_divtab_wv[(s >> t) >> 1];
+        return (x & ((1ull << t) - 1ull)) == 0ull && (x >> t) * e.x <= e.y;
+    }
+    return mod_is_zero(x, s);
+}
+
 __device__ __forceinline__ double gval_of(long long ds, long long dc, double phi) {
     return __dadd_rn((double)ds, __dmul_rn(phi, (double)dc));  // no FMA (:193)
 }
@@ -204,28 +216,56 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
     // drop of the class max if that member were the only one at its rank
     auto refresh_class = [&](int c) {
         const uint16_t *row = wc + (size_t)c * nranks;
-        int mr = -1;
-        for (int r0 = nranks - 1; r0 >= 0 && mr < 0; r0 -= 32) {
-            const int r = r0 - lane;
-            const bool has = r >= 0 && row[r] > 0;
-            const unsigned b = __ballot_sync(FULL, has);
-            if (b) mr = r0 - (__ffs(b) - 1);
-        }
-        long long mv = 0, ud = 0;
-        if (mr >= 0) {
-            mv = P.wvals[mr];
-            if (row[mr] > 1) {
-                ud = 0;
-            } else {
-                int sr = -1;
+        int mr = -1, sr = -1;
+        unsigned cnt_mr = 0;
+        if (nranks <= 128) {
+            // all of the class's rank counts in flight at once (one L2 round trip):
+            // lane L holds ranks nranks-1-L-32j, j < 4, top rank first
+            uint32_t h[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int r = nranks - 1 - lane - 32 * j;
+                h[j] = r >= 0 ? row[r] : 0u;
+            }
+            int found = 0;  // ranks with a member, highest first: mr, then sr
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                unsigned b = __ballot_sync(FULL, h[j] > 0);
+                while (b && found < 2) {
+                    const int L = __ffs(b) - 1;
+                    b &= b - 1;
+                    const int r = nranks - 1 - L - 32 * j;
+                    if (found == 0) {
+                        mr = r;
+                        cnt_mr = __shfl_sync(FULL, h[j], L);
+                    } else {
+                        sr = r;
+                    }
+                    found++;
+                    if (found == 1 && cnt_mr > 1) found = 2;  // the drop is 0: no second rank needed
+                }
+            }
+        } else {
+            for (int r0 = nranks - 1; r0 >= 0 && mr < 0; r0 -= 32) {
+                const int r = r0 - lane;
+                const bool has = r >= 0 && row[r] > 0;
+                const unsigned b = __ballot_sync(FULL, has);
+                if (b) mr = r0 - (__ffs(b) - 1);
+            }
+            if (mr >= 0) cnt_mr = row[mr];
+            if (mr >= 0 && cnt_mr == 1) {
                 for (int r0 = mr - 1; r0 >= 0 && sr < 0; r0 -= 32) {
                     const int r = r0 - lane;
                     const bool has = r >= 0 && row[r] > 0;
                     const unsigned b = __ballot_sync(FULL, has);
                     if (b) sr = r0 - (__ffs(b) - 1);
                 }
-                ud = mv - (sr >= 0 ? P.wvals[sr] : 0);
             }
+        }
+        long long mv = 0, ud = 0;
+        if (mr >= 0) {
+            mv = P.wvals[mr];
+            ud = cnt_mr > 1 ? 0 : mv - (sr >= 0 ? P.wvals[sr] : 0);
         }
         if (lane == 0) {
             max_rank[c] = mr;
@@ -640,7 +680,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                     const unsigned long long c0 = ctr + (unsigned long long)(total - (T - 1));
                                     int smax = 1;
                                     for (int s2 = 2 + lane; s2 <= T; s2 += 32)
-                                        if (mod_is_zero(stream_value(key, c0 + (unsigned long long)(s2 - 2)), (uint32_t)s2))
+                                        if (divisible_wv(stream_value(key, c0 + (unsigned long long)(s2 - 2)), (uint32_t)s2))
                                             smax = s2;
                                     sstar = __reduce_max_sync(FULL, smax);
                                 } else {
@@ -880,7 +920,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                 const unsigned long long c0 = ctr + (unsigned long long)(total - (T - 1));
                                 int smax = 1;
                                 for (int s = 2 + lane; s <= T; s += 32)
-                                    if (mod_is_zero(stream_value(key, c0 + (unsigned long long)(s - 2)), (uint32_t)s))
+                                    if (divisible_wv(stream_value(key, c0 + (unsigned long long)(s - 2)), (uint32_t)s))
                                         smax = s;
                                 sstar = __reduce_max_sync(FULL, smax);
                             } else {
@@ -1072,9 +1112,29 @@ static size_t wv_smem(int n, int k, int gbytes) {
            a16((size_t)(n + 1) * 4) + a16((size_t)n * 4);
 }
 
+static int upload_divtab_wv(cudaStream_t st) {
+    static bool done[64] = {false};
+    int d = 0;
+    cudaGetDevice(&d);
+    if (done[d & 63]) return MCB_OK;
+    ulonglong2 tab[32];
+    for (int i = 0; i < 32; i++) {
+        const uint64_t o = 2 * (uint64_t)i + 1;
+        uint64_t x = o;  // Newton: inverse of o modulo 2^64
+        for (int r = 0; r < 6; r++) x *= 2 - o * x;
+        tab[i] = make_ulonglong2(x, ~0ull / o);
+    }
+    if (cudaMemcpyToSymbolAsync(g_divtab_wv, tab, sizeof(tab), 0, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return set_error(MCB_ERR_CUDA, "wvcp: divisor table upload failed");
+    done[d & 63] = true;
+    return MCB_OK;
+}
+
 template <typename GT, bool STATS>
 static int wvcp_launch_t(WvParams P, int64_t nwork, cudaStream_t st, uint8_t *ws_base, size_t ws_cap_ctas,
                          size_t wc_stride) {
+    if (int rc = upload_divtab_wv(st)) return rc;
     const size_t smem = wv_smem(P.n, P.k, sizeof(GT));
     if (smem > (size_t)max_smem_optin())
         return set_error(MCB_ERR_UNSUPPORTED, "wvcp: n*k too large for shared memory (%zu B)", smem);
