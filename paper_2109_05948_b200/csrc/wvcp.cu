@@ -44,6 +44,9 @@ namespace mcb {
 
 constexpr int WV_NT = 256;
 constexpr int WV_INF_SCORE_SHIFT = 62;
+// shared-memory segments, in layout order
+enum WvSeg { S_GAMMA, S_TABU, S_WGT, S_WRK, S_ASSIGN, S_RMIN, S_RCNT, S_MAXRANK, S_MAXVAL, S_UNIQ, S_CMAX, S_MX32,
+             S_LOWQ, S_IP32, S_NBUF, S_LOWR, WV_NSEG };
 
 struct WvParams {
     int32_t *assigns;
@@ -79,6 +82,10 @@ struct WvParams {
     int32_t *err_flag;
     uint16_t *ws_wc;  // per-CTA [k][nranks]
     size_t ws_wc_stride;
+    // dynamic shared-memory layout, computed on the host (wv_layout): offsets
+    // read from the parameter bank are free operands, whereas offsets carved
+    // in the kernel are rematerialised inside the loop under the register cap
+    uint32_t so[WV_NSEG + 1];
 };
 
 struct WvCtrl {
@@ -169,28 +176,22 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ WvCtrl ctl;
     const int n = P.n, k = P.k, nranks = P.nranks;
-    size_t off = 0;
-    auto take = [&](size_t bytes) {
-        uint8_t *p = smem + off;
-        off += (bytes + 15) & ~(size_t)15;
-        return p;
-    };
-    GT *gamma = reinterpret_cast<GT *>(take((size_t)n * k * sizeof(GT)));
-    uint32_t *tabu_until = reinterpret_cast<uint32_t *>(take((size_t)n * 4));
-    int32_t *wgt = reinterpret_cast<int32_t *>(take((size_t)n * 4));
-    uint16_t *wrk = reinterpret_cast<uint16_t *>(take((size_t)n * 2));
-    uint8_t *assign = take((size_t)n);
-    double *rmin = reinterpret_cast<double *>(take((size_t)n * 8));
-    uint16_t *rcnt = reinterpret_cast<uint16_t *>(take((size_t)n * 2));
-    int32_t *max_rank = reinterpret_cast<int32_t *>(take((size_t)k * 4));
-    int64_t *max_val = reinterpret_cast<int64_t *>(take((size_t)k * 8));
-    int64_t *uniq_drop = reinterpret_cast<int64_t *>(take((size_t)k * 8));
-    int32_t *cmax = reinterpret_cast<int32_t *>(take((size_t)k * 4));  // scratch
-    int32_t *mx32 = reinterpret_cast<int32_t *>(take((size_t)k * 4));  // max_val as int32 (the scan's copy)
-    int32_t *lowq = reinterpret_cast<int32_t *>(take((size_t)(2 * n + 64) * 4));  // 32-bit path: chunk minima / counts, walk queue
-    int32_t *ip32 = reinterpret_cast<int32_t *>(take((size_t)(n + 1) * 4));      // CSR row offsets
-    int32_t *nbuf = reinterpret_cast<int32_t *>(take((size_t)n * 4));            // the moved vertex's neighbours
-    double *lowR = reinterpret_cast<double *>(take((size_t)n * 8));
+    GT *gamma = reinterpret_cast<GT *>(smem + P.so[S_GAMMA]);
+    uint32_t *tabu_until = reinterpret_cast<uint32_t *>(smem + P.so[S_TABU]);
+    int32_t *wgt = reinterpret_cast<int32_t *>(smem + P.so[S_WGT]);
+    uint16_t *wrk = reinterpret_cast<uint16_t *>(smem + P.so[S_WRK]);
+    uint8_t *assign = smem + P.so[S_ASSIGN];
+    double *rmin = reinterpret_cast<double *>(smem + P.so[S_RMIN]);
+    uint16_t *rcnt = reinterpret_cast<uint16_t *>(smem + P.so[S_RCNT]);
+    int32_t *max_rank = reinterpret_cast<int32_t *>(smem + P.so[S_MAXRANK]);
+    int64_t *max_val = reinterpret_cast<int64_t *>(smem + P.so[S_MAXVAL]);
+    int64_t *uniq_drop = reinterpret_cast<int64_t *>(smem + P.so[S_UNIQ]);
+    int32_t *cmax = reinterpret_cast<int32_t *>(smem + P.so[S_CMAX]);  // scratch
+    int32_t *mx32 = reinterpret_cast<int32_t *>(smem + P.so[S_MX32]);  // max_val as int32 (the scan's copy)
+    int32_t *lowq = reinterpret_cast<int32_t *>(smem + P.so[S_LOWQ]);  // 32-bit path: chunk minima / counts, walk queue
+    int32_t *ip32 = reinterpret_cast<int32_t *>(smem + P.so[S_IP32]);  // CSR row offsets
+    int32_t *nbuf = reinterpret_cast<int32_t *>(smem + P.so[S_NBUF]);  // the moved vertex's neighbours
+    double *lowR = reinterpret_cast<double *>(smem + P.so[S_LOWR]);
     uint16_t *wc = P.ws_wc + blockIdx.x * P.ws_wc_stride;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1104,13 +1105,21 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
     }
 }
 
-static size_t wv_smem(int n, int k, int gbytes) {
-    auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
-    return a16((size_t)n * k * gbytes) + a16((size_t)n * 4) + a16((size_t)n * 4) + a16((size_t)n * 2) +
-           a16((size_t)n) + a16((size_t)n * 8) + a16((size_t)n * 2) + a16((size_t)k * 4) +
-           2 * a16((size_t)k * 8) + 2 * a16((size_t)k * 4) + a16((size_t)(2 * n + 64) * 4) + a16((size_t)n * 8) +
-           a16((size_t)(n + 1) * 4) + a16((size_t)n * 4);
+// segment sizes in WvSeg order, each 16-byte aligned; so[WV_NSEG] = total
+static size_t wv_layout(int n, int k, int gbytes, uint32_t *so) {
+    const size_t N = (size_t)n, K = (size_t)k;
+    const size_t bytes[WV_NSEG] = {N * K * gbytes, N * 4, N * 4, N * 2, N, N * 8, N * 2, K * 4,
+                                   K * 8,          K * 8, K * 4, K * 4, (2 * N + 64) * 4, (N + 1) * 4,
+                                   N * 4,          N * 8};
+    size_t off = 0;
+    for (int i = 0; i < WV_NSEG; i++) {
+        if (so) so[i] = (uint32_t)off;
+        off += (bytes[i] + 15) & ~(size_t)15;
+    }
+    if (so) so[WV_NSEG] = (uint32_t)off;
+    return off;
 }
+static size_t wv_smem(int n, int k, int gbytes) { return wv_layout(n, k, gbytes, nullptr); }
 
 static int upload_divtab_wv(cudaStream_t st) {
     static bool done[64] = {false};
@@ -1135,7 +1144,7 @@ template <typename GT, bool STATS>
 static int wvcp_launch_t(WvParams P, int64_t nwork, cudaStream_t st, uint8_t *ws_base, size_t ws_cap_ctas,
                          size_t wc_stride) {
     if (int rc = upload_divtab_wv(st)) return rc;
-    const size_t smem = wv_smem(P.n, P.k, sizeof(GT));
+    const size_t smem = wv_layout(P.n, P.k, sizeof(GT), P.so);
     if (smem > (size_t)max_smem_optin())
         return set_error(MCB_ERR_UNSUPPORTED, "wvcp: n*k too large for shared memory (%zu B)", smem);
     if (cudaFuncSetAttribute(wvcp_kernel<GT, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
