@@ -626,7 +626,7 @@ def run_extra(wl, world, rank, dev, flush, reduce_max_sum):
         desc = ctypes.create_string_buffer(256)
         N.check(N.lib().mcb_tabucol_describe(n, k, hi - lo, desc, 256))
         alg = algorithmic_bytes(k, sc, sd) / world
-        in_l2 = "tabucol_kernel" in desc.value.decode() and n > 1024
+        in_l2 = "gamma in L2" in desc.value.decode()
         gbs, pms = ctypes.c_double(), ctypes.c_double()
         if in_l2:
             N.check(N.lib().mcb_probe_l2_bandwidth(ctypes.byref(gbs), ctypes.byref(pms)))

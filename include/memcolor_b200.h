@@ -53,6 +53,7 @@ extern "C" {
 #define MCB_FLAG_FORCE_GLOBAL 0x8u /* gamma/tabu tables in global memory (L2-resident path, tests) */
 #define MCB_FLAG_PROFILE 0x100u    /* accumulate per-phase clock64 cycles (mcb_debug_phase_cycles) */
 #define MCB_FLAG_WSTATS 0x200u     /* warp kernel: event counters + phase cycles (mcb_debug_warp_stats) */
+#define MCB_FLAG_FORCE_CLUSTER 0x800u /* TabuCol on the 2-CTA cluster kernel whatever the shape (tests) */
 #define MCB_FLAG_ASYNC 0x400u      /* mcb_tabucol_batch: no host synchronisation (per-stream scratch, every
                                       fallback pass enqueued with device-side counts; CUDA-graph capturable
                                       after one warm-up call); errors via mcb_tabucol_async_status */
@@ -69,11 +70,15 @@ int mcb_probe_smem_bandwidth(double *gbs, double *ms);
  * roofline denominator of the out-of-shared-memory TabuCol shapes. */
 int mcb_probe_l2_bandwidth(double *gbs, double *ms);
 /* Diagnostics: per-phase cycle totals of the TabuCol iteration accumulated
- * by runs with MCB_FLAG_PROFILE (out: 16 counters; [10] = iterations). */
+ * by runs with MCB_FLAG_PROFILE (out: 16 counters; [10] = iterations; the
+ * CTA kernel's and the cluster kernel's counters, see tabucol_cluster.cu). */
 int mcb_debug_phase_cycles(unsigned long long *out, int reset);
 /* Diagnostics: counters of the last warp-kernel TabuCol launch made with
  * MCB_FLAG_WSTATS (out: 40 counters, see tabucol_warp.cu WS_*). */
 int mcb_debug_warp_stats(unsigned long long *out);
+/* Cluster TabuCol kernel under MCB_FLAG_PROFILE, rank-0 CTAs: per warp w,
+ * out[w] pass-1 cycles, out[32+w] start delays, out[64+w] warp scans (96). */
+int mcb_debug_cluster_warps(unsigned long long *out, int reset);
 /* Group-of-warps TabuCol kernel run with MCB_GSTATS=1 in the environment:
  * thread 0's cycles per phase (out: 32 counters; [15] = iterations). */
 int mcb_debug_group_stats(unsigned long long *out);

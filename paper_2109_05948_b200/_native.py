@@ -23,12 +23,13 @@ FLAG_FORCE_GLOBAL = 0x8
 FLAG_PROFILE = 0x100
 FLAG_WSTATS = 0x200
 FLAG_ASYNC = 0x400
+FLAG_FORCE_CLUSTER = 0x800
 
 EXPORTS = [
     "mcb_version", "mcb_last_error", "mcb_device_count", "mcb_stream_values",
     "mcb_tabucol_batch", "mcb_tabucol_batch_host", "mcb_tabucol_async_status", "mcb_wvcp_batch", "mcb_wvcp_batch_host",
     "mcb_gpx_batch", "mcb_gpx_batch_host", "mcb_gpx_rows", "mcb_pairwise", "mcb_pairwise_host", "mcb_pairwise_jobs", "mcb_pairwise_scatter",
-    "mcb_probe_smem_bandwidth", "mcb_probe_l2_bandwidth", "mcb_debug_phase_cycles", "mcb_debug_warp_stats", "mcb_debug_group_stats", "mcb_debug_wvcp_stats",
+    "mcb_probe_smem_bandwidth", "mcb_probe_l2_bandwidth", "mcb_debug_phase_cycles", "mcb_debug_warp_stats", "mcb_debug_cluster_warps", "mcb_debug_group_stats", "mcb_debug_wvcp_stats",
     "mcb_debug_modcheck", "mcb_tabucol_describe",
     "mcb_update_population", "mcb_update_population_host", "mcb_match_parents", "mcb_match_parents_host",
     "mcb_greedy_wvcp_init", "mcb_greedy_wvcp_init_host", "mcb_segsum", "mcb_segsum_async",
@@ -69,6 +70,7 @@ def _declare(L):
     L.mcb_probe_l2_bandwidth.argtypes = [P, P]
     L.mcb_debug_phase_cycles.argtypes = [P, C.c_int]
     L.mcb_debug_warp_stats.argtypes = [P]
+    L.mcb_debug_cluster_warps.argtypes = [P, C.c_int]
     L.mcb_debug_group_stats.argtypes = [P]
     L.mcb_debug_wvcp_stats.argtypes = [P, C.c_int]
     L.mcb_debug_modcheck.argtypes = [I64, P]

@@ -54,6 +54,13 @@ int tabucol_group_launch(const TabucolArgs &A, cudaStream_t st, int32_t *work_co
 int tabucol_group_describe(int64_t n, int64_t k, int64_t p, char *buf, int len);
 int tabucol_group_stats(unsigned long long *out);
 int tabucol_phase_cycles(unsigned long long *out, int reset);
+struct TabuParams;  // tc_shared.cuh
+int tabucol_cta_describe(int64_t n, int64_t k, int64_t p, char *buf, int len);
+size_t tabucol_cluster_smem(int n, int k);
+int tabucol_cluster_phase_cycles(unsigned long long *out, int reset);
+int tabucol_cluster_warp_stats(unsigned long long *out, int reset);
+size_t tabucol_cluster_stamp_stride(int n, int k);
+int tabucol_cluster_launch(const TabuParams &P, int max_clusters, cudaStream_t st, int *grid_out, bool query_only);
 int tabucol_warp_stats(unsigned long long *out);
 
 struct WvcpArgs {

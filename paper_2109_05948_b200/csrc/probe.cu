@@ -99,6 +99,9 @@ extern "C" int mcb_debug_phase_cycles(unsigned long long *out, int reset) {
 }
 
 extern "C" int mcb_debug_warp_stats(unsigned long long *out) { return mcb::tabucol_warp_stats(out); }
+extern "C" int mcb_debug_cluster_warps(unsigned long long *out, int reset) {
+    return mcb::tabucol_cluster_warp_stats(out, reset);
+}
 extern "C" int mcb_debug_group_stats(unsigned long long *out) { return mcb::tabucol_group_stats(out); }
 extern "C" int mcb_debug_wvcp_stats(unsigned long long *out, int reset) { return mcb::wvcp_stats(out, reset); }
 

@@ -51,13 +51,12 @@
 
 #include "common.cuh"
 #include "launch.h"
+#include "tc_shared.cuh"
 
 namespace mcb {
 
-constexpr int TC_BIG = 1 << 20;
 constexpr int TC_CONST_INDPTR = 12288;
 constexpr int TC_NT = 128;
-constexpr int TC_LOWCAP = 192;
 
 __constant__ uint32_t c_indptr[TC_CONST_INDPTR];
 __device__ unsigned long long g_phase_cycles[16];
@@ -69,59 +68,6 @@ __device__ unsigned long long g_phase_cycles[16];
         ph_t = _t;                      \
     }
 
-struct TabuParams {
-    int32_t *assigns;
-    int32_t *best_assigns;
-    const int64_t *indptr;
-    const int32_t *indices;
-    const int32_t *eu;
-    const int32_t *ev;
-    int64_t m;
-    int n, k, kp;
-    int64_t depth;
-    const uint64_t *keys;
-    int64_t *best_conflicts, *end_conflicts, *iters_used, *diag;
-    int64_t log_cap;
-    int32_t *log_v;
-    int64_t *log_iter, *log_tt, *log_cnt;
-    int64_t *counters;
-    const int32_t *work;       // optional list of individual ids
-    const int32_t *nwork_dev;  // optional device-side work count
-    int nwork;
-    int32_t *work_counter;
-    int32_t *ovf_list, *ovf_count;  // individuals to redo wide
-    int32_t *err_flag;
-    int32_t *sm_ticket;  // per-SM counters: master-warp assignment
-    uint8_t *ws_gamma;  // per-CTA gamma slice (when gamma is not in smem)
-    uint8_t *ws_stamp;  // per-CTA dense overflow expiry table
-    size_t ws_g_stride, ws_s_stride;
-    uint32_t flags;
-    int const_indptr;
-    int swz_rs, swz_rm;  // gamma row word rotation: rot(v) = (v >> rs) & rm
-};
-
-// (int, int) pair records: packed int16 x 2 for the narrow variant (deltas in
-// [-254, 254] or TC_BIG), int2 for the wide one
-template <bool NARROW>
-struct RecT;
-template <>
-struct RecT<true> {
-    using T = uint32_t;
-};
-template <>
-struct RecT<false> {
-    using T = int2;
-};
-__device__ __forceinline__ uint32_t rec_pack(int x, int y, uint32_t *) {
-    return (uint32_t)(uint16_t)(int16_t)(x >= TC_BIG ? 0x7FFF : x) | ((uint32_t)y << 16);
-}
-__device__ __forceinline__ int2 rec_pack(int x, int y, int2 *) { return make_int2(x, y); }
-__device__ __forceinline__ int2 rec_unpack(uint32_t r) {
-    const int x = (int)(int16_t)(r & 0xFFFFu);
-    return make_int2(x == 0x7FFF ? TC_BIG : x, (int)(r >> 16));
-}
-__device__ __forceinline__ int2 rec_unpack(int2 r) { return r; }
-
 template <int NW>
 struct TabuCtrl {
     long long it, conflicts, best, nlog, sum_c, sum_deg, diag;
@@ -132,43 +78,6 @@ struct TabuCtrl {
     int wcnt[NW];
     long long ph[10];
 };
-
-template <typename S>
-__device__ __forceinline__ bool active(S e, uint32_t it) {
-    if constexpr (sizeof(S) == 2)
-        return (int16_t)(uint16_t)((uint16_t)e - (uint16_t)it) > 0;
-    else
-        return (int32_t)((uint32_t)e - it) > 0;
-}
-
-// a 5th live tabu entry of a vertex: spill to its dense global row (rare)
-template <typename S>
-__device__ __noinline__ void spill_set(S *gs, S *tovf_v, bool ovf_live, int k, int a, S e_new,
-                                       uint32_t it) {
-    if (!ovf_live) {  // fresh spill row
-        for (int cc = 0; cc < k; cc++) gs[cc] = (S)it;
-        *tovf_v = e_new;
-    } else if (active<S>(e_new, (uint32_t)*tovf_v)) {
-        *tovf_v = e_new;
-    }
-    gs[a] = e_new;
-}
-
-// number of bytes of x equal to byte value c
-__device__ __forceinline__ int count_eq_bytes(uint32_t x, uint32_t c) {
-    const uint32_t z = x ^ (c * 0x01010101u);
-    const uint32_t t = ((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z;
-    return __popc(~t & 0x80808080u);
-}
-// unsigned byte minimum (native 16x2 min)
-__device__ __forceinline__ uint32_t min_bytes(uint32_t x) {
-    const uint32_t m2 = __vminu2(x & 0x00FF00FFu, (x >> 8) & 0x00FF00FFu);
-    return min(m2 & 0xFFFFu, m2 >> 16);
-}
-// 4 bits -> 4 byte masks
-__device__ __forceinline__ uint32_t expand_nibble(uint32_t nib) {
-    return ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;
-}
 
 // Candidate row of one conflicting vertex v.  Candidates are gamma values g
 // (delta = g - gva); excluded: c == a, and live tabu colours without
@@ -365,22 +274,6 @@ struct RowEval {
         return __reduce_add_sync(FULL, t);
     }
 };
-
-// conflict-list membership update (:374-385): append, or swap-with-last remove
-__device__ __forceinline__ void cl_apply(uint16_t *clist, uint16_t *cpos, int &Cn, int u, bool in_conf) {
-    const int pu = cpos[u];
-    if (in_conf && pu == 0xFFFF) {
-        cpos[u] = (uint16_t)Cn;
-        clist[Cn] = (uint16_t)u;
-        Cn++;
-    } else if (!in_conf && pu != 0xFFFF) {
-        const int last = clist[Cn - 1];
-        clist[pu] = (uint16_t)last;
-        cpos[last] = (uint16_t)pu;
-        Cn--;
-        cpos[u] = 0xFFFF;
-    }
-}
 
 // warp-cooperative walks of the queued (running min, row) pairs; returns the
 // tie events on lane 0 (0 elsewhere)
@@ -1080,7 +973,7 @@ int tabucol_phase_cycles(unsigned long long *out, int reset) {
         unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
     }
-    return MCB_OK;
+    return tabucol_cluster_phase_cycles(out, reset);  // added in: a run uses one of the two kernels
 }
 
 static const int32_t *&async_err_slot(cudaStream_t st) {
@@ -1099,6 +992,31 @@ int tabucol_async_status(cudaStream_t st) {
         return set_error(MCB_ERR_CUDA, "tabucol: kernel failed: %s", cudaGetErrorString(cudaGetLastError()));
     if (h == 1) return set_error(MCB_ERR_RANGE, "color id out of range [0, k)");
     if (h == 2) return set_error(MCB_ERR_UNSUPPORTED, "tabucol: wide tables overflowed");
+    return MCB_OK;
+}
+
+// 0: narrow, gamma in smem (warp / group kernels first); 1: narrow, gamma in
+// global (L2) slices; 2: wide only; 3: narrow, gamma split over a 2-CTA
+// cluster's shared memory (tabucol_cluster.cu) -- the default where one
+// SM's shared memory cannot hold the table (MCB_NO_CLUSTER=1: variant 1)
+static int tabucol_variant(int n, int k, uint32_t flags) {
+    const int kp = (k + 3) & ~3;
+    if (flags & MCB_FLAG_FORCE_WIDE) return 2;
+    if (flags & MCB_FLAG_FORCE_CLUSTER) return 3;
+    if (flags & MCB_FLAG_FORCE_GLOBAL) return 1;
+    if (fits_smem(smem_bytes<uint8_t, uint16_t, true>(n, kp))) return 0;
+    if (!getenv("MCB_NO_CLUSTER") && fits_smem(tabucol_cluster_smem(n, k))) return 3;
+    return 1;
+}
+
+int tabucol_cta_describe(int64_t n, int64_t k, int64_t p, char *buf, int len) {
+    const int v = tabucol_variant((int)n, (int)k, 0);
+    if (v == 3)
+        snprintf(buf, len, "tabucol_cluster_kernel (2-CTA cluster per individual, %zu B smem per CTA)",
+                 tabucol_cluster_smem((int)n, (int)k));
+    else
+        snprintf(buf, len, "tabucol_kernel (CTA per individual; gamma in %s)", v == 0 ? "shared memory" : "L2");
+    (void)p;
     return MCB_OK;
 }
 
@@ -1160,13 +1078,7 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
         if (!getenv("MCB_SWIZZLE")) P.swz_rm = 0;  // measured: no gain at k=48 (latency-bound)
     }
 
-    const bool force_wide = (A.flags & MCB_FLAG_FORCE_WIDE) != 0;
-    const bool force_glob = (A.flags & MCB_FLAG_FORCE_GLOBAL) != 0;
-    // 0: narrow, gamma in smem; 1: narrow, gamma global; 2: wide only
-    int variant;
-    if (force_wide) variant = 2;
-    else if (!force_glob && fits_smem(smem_bytes<uint8_t, uint16_t, true>(n, kp))) variant = 0;
-    else variant = 1;
+    const int variant = tabucol_variant(n, k, A.flags);
 
     const size_t tab = (size_t)n * kp;
     const int grid_cap = 16 * num_sms();
@@ -1180,7 +1092,12 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
 
     int grid = 1, rc;
     size_t narrow_ws = 0;
-    if (variant != 2) {
+    const size_t cl_stride = tabucol_cluster_stamp_stride(n, k);
+    if (variant == 3) {
+        rc = tabucol_cluster_launch(P, (int)A.p, st, &grid, true);
+        if (rc) return rc;
+        narrow_ws = (size_t)grid * cl_stride;
+    } else if (variant != 2) {
         rc = variant == 0
                  ? launch_variant<uint8_t, uint16_t, true>(P, grid_cap, (int)A.p, st, &grid, true)
                  : launch_variant<uint8_t, uint16_t, false>(P, grid_cap, (int)A.p, st, &grid, true);
@@ -1260,14 +1177,14 @@ int tabucol_run(const TabucolArgs &A, cudaStream_t st) {
         P.ovf_count = ctl32 + 2;
         P.ovf_list = ctl32 + 64 + 256;
         P.ws_stamp = tables;
-        P.ws_s_stride = ns_stride;
+        P.ws_s_stride = variant == 3 ? cl_stride : ns_stride;
         if (variant == 1) {
             P.ws_gamma = tables + (size_t)grid * ns_stride;
             P.ws_g_stride = ng_stride;
         }
-        rc = variant == 0
-                 ? launch_variant<uint8_t, uint16_t, true>(P, grid_cap, (int)A.p, st, &grid, false)
-                 : launch_variant<uint8_t, uint16_t, false>(P, grid_cap, (int)A.p, st, &grid, false);
+        rc = variant == 3   ? tabucol_cluster_launch(P, (int)A.p, st, &grid, false)
+             : variant == 0 ? launch_variant<uint8_t, uint16_t, true>(P, grid_cap, (int)A.p, st, &grid, false)
+                            : launch_variant<uint8_t, uint16_t, false>(P, grid_cap, (int)A.p, st, &grid, false);
         if (rc) return rc;
     }
     // wide pass: either everything (forced) or the overflowed individuals

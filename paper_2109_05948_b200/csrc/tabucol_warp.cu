@@ -1290,8 +1290,7 @@ namespace mcb {
 int tabucol_warp_describe(int64_t n, int64_t k, int64_t p, char *buf, int len) {
     WarpPlan pl;
     if (!tw_plan((int)n, (int)k, p, &pl)) {
-        snprintf(buf, len, "tabucol_kernel (CTA per individual; shape outside the warp kernel)");
-        return MCB_OK;
+        return tabucol_cta_describe(n, k, p, buf, len);  // shape outside the warp kernel
     }
     snprintf(buf, len, "tabucol_warp_kernel<KV=%d,%s> %d warps/CTA x %d CTAs, %zu B smem/individual", pl.kv,
              pl.ch ? (pl.ch == 8 ? "bitset CH=8" : pl.ch == 16 ? "bitset CH=16" : "bitset CH=32") : "csr",

@@ -2,8 +2,9 @@
 bit-exact against the C restatement of `_tabucol_batch` (`mc/localsearch.py:
 266-410`), move logs included:
 
-* config 4 (C5): G(2000, .5), k = 150 -- the CTA kernel with its gamma table
-  in per-CTA global (L2-resident) slices, both thread counts per individual;
+* config 4 (C5): G(2000, .5), k = 150 -- the 2-CTA cluster kernel (gamma
+  split over two SMs' shared memory), and the CTA kernel with its gamma table
+  in per-CTA global (L2-resident) slices at both thread counts;
 * config 2 (C3): G(1000, .5), k = 83 from random colourings at 20,000
   iterations -- tenures ~1,800 keep > 1,024 tabu entries live, so the
   individuals run on the warp kernel's SPILL variant (rows spilled to global
@@ -39,15 +40,19 @@ def c5_case(oracle_lib):
     return g, A, keys, ref
 
 
-@pytest.mark.parametrize("nt", ["128", "256"])
-def test_c5_shape_vs_oracle(c5_case, nt, monkeypatch):
+@pytest.mark.parametrize("path", ["cluster", "l2-nt128", "l2-nt256"])
+def test_c5_shape_vs_oracle(c5_case, path, monkeypatch):
     g, A, keys, ref = c5_case
-    monkeypatch.setenv("MCB_TC_NT", nt)
+    if path.startswith("l2"):
+        monkeypatch.setenv("MCB_NO_CLUSTER", "1")
+        monkeypatch.setenv("MCB_TC_NT", path[-3:])
     buf = ctypes.create_string_buffer(256)
     N.check(N.lib().mcb_tabucol_describe(2000, 150, 4, buf, 256))
-    assert b"tabucol_kernel" in buf.value  # k > 128 and gamma beyond shared memory
+    # k > 128 and gamma beyond one SM's shared memory: split over a 2-CTA
+    # cluster by default, else the CTA kernel with gamma in L2
+    assert (b"tabucol_cluster_kernel" if path == "cluster" else b"gamma in L2") in buf.value, buf.value
     got = LS._run_tabucol_batch(g, A.copy(), 150, keys, 3000, log_moves=True, counters=True)
-    _check(got, ref, f"c5/nt{nt}")
+    _check(got, ref, f"c5/{path}")
     assert (ref["iters_used"] == 3000).all()
 
 

@@ -22,6 +22,8 @@ ap.add_argument("--depth", type=int, default=20000)
 ap.add_argument("--n", type=int, default=500)
 ap.add_argument("--k", type=int, default=48)
 ap.add_argument("--philox", action="store_true")
+ap.add_argument("--cluster", action="store_true", help="force the 2-CTA cluster kernel (its own phase names)")
+ap.add_argument("--nodiag", action="store_true")
 a = ap.parse_args()
 g = rand_graph(1, a.n, 0.5)
 A = random_col_assigns(a.n, a.k, a.pop, 1)
@@ -29,7 +31,13 @@ dg = Dv.DeviceGraph(g, "cuda")
 keys = Dv.keys_to_tensor(stream_keys(1, TAG_LS, 0, a.pop), "cuda")
 buf = (ctypes.c_ulonglong * 16)()
 N.lib().mcb_debug_phase_cycles(buf, 1)
-flags = N.FLAG_DIAG | N.FLAG_PROFILE | (N.FLAG_PRODUCTION if a.philox else 0)
+wbuf = (ctypes.c_ulonglong * 96)()
+N.lib().mcb_debug_cluster_warps(wbuf, 1)
+flags = (0 if a.nodiag else N.FLAG_DIAG) | N.FLAG_PROFILE | (N.FLAG_PRODUCTION if a.philox else 0)
+if a.cluster:
+    flags |= N.FLAG_FORCE_CLUSTER
+    NAMES = {1: "pass1+#1", 2: "prefix/walk+#2", 3: "draw/locate+#3", 4: "move lane0", 5: "gamma update",
+             6: "list/best", 7: "tail", 8: "(p1 work r0)", 9: "(p1 work r1)"}
 t = torch.from_numpy(A).cuda()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record()
@@ -38,8 +46,18 @@ ev[1].record()
 torch.cuda.synchronize()
 N.check(N.lib().mcb_debug_phase_cycles(buf, 0))
 its = buf[10]
-tot = sum(buf[i] for i in range(1, 10))
+tot = sum(buf[i] for i in range(1, 8 if a.cluster else 10))
 print(f"iterations {its}, mean C {out['counters'][:,0].sum().item()/its:.1f}, "
       f"{tot/its:.0f} cycles/iteration (thread 0 view), kernel {ev[0].elapsed_time(ev[1]):.1f} ms")
 for i in range(1, 10):
     print(f"  {NAMES[i]:14s} {buf[i]/its:9.1f} cycles  {100*buf[i]/tot:5.1f}%")
+if a.cluster:
+    print(f"  spilled rows/iteration (rank 0) {buf[11]/its:.1f}, walked half-rows/iteration {buf[12]/its:.2f}, "
+          f"stale rescans {buf[13]/its:.1f}, masked scans {buf[14]/its:.2f} (rank 0)")
+if a.cluster:
+    N.check(N.lib().mcb_debug_cluster_warps(wbuf, 0))
+    cl = a.pop // 1  # rank-0 CTAs: one per individual
+    print("  per warp (rank 0, per iteration): pass-1 cycles / start delay / warp scans")
+    print("   " + " ".join(f"{wbuf[w]/its:6.0f}" for w in range(32) if wbuf[w]))
+    print("   " + " ".join(f"{wbuf[32+w]/its:6.0f}" for w in range(32) if wbuf[w]))
+    print("   " + " ".join(f"{wbuf[64+w]/its:6.2f}" for w in range(32) if wbuf[w]))
