@@ -65,7 +65,8 @@ struct ClCtrl {
     long long it, conflicts, best, nlog, sum_c, sum_deg, diag;
     unsigned long long ctr;
     long long s0, s1;
-    int C, wi, ovf, D, total, mv_v, mv_a, mv_b, gvb, plow;
+    int C, wi, ovf, D, mylow, mv_b, gvb, plow;
+    int smax[NW];
     int bmin[2][NW];  // per-warp block minima of the half-0 / half-1 records
     int beq[NW], blow[NW], bD[NW];
     long long red[NW];
@@ -83,149 +84,90 @@ struct ClLayout {
     int kh;
 };
 
-// One CTA's half of a conflicting row: local colours 0..KH-1 (bytes of KW
-// words), excluded ones (own colour, live tabu without aspiration, padding)
-// forced to 0xFF through a nibble -> byte-mask table.
-template <int KQ>
-struct HalfRow {
-    const uint8_t *g;
-    const uint32_t *lut;
-    int gva, KW;
-    uint64_t ex0, ex1;  // exclusion bits of colours 0-63 / 64-127 (scalars: an array went to local memory)
+// Word `lane` of row v's local half with its excluded colours forced to 0xFF:
+// the own colour (aloc >= 0) and live tabu colours without aspiration (their
+// g >= A = thr + gva, :336-339) -- from the 4 slots (cols / expiries tx) and,
+// when spl, the dense spilled row, each lane checking its own 4 colours.
+// Padding colours are 0xFF already.  Warp-cooperative: lanes >= KW get ~0.
+__device__ __forceinline__ uint32_t cl_word(const uint8_t *gamma, const uint16_t *gstamp, int KH, int v, int aloc,
+                                            uint32_t cols, uint2 tx, bool spl, int A, uint32_t it, int lane) {
+    const int KW = KH >> 2;
+    const uint8_t *gr = gamma + (size_t)v * KH;
+    const uint32_t x0 = lane < KW ? reinterpret_cast<const uint32_t *>(gr)[lane] : 0xFFFFFFFFu;
+    uint32_t x = x0;
+    if (aloc >= 0 && (aloc >> 2) == lane) x |= 0xFFu << (8 * (aloc & 3));
+    if (cols != 0xFFFFFFFFu) {
+        const uint16_t e[4] = {(uint16_t)tx.x, (uint16_t)(tx.x >> 16), (uint16_t)tx.y, (uint16_t)(tx.y >> 16)};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int t = (cols >> (8 * q)) & 0xFF;
+            if (t != 0xFF && (t >> 2) == lane && active<uint16_t>(e[q], it) && !((int)((x0 >> (8 * (t & 3))) & 0xFF) < A))
+                x |= 0xFFu << (8 * (t & 3));
+        }
+    }
+    if (spl && lane < KW) {
+        const uint16_t *gs = gstamp + (size_t)v * KH + 4 * lane;
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            if (active<uint16_t>(gs[e], it) && !((int)((x0 >> (8 * e)) & 0xFF) < A)) x |= 0xFFu << (8 * e);
+    }
+    return x;
+}
+// (minimum byte or 0xFF, #bytes at it) over the warp's words
+__device__ __forceinline__ void warp_min_count(uint32_t x, int &m, int &c) {
+    constexpr unsigned FULL = 0xffffffffu;
+    m = (int)__reduce_min_sync(FULL, min_bytes(x));
+    c = m == 0xFF ? 0 : (int)__reduce_add_sync(FULL, (unsigned)count_eq_bytes(x, (uint32_t)m));
+}
+// Tie events of the sequential scan over a half row (words x, lane = word)
+// entered with running minimum E (delta space): an exclusive prefix-min over
+// the words gives each lane the running minimum entering its word, then each
+// lane walks its 4 bytes (:340-350).
+__device__ __forceinline__ int walk_ties(uint32_t x, int E, int gva, int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int incl = warp_incl_min((int)min_bytes(x), lane);
+    int excl = __shfl_up_sync(FULL, incl, 1);
+    if (lane == 0) excl = INT_MAX;
+    int cur = min(E >= TC_BIG ? INT_MAX : E + gva, excl);
+    int t = 0;
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        const int b = (x >> (8 * e)) & 0xFF;
+        if (b == 0xFF) continue;
+        if (b < cur) cur = b;
+        else if (b == cur) t++;
+    }
+    return __reduce_add_sync(FULL, t);
+}
+// local column of the need-th byte equal to Dg in word order, or -1
+__device__ __forceinline__ int locate_col(uint32_t x, int Dg, int need, int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int c = count_eq_bytes(x, (uint32_t)Dg);
+    const int incl = warp_incl_sum(c, lane);
+    const unsigned bm = __ballot_sync(FULL, incl >= need);
+    if (!bm) return -1;
+    const int src = __ffs(bm) - 1;
+    int col = -1;
+    if (lane == src) {
+        int r = need - (incl - c);
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            if ((int)((x >> (8 * e)) & 0xFF) == Dg && --r == 0 && col < 0) col = 4 * lane + e;
+    }
+    return __shfl_sync(FULL, col, src);
+}
 
-    __device__ __forceinline__ void setbit(int c) {
-        const uint64_t b = 1ull << (c & 63);
-        if (KQ == 1 || c < 64) ex0 |= b;
-        else ex1 |= b;
-    }
-    __device__ __forceinline__ uint64_t exq(int q) const { return (KQ == 1 || q == 0) ? ex0 : ex1; }
-    __device__ __forceinline__ uint32_t word(int w) const {
-        return reinterpret_cast<const uint32_t *>(g)[w] | lut[(uint32_t)(exq(w >> 4) >> (4 * (w & 15))) & 0xFu];
-    }
-    // aloc: the own colour's local index, or -1 when the other CTA holds it
-    __device__ __forceinline__ void init(const uint8_t *gamma, const uint16_t *texp, const uint8_t *tcol,
-                                         const uint16_t *tovf, const uint16_t *gstamp, int v, int aloc, int gva_,
-                                         int KH, uint32_t it, int thr, const uint32_t *lut_) {
-        lut = lut_;
-        KW = KH >> 2;
-        g = gamma + (size_t)v * KH;
-        gva = gva_;
-        const int A = thr + gva;  // tabu colour c is admissible iff g_c < A (:336-339)
-        ex0 = ex1 = 0;
-        if (aloc >= 0) setbit(aloc);
-        const uint32_t cols = reinterpret_cast<const uint32_t *>(tcol)[v];
-        if (cols != 0xFFFFFFFFu) {
-            const uint2 x = reinterpret_cast<const uint2 *>(texp)[v];
-            const uint16_t e[4] = {(uint16_t)x.x, (uint16_t)(x.x >> 16), (uint16_t)x.y, (uint16_t)(x.y >> 16)};
-#pragma unroll
-            for (int s = 0; s < 4; s++) {
-                const int c = (cols >> (8 * s)) & 0xFF;
-                if (c != 0xFF && active<uint16_t>(e[s], it) && !((int)g[c] < A)) setbit(c);
-            }
-        }
-        if (active<uint16_t>(tovf[v], it)) {  // spilled expiries (dense global row)
-            const uint16_t *gs = gstamp + (size_t)v * KH;
-            for (int c = 0; c < KH; c++)
-                if (active<uint16_t>(gs[c], it) && !((int)g[c] < A)) setbit(c);
-        }
-    }
-    // own colour excluded only (the row cache)
-    __device__ __forceinline__ void init_own(const uint8_t *gamma, int v, int aloc, int gva_, int KH,
-                                             const uint32_t *lut_) {
-        lut = lut_;
-        KW = KH >> 2;
-        g = gamma + (size_t)v * KH;
-        gva = gva_;
-        ex0 = ex1 = 0;
-        if (aloc >= 0) setbit(aloc);
-    }
-    // (minimum g or 0xFF, #columns at it) over the non-excluded columns
-    __device__ __forceinline__ void min_count_raw(int &m, int &c) const {
-        m = 0xFF;
-        c = 0;
-#pragma unroll 4
-        for (int w = 0; w < KW; w++) {
-            const uint32_t x = word(w);
-            const int wm = (int)min_bytes(x);
-            const int wc = count_eq_bytes(x, (uint32_t)wm);
-            c = (wm < m) ? wc : (wm == m ? c + wc : c);
-            m = min(m, wm);
-        }
-    }
-    // (minimum g or 0xFF, #columns at it), warp-cooperative: lane = word
-    __device__ __forceinline__ void warp_min_count(int lane, int &m, int &c) const {
-        constexpr unsigned FULL = 0xffffffffu;
-        const uint32_t x = lane < KW ? word(lane) : 0xFFFFFFFFu;
-        m = (int)__reduce_min_sync(FULL, min_bytes(x));
-        c = m == 0xFF ? 0 : (int)__reduce_add_sync(FULL, (unsigned)count_eq_bytes(x, (uint32_t)m));
-    }
-    // (minimum delta or TC_BIG, #admissible candidates at it)
-    __device__ __forceinline__ void min_count(int &rmin, int &cnt) const {
-        int m = 0xFF, c = 0;
-#pragma unroll 4
-        for (int w = 0; w < KW; w++) {
-            const uint32_t x = word(w);
-            const int wm = (int)min_bytes(x);
-            const int wc = count_eq_bytes(x, (uint32_t)wm);
-            c = (wm < m) ? wc : (wm == m ? c + wc : c);
-            m = min(m, wm);
-        }
-        rmin = (m == 0xFF) ? TC_BIG : m - gva;
-        cnt = (m == 0xFF) ? 0 : c;
-    }
-    // tie events of the sequential scan over this half entered with running
-    // minimum E (delta space), warp-cooperative: lane = word (KW <= 32)
-    __device__ __forceinline__ int walk(int E, int lane) const {
-        constexpr unsigned FULL = 0xffffffffu;
-        const uint32_t x = lane < KW ? word(lane) : 0xFFFFFFFFu;
-        const int incl = warp_incl_min((int)min_bytes(x), lane);
-        int excl = __shfl_up_sync(FULL, incl, 1);
-        if (lane == 0) excl = INT_MAX;
-        int cur = min(E >= TC_BIG ? INT_MAX : E + gva, excl);
-        int t = 0;
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            const int b = (x >> (8 * e)) & 0xFF;
-            if (b == 0xFF) continue;
-            if (b < cur) cur = b;
-            else if (b == cur) t++;
-        }
-        return __reduce_add_sync(FULL, t);
-    }
-    // local column of the need-th candidate equal to Dg (warp-cooperative)
-    __device__ __forceinline__ int locate(int Dg, int need, int lane) const {
-        constexpr unsigned FULL = 0xffffffffu;
-        const uint32_t x = lane < KW ? word(lane) : 0xFFFFFFFFu;
-        const int c = count_eq_bytes(x, (uint32_t)Dg);
-        const int incl = warp_incl_sum(c, lane);
-        const unsigned bm = __ballot_sync(FULL, incl >= need);
-        if (!bm) return -1;
-        const int src = __ffs(bm) - 1;
-        int col = -1;
-        if (lane == src) {
-            int r = need - (incl - c);
-#pragma unroll
-            for (int e = 0; e < 4; e++)
-                if ((int)((x >> (8 * e)) & 0xFF) == Dg && --r == 0 && col < 0) col = 4 * lane + e;
-        }
-        return __shfl_sync(FULL, col, src);
-    }
-};
-
-template <int KQ, int NT>
+template <int NT>
 __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, ClLayout L) {
     constexpr int NW = NT / 32;
     constexpr unsigned FULL = 0xffffffffu;
-    using HR = HalfRow<KQ>;
 
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ ClCtrl<NW> ctl;
-    __shared__ uint32_t s_nib[16];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid < 16) s_nib[tid] = expand_nibble(tid);
     if (tid == 0) ctl.ovf = 0;
 
     const int n = P.n, k = P.k, KH = L.kh;
@@ -290,6 +232,7 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
         int32_t *b_out = P.best_assigns + (size_t)ind * n;
 
         // ---------------- init (localsearch.py:289-318) ----------------
+        const long long t_init = prof0 ? clock64() : 0;
         for (int v = tid; v < n; v += NT) {
             int c = a_io[v];
             if (c < 0 || c >= k) {
@@ -390,6 +333,7 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
         if (rank == 0)
             for (int v = tid; v < n; v += NT) b_out[v] = assign[v];
         cluster.sync();  // both halves built; an init overflow is visible to both
+        if (prof0) atomicAdd(&g_cl_cycles[15], (unsigned long long)(clock64() - t_init));
 
         // ---------------- iterations (:320-405) ----------------
         if (k >= 2 && !ctl.ovf) {
@@ -415,79 +359,109 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
                 unsigned n_scans = 0;
                 {
                     int bm = TC_BIG;
-                    for (int l0 = b0; l0 < b1; l0 += 32) {
-                        const int li = l0 + lane;
-                        const bool on = li < b1;
-                        const int v = on ? clist[li] : 0;
-                        const int aloc = local_col(assign[v]);
-                        const int gv = gva[v];
-                        const uint8_t *gr = gamma + (size_t)v * KH;
-                        uint32_t h = on ? hc[v] : 0x1FFu;
-                        // stale cache rows: rescanned by the whole warp, one row at a time
-                        for (unsigned sm = __ballot_sync(FULL, (h >> 8) == 0); sm; sm &= sm - 1) {
-                            const int src = __ffs(sm) - 1;
-                            const int vs = __shfl_sync(FULL, v, src);
-                            HR re;
-                            re.init_own(gamma, vs, __shfl_sync(FULL, aloc, src), 0, KH, s_nib);
-                            int m, c;
-                            re.warp_min_count(lane, m, c);
-                            if (lane == src) {
-                                h = (uint32_t)m | (uint32_t)(m == 0xFF ? 1 : c) << 8;
-                                hc[v] = (uint16_t)h;
-                            }
-                            n_stale += prof && lane == 0;
-                            n_scans++;
-                        }
-                        int m = (int)(h & 0xFFu), c = (int)(h >> 8);
-                        bool masked = false;
-                        if (on && m != 0xFF) {
-                            // live tabu colours at the minimum without aspiration
-                            // (g < thr + gva admits them, :336-339) leave the group
-                            const bool adm = m < thr + gv;
-                            const uint32_t cols = reinterpret_cast<const uint32_t *>(tcol)[v];
-                            if (!adm && cols != 0xFFFFFFFFu) {
-                                const uint2 x = reinterpret_cast<const uint2 *>(texp)[v];
-                                const uint16_t e[4] = {(uint16_t)x.x, (uint16_t)(x.x >> 16), (uint16_t)x.y,
-                                                       (uint16_t)(x.y >> 16)};
+                    // up to 4 rows per lane in flight: their dependent shared-memory
+                    // chains (list -> vertex -> cache / slots -> slot columns) overlap
+                    constexpr int R = 4;
+                    for (int c0 = b0; c0 < b1; c0 += 32 * R) {
+                        int v[R], aloc[R], gv[R], m[R], c[R];
+                        uint32_t h[R], cols[R];
+                        uint2 tx[R];
+                        bool on[R], spl[R], masked[R];
 #pragma unroll
-                                for (int q = 0; q < 4; q++) {
-                                    const int t = (cols >> (8 * q)) & 0xFF;
-                                    if (t != 0xFF && t != aloc && gr[t] == m && active<uint16_t>(e[q], it32)) c--;
+                        for (int r = 0; r < R; r++) {
+                            const int li = c0 + 32 * r + lane;
+                            on[r] = li < b1;
+                            v[r] = on[r] ? clist[li] : 0;
+                        }
+#pragma unroll
+                        for (int r = 0; r < R; r++) {
+                            aloc[r] = local_col(assign[v[r]]);
+                            gv[r] = gva[v[r]];
+                            h[r] = on[r] ? hc[v[r]] : 0x1FFu;
+                            cols[r] = reinterpret_cast<const uint32_t *>(tcol)[v[r]];
+                            tx[r] = reinterpret_cast<const uint2 *>(texp)[v[r]];
+                            spl[r] = active<uint16_t>(tovf[v[r]], it32);
+                        }
+                        // stale cache rows: rescanned by the whole warp (own colour excluded)
+#pragma unroll
+                        for (int r = 0; r < R; r++) {
+                            for (unsigned sm = __ballot_sync(FULL, (h[r] >> 8) == 0); sm; sm &= sm - 1) {
+                                const int src = __ffs(sm) - 1;
+                                const uint32_t x = cl_word(gamma, gstamp, KH, __shfl_sync(FULL, v[r], src),
+                                                           __shfl_sync(FULL, aloc[r], src), 0xFFFFFFFFu,
+                                                           make_uint2(0, 0), false, 0, it32, lane);
+                                int wm, wc;
+                                warp_min_count(x, wm, wc);
+                                if (lane == src) {
+                                    h[r] = (uint32_t)wm | (uint32_t)(wm == 0xFF ? 1 : wc) << 8;
+                                    hc[v[r]] = (uint16_t)h[r];
                                 }
+                                n_stale += prof && lane == 0;
+                                n_scans++;
                             }
-                            const bool spl = active<uint16_t>(tovf[v], it32);
-                            if (prof) n_spill += spl;
-                            if (!adm && spl) {
-                                const uint16_t *gs = gstamp + (size_t)v * KH;
-                                for (int t = 0; t < KH; t++)
-                                    if (t != aloc && gr[t] == m && active<uint16_t>(gs[t], it32)) c--;
+                        }
+#pragma unroll
+                        for (int r = 0; r < R; r++) {
+                            m[r] = (int)(h[r] & 0xFFu);
+                            c[r] = (int)(h[r] >> 8);
+                            masked[r] = false;
+                            if (on[r] && m[r] != 0xFF) {
+                                // live tabu colours at the minimum without aspiration
+                                // (g < thr + gva admits them, :336-339) leave the group
+                                const bool adm = m[r] < thr + gv[r];
+                                const uint8_t *gr = gamma + (size_t)v[r] * KH;
+                                if (!adm && cols[r] != 0xFFFFFFFFu) {
+                                    const uint16_t e[4] = {(uint16_t)tx[r].x, (uint16_t)(tx[r].x >> 16),
+                                                           (uint16_t)tx[r].y, (uint16_t)(tx[r].y >> 16)};
+#pragma unroll
+                                    for (int q = 0; q < 4; q++) {
+                                        const int t = (cols[r] >> (8 * q)) & 0xFF;
+                                        if (t != 0xFF && t != aloc[r] && gr[t] == m[r] && active<uint16_t>(e[q], it32))
+                                            c[r]--;
+                                    }
+                                }
+                                if (prof) n_spill += spl[r];
+                                if (!adm && spl[r]) {
+                                    const uint16_t *gs = gstamp + (size_t)v[r] * KH;
+                                    for (int t = 0; t < KH; t++)
+                                        if (t != aloc[r] && gr[t] == m[r] && active<uint16_t>(gs[t], it32)) c[r]--;
+                                }
+                                masked[r] = c[r] == 0;
+                                m[r] -= gv[r];
+                            } else {
+                                m[r] = TC_BIG;
+                                c[r] = 0;
                             }
-                            masked = c == 0;
-                            m -= gv;
-                        } else {
-                            m = TC_BIG;
-                            c = 0;
                         }
                         // rows whose whole minimum group is tabu: masked scan by the warp
-                        for (unsigned mm = __ballot_sync(FULL, masked); mm; mm &= mm - 1) {
-                            const int src = __ffs(mm) - 1;
-                            const int vs = __shfl_sync(FULL, v, src);
-                            HR re;
-                            re.init(gamma, texp, tcol, tovf, gstamp, vs, __shfl_sync(FULL, aloc, src),
-                                    __shfl_sync(FULL, gv, src), KH, it32, thr, s_nib);
-                            int wm, wc;
-                            re.warp_min_count(lane, wm, wc);
-                            if (lane == src) {
-                                m = wm == 0xFF ? TC_BIG : wm - gv;
-                                c = wc;
+                        // (per-lane scans of these rows measured slower: 19 dependent
+                        // word steps per lane against one word per lane and two REDUX)
+#pragma unroll
+                        for (int r = 0; r < R; r++) {
+                            for (unsigned mm = __ballot_sync(FULL, masked[r]); mm; mm &= mm - 1) {
+                                const int src = __ffs(mm) - 1;
+                                const int gs = __shfl_sync(FULL, gv[r], src);
+                                const uint32_t x = cl_word(
+                                    gamma, gstamp, KH, __shfl_sync(FULL, v[r], src), __shfl_sync(FULL, aloc[r], src),
+                                    __shfl_sync(FULL, cols[r], src),
+                                    make_uint2(__shfl_sync(FULL, tx[r].x, src), __shfl_sync(FULL, tx[r].y, src)),
+                                    __shfl_sync(FULL, spl[r], src), thr + gs, it32, lane);
+                                int wm, wc;
+                                warp_min_count(x, wm, wc);
+                                if (lane == src) {
+                                    m[r] = wm == 0xFF ? TC_BIG : wm - gs;
+                                    c[r] = wc;
+                                }
+                                n_mask += prof && lane == 0;
+                                n_scans++;
                             }
-                            n_mask += prof && lane == 0;
-                            n_scans++;
                         }
-                        if (on) {
-                            const uint32_t rec = rec_pack(m, c, (uint32_t *)nullptr);
-                            rown[li] = rec;
-                            bm = min(bm, m);
+#pragma unroll
+                        for (int r = 0; r < R; r++) {
+                            if (on[r]) {
+                                rown[c0 + 32 * r + lane] = rec_pack(m[r], c[r], (uint32_t *)nullptr);
+                                bm = min(bm, m[r]);
+                            }
                         }
                     }
                     bm = __reduce_min_sync(FULL, bm);
@@ -554,10 +528,12 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
                             const int src = __ffs(wm) - 1;
                             const int Es = __shfl_sync(FULL, E, src);
                             const int v = clist[q0 + src];
-                            HR re;
-                            re.init(gamma, texp, tcol, tovf, gstamp, v, local_col(assign[v]), gva[v], KH, it32, thr,
-                                    s_nib);
-                            const int t = re.walk(Es, lane);
+                            const int gvv = gva[v];
+                            const uint32_t x = cl_word(gamma, gstamp, KH, v, local_col(assign[v]),
+                                                       reinterpret_cast<const uint32_t *>(tcol)[v],
+                                                       reinterpret_cast<const uint2 *>(texp)[v],
+                                                       active<uint16_t>(tovf[v], it32), thr + gvv, it32, lane);
+                            const int t = walk_ties(x, Es, gvv, lane);
                             if (lane == 0) {
                                 low += t;
                                 n_walk += prof;
@@ -579,226 +555,244 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
                 if (warp == 0) {
                     const int lw = __reduce_add_sync(FULL, lane < NW ? ctl.blow[lane] : 0);
                     if (lane == 0) ctl_peer->plow = lw;
-                    if (lane == 0) ctl.total = lw;
+                    if (lane == 0) ctl.mylow = lw;
                 }
                 cluster.sync();  // #2: the partner's walk events
                 CLPH(2);
 
-                // the reservoir draw and the winner (warp 0 of both CTAs, same result);
-                // the CTA owning the winner's half locates its column
-                if (warp == 0) {
-                    const int D = ctl.D;
-                    int mv_v = -1;
-                    if (D < TC_BIG) {
-                        const int T = __reduce_add_sync(FULL, lane < NW ? ctl.bD[lane] : 0);
-                        const int total =
-                            __reduce_add_sync(FULL, lane < NW ? ctl.beq[lane] : 0) + ctl.total + ctl.plow;
-                        const unsigned long long ctr = ctl.ctr;
-                        int sstar = 1;
-                        if (T > 1) {
-                            if (!prod) {
-                                const unsigned long long c0 = ctr + (unsigned long long)(total - (T - 1));
-                                int smax = 1;
-                                for (int s = 2 + lane; s <= T; s += 32)
-                                    if (below_is_zero(key, c0 + (unsigned long long)(s - 2), (uint32_t)s)) smax = s;
-                                sstar = __reduce_max_sync(FULL, smax);
-                            } else {
-                                sstar = 1 + (int)philox_below(key, ctr, (uint32_t)T);
-                            }
-                        }
-                        // block, then row, then half holding the sstar-th D-candidate
-                        const int cj = lane < NW ? ctl.bD[lane] : 0;
-                        const int cin = warp_incl_sum(cj, lane);
-                        const int wb = __ffs(__ballot_sync(FULL, cin >= sstar)) - 1;
-                        int need = sstar - __shfl_sync(FULL, cin - cj, wb);
-                        const int r0 = min(C, wb * BS), r1 = min(C, r0 + BS);
-                        int row = -1;
-                        int2 rh0 = make_int2(TC_BIG, 0);
-                        for (int q0 = r0; q0 < r1 && row < 0; q0 += 32) {
-                            const int q = q0 + lane;
-                            int2 h0 = make_int2(TC_BIG, 0), h1 = make_int2(TC_BIG, 0);
-                            if (q < r1) {
-                                h0 = rec_unpack(rlo[q]);
-                                h1 = rec_unpack(rhi[q]);
-                            }
-                            const int x = min(h0.x, h1.x);
-                            const int y = (x == D) ? (h0.x == x ? h0.y : 0) + (h1.x == x ? h1.y : 0) : 0;
-                            const int inc = warp_incl_sum(y, lane);
-                            const unsigned bm = __ballot_sync(FULL, inc >= need);
-                            if (bm) {
-                                const int src = __ffs(bm) - 1;
-                                row = q0 + src;
-                                need -= __shfl_sync(FULL, inc - y, src);
-                                rh0.x = __shfl_sync(FULL, h0.x, src);
-                                rh0.y = __shfl_sync(FULL, h0.y, src);
-                            } else {
-                                need -= __shfl_sync(FULL, inc, 31);
-                            }
-                        }
-                        if (row >= 0) {
-                            mv_v = clist[row];
-                            const int c0d = rh0.x == D ? rh0.y : 0;
-                            const int owner = need <= c0d ? 0 : 1;
-                            if (owner == rank) {
-                                HR re;
-                                re.init(gamma, texp, tcol, tovf, gstamp, mv_v, local_col(assign[mv_v]), gva[mv_v], KH,
-                                        it32, thr, s_nib);
-                                const int col = re.locate(D + re.gva, owner ? need - c0d : need, lane);
-                                if (lane == 0) both(&ClCtrl<NW>::mv_b, col < 0 ? -1 : cb + col);
-                            }
-                        }
-                        if (lane == 0) ctl.total = total;
+                // the reservoir draw (:340-350) spread over all warps, then every warp
+                // derives the same winner row; the CTA owning the winner's half
+                // locates its column while all threads prefetch N(v*)
+                const int D = ctl.D;
+                const unsigned long long ctr = ctl.ctr;
+                int T = 0, total = 0, mv_v = -1, need = 0, c0d = 0;
+                if (D < TC_BIG) {
+                    T = __reduce_add_sync(FULL, lane < NW ? ctl.bD[lane] : 0);
+                    total = __reduce_add_sync(FULL, lane < NW ? ctl.beq[lane] : 0) + ctl.mylow + ctl.plow;
+                    int smax = 1;
+                    if (T > 1 && !prod) {
+                        const unsigned long long c0 = ctr + (unsigned long long)(total - (T - 1));
+                        for (int s = 2 + tid; s <= T; s += NT)
+                            if (below_is_zero(key, c0 + (unsigned long long)(s - 2), (uint32_t)s)) smax = s;
                     }
-                    if (lane == 0) ctl.mv_v = mv_v;
+                    smax = __reduce_max_sync(FULL, smax);
+                    if (lane == 0) ctl.smax[warp] = smax;
+                }
+                __syncthreads();
+                if (D < TC_BIG) {
+                    int sstar = 1;
+                    if (T > 1)
+                        sstar = prod ? 1 + (int)philox_below(key, ctr, (uint32_t)T)
+                                     : (int)__reduce_max_sync(FULL, lane < NW ? ctl.smax[lane] : 1);
+                    // block, then row, then half holding the sstar-th D-candidate
+                    const int cj = lane < NW ? ctl.bD[lane] : 0;
+                    const int cin = warp_incl_sum(cj, lane);
+                    const int wb = __ffs(__ballot_sync(FULL, cin >= sstar)) - 1;
+                    need = sstar - __shfl_sync(FULL, cin - cj, wb);
+                    const int r0 = min(C, wb * BS), r1 = min(C, r0 + BS);
+                    for (int q0 = r0; q0 < r1 && mv_v < 0; q0 += 32) {
+                        const int q = q0 + lane;
+                        int2 h0 = make_int2(TC_BIG, 0), h1 = make_int2(TC_BIG, 0);
+                        if (q < r1) {
+                            h0 = rec_unpack(rlo[q]);
+                            h1 = rec_unpack(rhi[q]);
+                        }
+                        const int x = min(h0.x, h1.x);
+                        const int y = (x == D) ? (h0.x == x ? h0.y : 0) + (h1.x == x ? h1.y : 0) : 0;
+                        const int inc = warp_incl_sum(y, lane);
+                        const unsigned bm = __ballot_sync(FULL, inc >= need);
+                        if (bm) {
+                            const int src = __ffs(bm) - 1;
+                            mv_v = clist[q0 + src];
+                            need -= __shfl_sync(FULL, inc - y, src);
+                            const int h0x = __shfl_sync(FULL, h0.x, src), h0y = __shfl_sync(FULL, h0.y, src);
+                            c0d = h0x == D ? h0y : 0;
+                        } else {
+                            need -= __shfl_sync(FULL, inc, 31);
+                        }
+                    }
+                }
+                // N(v*): update threads (warps 1..) hold their neighbours in registers
+                constexpr int NBR = 4;
+                int64_t g0 = 0, g1 = 0;
+                int nb[NBR];
+                if (mv_v >= 0) {
+                    g0 = P.indptr[mv_v];
+                    g1 = P.indptr[mv_v + 1];
+                }
+#pragma unroll
+                for (int q = 0; q < NBR; q++) {
+                    const int64_t j = g0 + (tid - 32) + (int64_t)q * (NT - 32);
+                    nb[q] = (warp > 0 && j < g1) ? __ldg(P.indices + j) : 0;
+                }
+                if (warp == 0 && mv_v >= 0) {
+                    const int owner = need <= c0d ? 0 : 1;
+                    if (owner == rank) {
+                        const int gvv = gva[mv_v];
+                        const uint32_t x = cl_word(gamma, gstamp, KH, mv_v, local_col(assign[mv_v]),
+                                                   reinterpret_cast<const uint32_t *>(tcol)[mv_v],
+                                                   reinterpret_cast<const uint2 *>(texp)[mv_v],
+                                                   active<uint16_t>(tovf[mv_v], it32), thr + gvv, it32, lane);
+                        const int col = locate_col(x, D + gvv, owner ? need - c0d : need, lane);
+                        if (lane == 0) both(&ClCtrl<NW>::mv_b, col < 0 ? -1 : cb + col);
+                    }
                 }
                 cluster.sync();  // #3: the column from its owner
                 CLPH(3);
 
-                // the move (:352-396): tenure, tabu entry (owner of colour a), counters
-                const int mvv = ctl.mv_v;
-                if (mvv >= 0 && tid == 0) {
-                    const int v = mvv, a = assign[v], D = ctl.D;
-                    int b = ctl.mv_b;
-                    const long long nconf = conflicts + D;
-                    unsigned long long c = ctl.ctr;
-                    uint32_t ll;
-                    if (!prod) {
-                        c += (unsigned long long)ctl.total;
-                        ll = u64_below32(key, c, 10u);
-                        c += 1;
-                    } else {
-                        ll = philox_below(key, c + 1, 10u);
-                        c += 2;
-                    }
-                    const long long tt = (long long)ll + (6LL * nconf) / 10LL;
-                    if (tt >= (long long)CL_SWEEP || b < 0) ctl.ovf = 1;
-                    if (b < 0) b = a;
-                    const int al = local_col(a);
-                    if (al >= 0) {  // tabu (v, a) until it + tt + 1: slot hit, free slot, or spill
-                        const uint16_t e_new = (uint16_t)(uint32_t)(it + tt + 1);
-                        const uint32_t cols = reinterpret_cast<const uint32_t *>(tcol)[v];
-                        int s_hit = -1, s_free = -1;
-#pragma unroll
-                        for (int s = 0; s < 4; s++) {
-                            const int cs = (cols >> (8 * s)) & 0xFF;
-                            if (cs == al) s_hit = s;
-                            else if (s_free < 0 && (cs == 0xFF || !active<uint16_t>(texp[4 * v + s], it32)))
-                                s_free = s;
-                        }
-                        const int s = s_hit >= 0 ? s_hit : s_free;
-                        const bool ovf_live = active<uint16_t>(tovf[v], it32);
-                        if (s >= 0) {
-                            tcol[4 * v + s] = (uint8_t)al;
-                            texp[4 * v + s] = e_new;
-                            if (ovf_live) gstamp[(size_t)v * KH + al] = (uint16_t)it32;  // supersede
-                        } else {
-                            spill_set<uint16_t>(gstamp + (size_t)v * KH, tovf + v, ovf_live, KH, al, e_new, it32);
-                        }
-                    }
-                    ctl.gvb = gva[v] + D;  // gamma[v][b] (row v is not changed by its own move)
-                    assign[v] = (uint8_t)b;
-                    hc[v] = 0;  // its own colour changed
-                    ctl.conflicts = nconf;
-                    ctl.ctr = c;
-                    const long long nl = ctl.nlog;
-                    if (nl < P.log_cap) {
-                        if (rank == 0) {
-                            const size_t o = (size_t)ind * P.log_cap + nl;
-                            P.log_v[o] = v;
-                            P.log_iter[o] = it;
-                            P.log_tt[o] = tt;
-                        }
-                        ctl.nlog = nl + 1;
-                    }
-                    ctl.s0 = P.indptr[v];
-                    ctl.s1 = P.indptr[v + 1];
-                    ctl.sum_deg += ctl.s1 - ctl.s0;
-                    ctl.mv_a = a;
-                    ctl.mv_b = b;
-                }
-                CLPH(4);
-                __syncthreads();
-                // gamma (this CTA's colours) and gva over N(v) (:356-359); ballots of
-                // conflict-set events per 32 consecutive neighbours
+                // the move (:352-396).  Warp 0: tenure, tabu entry (owner of colour a),
+                // counters, log; warps 1..: gamma (this CTA's colours), gva and the row
+                // cache over N(v) (:356-359) with ballots of conflict-set events per 32
+                // neighbours, and the best copy (:387-390).  assign[v] changes after the
+                // next barrier (the update reads the old colours).
+                const int mvv = mv_v;
+                bool improved = false;
                 if (mvv >= 0) {
-                    const int ma = ctl.mv_a, mb = ctl.mv_b;
-                    const int al = local_col(ma), bl = local_col(mb);
-                    const int64_t s0 = ctl.s0;
-                    const int deg = (int)(ctl.s1 - s0);
-                    bool bad = false;
-                    for (int j0 = 0; j0 < deg; j0 += NT) {
-                        const int j = j0 + tid;
-                        bool evt = false;
-                        if (j < deg) {
-                            const int u = __ldg(P.indices + s0 + j);
-                            nbs[j] = (uint16_t)u;
-                            uint8_t *gr = gamma + (size_t)u * KH;
-                            const int au = assign[u];
-                            uint32_t h = hc[u];
-                            int hm = (int)(h & 0xFFu), hn = (int)(h >> 8);
-                            if (al >= 0) {
-                                const int ga = gr[al] - 1;
-                                gr[al] = (uint8_t)ga;
-                                if (au != ma && hn != 0) {
-                                    hn = ga < hm ? 1 : hn + (ga == hm);
-                                    hm = min(hm, ga);
+                    const int ma = assign[mvv];
+                    int mb = ctl.mv_b;
+                    const long long nconf = conflicts + D;
+                    improved = nconf < best;
+                    const int deg = (int)(g1 - g0);
+                    if (warp == 0) {
+                        if (lane == 0) {
+                            unsigned long long c = ctr;
+                            uint32_t ll;
+                            if (!prod) {
+                                c += (unsigned long long)total;
+                                ll = u64_below32(key, c, 10u);
+                                c += 1;
+                            } else {
+                                ll = philox_below(key, c + 1, 10u);
+                                c += 2;
+                            }
+                            const long long tt = (long long)ll + (6LL * nconf) / 10LL;
+                            if (tt >= (long long)CL_SWEEP || mb < 0) ctl.ovf = 1;
+                            const int v = mvv, al = local_col(ma);
+                            if (al >= 0) {  // tabu (v, a) until it + tt + 1: slot hit, free slot, or spill
+                                const uint16_t e_new = (uint16_t)(uint32_t)(it + tt + 1);
+                                const uint32_t cols = reinterpret_cast<const uint32_t *>(tcol)[v];
+                                int s_hit = -1, s_free = -1;
+#pragma unroll
+                                for (int s = 0; s < 4; s++) {
+                                    const int cs = (cols >> (8 * s)) & 0xFF;
+                                    if (cs == al) s_hit = s;
+                                    else if (s_free < 0 && (cs == 0xFF || !active<uint16_t>(texp[4 * v + s], it32)))
+                                        s_free = s;
+                                }
+                                const int s = s_hit >= 0 ? s_hit : s_free;
+                                const bool ovf_live = active<uint16_t>(tovf[v], it32);
+                                if (s >= 0) {
+                                    tcol[4 * v + s] = (uint8_t)al;
+                                    texp[4 * v + s] = e_new;
+                                    if (ovf_live) gstamp[(size_t)v * KH + al] = (uint16_t)it32;  // supersede
+                                } else {
+                                    spill_set<uint16_t>(gstamp + (size_t)v * KH, tovf + v, ovf_live, KH, al, e_new,
+                                                        it32);
                                 }
                             }
-                            if (bl >= 0) {
-                                const int gb = gr[bl];
-                                if (gb >= CL_GMAX) bad = true;
-                                else gr[bl] = (uint8_t)(gb + 1);
-                                if (au != mb && hn != 0 && gb == hm) hn--;  // 0: stale
+                            ctl.gvb = gva[v] + D;  // gamma[v][b] (row v is not changed by its own move)
+                            hc[v] = 0;             // its own colour changes
+                            ctl.conflicts = nconf;
+                            ctl.ctr = c;
+                            const long long nl = ctl.nlog;
+                            if (nl < P.log_cap) {
+                                if (rank == 0) {
+                                    const size_t o = (size_t)ind * P.log_cap + nl;
+                                    P.log_v[o] = v;
+                                    P.log_iter[o] = it;
+                                    P.log_tt[o] = tt;
+                                }
+                                ctl.nlog = nl + 1;
                             }
-                            hc[u] = (uint16_t)(hm | hn << 8);
-                            if (au == ma) {
-                                const int g = gva[u] - 1;
-                                gva[u] = (uint8_t)g;
-                                evt = g == 0;
-                            } else if (au == mb) {
-                                const int g = gva[u];
-                                if (g >= CL_GMAX) bad = true;
-                                else gva[u] = (uint8_t)(g + 1);
-                                evt = g == 0;
-                            }
+                            ctl.sum_deg += deg;
                         }
-                        const unsigned em = __ballot_sync(FULL, evt);
-                        if (lane == 0) evm[(j0 >> 5) + warp] = em;
+                    } else {
+                        if (mb < 0) mb = ma;  // (overflow path: the individual is re-run)
+                        const int al = local_col(ma), bl = local_col(mb);
+                        bool bad = false;
+                        for (int q = 0; q * (NT - 32) < deg; q++) {
+                            const int j = (tid - 32) + q * (NT - 32);
+                            bool evt = false;
+                            if (j < deg) {
+                                int u = 0;
+#pragma unroll
+                                for (int r = 0; r < NBR; r++)
+                                    if (q == r) u = nb[r];
+                                if (q >= NBR) u = __ldg(P.indices + g0 + j);
+                                nbs[j] = (uint16_t)u;
+                                uint8_t *gr = gamma + (size_t)u * KH;
+                                const int au = assign[u];
+                                uint32_t h = hc[u];
+                                int hm = (int)(h & 0xFFu), hn = (int)(h >> 8);
+                                if (al >= 0) {
+                                    const int ga = gr[al] - 1;
+                                    gr[al] = (uint8_t)ga;
+                                    if (au != ma && hn != 0) {
+                                        hn = ga < hm ? 1 : hn + (ga == hm);
+                                        hm = min(hm, ga);
+                                    }
+                                }
+                                if (bl >= 0) {
+                                    const int gb = gr[bl];
+                                    if (gb >= CL_GMAX) bad = true;
+                                    else gr[bl] = (uint8_t)(gb + 1);
+                                    if (au != mb && hn != 0 && gb == hm) hn--;  // 0: stale
+                                }
+                                hc[u] = (uint16_t)(hm | hn << 8);
+                                if (au == ma) {
+                                    const int g = gva[u] - 1;
+                                    gva[u] = (uint8_t)g;
+                                    evt = g == 0;
+                                } else if (au == mb) {
+                                    const int g = gva[u];
+                                    if (g >= CL_GMAX) bad = true;
+                                    else gva[u] = (uint8_t)(g + 1);
+                                    evt = g == 0;
+                                }
+                            }
+                            const unsigned em = __ballot_sync(FULL, evt);
+                            if (lane == 0) evm[q * (NW - 1) + warp - 1] = em;
+                        }
+                        if (bad) both(&ClCtrl<NW>::ovf, 1);
+                        if (rank == 0 && improved)
+                            for (int u = tid - 32; u < n; u += NT - 32) b_out[u] = u == mvv ? mb : assign[u];
                     }
-                    if (bad) both(&ClCtrl<NW>::ovf, 1);
                 }
                 __syncthreads();
-                CLPH(5);
-                // conflict-list events in neighbour order, then v (:368-385); best (:387-390)
+                CLPH(4);
+                // conflict-list events in neighbour order, then v (:368-385): warp 0
+                // loads the event words in parallel, lane 0 applies the non-zero ones
                 if (warp == 0) {
-                    bool improved = false;
+                    int Cn = C;
+                    if (mvv >= 0) {
+                        const int nwd = (int)((g1 - g0 + 31) >> 5);
+                        for (int w0 = 0; w0 < nwd; w0 += 32) {
+                            const unsigned el = w0 + lane < nwd ? evm[w0 + lane] : 0u;
+                            for (unsigned nz = __ballot_sync(FULL, el != 0u); nz; nz &= nz - 1) {
+                                const int src = __ffs(nz) - 1;
+                                unsigned e = __shfl_sync(FULL, el, src);
+                                if (lane == 0) {
+                                    while (e) {
+                                        const int bit = __ffs(e) - 1;
+                                        e &= e - 1u;
+                                        const int u = nbs[(w0 + src) * 32 + bit];
+                                        cl_apply(clist, cpos, Cn, u, cpos[u] == 0xFFFF);  // enter iff outside
+                                    }
+                                }
+                            }
+                        }
+                    }
                     if (lane == 0) {
                         if (mvv >= 0) {
-                            int Cn = C;
-                            const int deg = (int)(ctl.s1 - ctl.s0);
-                            for (int c = 0; c * 32 < deg; c++) {
-                                unsigned e = evm[c];
-                                while (e) {
-                                    const int bit = __ffs(e) - 1;
-                                    e &= e - 1u;
-                                    const int u = nbs[c * 32 + bit];
-                                    cl_apply(clist, cpos, Cn, u, cpos[u] == 0xFFFF);  // enter iff outside
-                                }
-                            }
+                            const int mb = ctl.mv_b;
+                            assign[mvv] = (uint8_t)(mb < 0 ? assign[mvv] : mb);
                             gva[mvv] = (uint8_t)ctl.gvb;
                             cl_apply(clist, cpos, Cn, mvv, ctl.gvb > 0);
                             ctl.C = Cn;
-                            if (ctl.conflicts < ctl.best) {
-                                ctl.best = ctl.conflicts;
-                                improved = true;
-                            }
+                            if (improved) ctl.best = ctl.conflicts;
                         }
                         ctl.sum_c += C;
                         ctl.it = it + 1;
-                    }
-                    if (rank == 0 && __shfl_sync(FULL, improved, 0)) {
-                        __syncwarp();
-                        for (int v = lane; v < n; v += 32) b_out[v] = assign[v];
                     }
                 }
                 __syncthreads();
@@ -907,10 +901,10 @@ int cl_threads() {
     return 512;
 }
 
-template <int KQ, int NT>
+template <int NT>
 int cl_launch_t(const TabuParams &P, const ClLayout &L, int max_clusters, cudaStream_t st, int *grid_out,
                 bool query_only) {
-    auto kern = tabucol_cluster_kernel<KQ, NT>;
+    auto kern = tabucol_cluster_kernel<NT>;
     const size_t smem = L.off[CS_NSEG];
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return set_error(MCB_ERR_CUDA, "tabucol cluster: smem attribute (%zu B) failed", smem);
@@ -934,20 +928,19 @@ int cl_launch_t(const TabuParams &P, const ClLayout &L, int max_clusters, cudaSt
     if (query_only) return MCB_OK;
     cfg.gridDim = dim3(2 * clusters);
     if (getenv("MCB_VERBOSE"))
-        fprintf(stderr, "[mcb] tabucol_cluster<kq=%d,nt=%d> clusters=%d (max %d) smem=%zu kh=%d\n", KQ, NT, clusters,
+        fprintf(stderr, "[mcb] tabucol_cluster<nt=%d> clusters=%d (max %d) smem=%zu kh=%d\n", NT, clusters,
                 nc, smem, L.kh);
     if (cudaLaunchKernelEx(&cfg, kern, P, L) != cudaSuccess)
         return set_error(MCB_ERR_CUDA, "tabucol cluster launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     return MCB_OK;
 }
 
-template <int KQ>
-int cl_launch_kq(const TabuParams &P, const ClLayout &L, int max_clusters, cudaStream_t st, int *grid_out,
+int cl_launch_nt(const TabuParams &P, const ClLayout &L, int max_clusters, cudaStream_t st, int *grid_out,
                  bool query_only) {
     switch (cl_threads()) {
-        case 256: return cl_launch_t<KQ, 256>(P, L, max_clusters, st, grid_out, query_only);
-        case 1024: return cl_launch_t<KQ, 1024>(P, L, max_clusters, st, grid_out, query_only);
-        default: return cl_launch_t<KQ, 512>(P, L, max_clusters, st, grid_out, query_only);
+        case 256: return cl_launch_t<256>(P, L, max_clusters, st, grid_out, query_only);
+        case 1024: return cl_launch_t<1024>(P, L, max_clusters, st, grid_out, query_only);
+        default: return cl_launch_t<512>(P, L, max_clusters, st, grid_out, query_only);
     }
 }
 
@@ -986,8 +979,7 @@ int tabucol_cluster_launch(const TabuParams &P, int max_clusters, cudaStream_t s
     if (L.off[CS_NSEG] > (size_t)max_smem_optin())
         return set_error(MCB_ERR_UNSUPPORTED, "tabucol cluster: n=%d k=%d needs %u B per CTA", P.n, P.k,
                          L.off[CS_NSEG]);
-    return L.kh <= 64 ? cl_launch_kq<1>(P, L, max_clusters, st, grid_out, query_only)
-                      : cl_launch_kq<2>(P, L, max_clusters, st, grid_out, query_only);
+    return cl_launch_nt(P, L, max_clusters, st, grid_out, query_only);
 }
 
 }  // namespace mcb

@@ -36,8 +36,8 @@ N.lib().mcb_debug_cluster_warps(wbuf, 1)
 flags = (0 if a.nodiag else N.FLAG_DIAG) | N.FLAG_PROFILE | (N.FLAG_PRODUCTION if a.philox else 0)
 if a.cluster:
     flags |= N.FLAG_FORCE_CLUSTER
-    NAMES = {1: "pass1+#1", 2: "prefix/walk+#2", 3: "draw/locate+#3", 4: "move lane0", 5: "gamma update",
-             6: "list/best", 7: "tail", 8: "(p1 work r0)", 9: "(p1 work r1)"}
+    NAMES = {1: "pass1+#1", 2: "prefix/walk+#2", 3: "draw/locate+#3", 4: "move+update", 5: "-",
+             6: "list events", 7: "tail", 8: "(p1 work r0)", 9: "(p1 work r1)"}
 t = torch.from_numpy(A).cuda()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record()
@@ -53,7 +53,8 @@ for i in range(1, 10):
     print(f"  {NAMES[i]:14s} {buf[i]/its:9.1f} cycles  {100*buf[i]/tot:5.1f}%")
 if a.cluster:
     print(f"  spilled rows/iteration (rank 0) {buf[11]/its:.1f}, walked half-rows/iteration {buf[12]/its:.2f}, "
-          f"stale rescans {buf[13]/its:.1f}, masked scans {buf[14]/its:.2f} (rank 0)")
+          f"stale rescans {buf[13]/its:.1f}, masked scans {buf[14]/its:.2f} (rank 0); "
+          f"init {buf[15]/a.pop:.0f} cycles per individual")
 if a.cluster:
     N.check(N.lib().mcb_debug_cluster_warps(wbuf, 0))
     cl = a.pop // 1  # rank-0 CTAs: one per individual
