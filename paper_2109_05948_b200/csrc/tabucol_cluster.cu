@@ -260,25 +260,48 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
         if (tid == 0) ctl.diag = 0;
         __syncthreads();
         {
-            // this CTA's half of gamma[u] and (both CTAs) gva[u]; a thread owns its rows
+            // this CTA's half of gamma[u] and (both CTAs) gva[u]: a warp per row,
+            // lanes over the CSR neighbours (coalesced), byte counts added to
+            // their 32-bit words by shared atomics; a count passing 254 shows
+            // as a 0xFF byte or, once it carried, as a row sum short of the
+            // number of local-coloured neighbours
             bool bad = false;
-            for (int u = tid; u < n; u += NT) {
+            const int KW = KH >> 2;
+            for (int u = warp; u < n; u += NW) {
                 const int au = assign[u];
-                int gu = 0;
-                for (int64_t idx = P.indptr[u]; idx < P.indptr[u + 1]; idx++) {
+                int gu = 0, nl = 0;
+                uint32_t *row32 = reinterpret_cast<uint32_t *>(gamma + (size_t)u * KH);
+                const int64_t s0 = P.indptr[u], s1 = P.indptr[u + 1];
+#pragma unroll 4
+                for (int64_t idx = s0 + lane; idx < s1; idx += 32) {
                     const int c = assign[__ldg(P.indices + idx)];
                     gu += c == au;
                     const int lc = local_col(c);
                     if (lc >= 0) {
-                        uint8_t *e = gamma + (size_t)u * KH + lc;
-                        if (*e >= CL_GMAX) bad = true;
-                        else *e = (uint8_t)(*e + 1);
+                        atomicAdd(row32 + (lc >> 2), 1u << (8 * (lc & 3)));
+                        nl++;
                     }
                 }
-                if (gu > CL_GMAX) bad = true;
-                gva[u] = (uint8_t)min(gu, CL_GMAX);
+                gu = __reduce_add_sync(FULL, gu);
+                nl = __reduce_add_sync(FULL, nl);
+                __syncwarp();
+                int sum = 0;
+                bool ff = false;
+                if (lane < KW) {
+                    const uint32_t x = row32[lane];
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        if (cb + 4 * lane + e >= k) continue;  // padding byte
+                        const int b = (x >> (8 * e)) & 0xFF;
+                        sum += b;
+                        ff |= b == 0xFF;
+                    }
+                }
+                sum = __reduce_add_sync(FULL, sum);
+                if (__any_sync(FULL, ff) || sum != nl || gu > CL_GMAX) bad = true;
+                if (lane == 0) gva[u] = (uint8_t)min(gu, CL_GMAX);
             }
-            if (bad) both(&ClCtrl<NW>::ovf, 1);
+            if (bad && lane == 0) both(&ClCtrl<NW>::ovf, 1);
         }
         __syncthreads();
         // conflicts and the ascending conflict list (:298-310), identical in both CTAs
