@@ -88,6 +88,7 @@ struct ClLayout {
 // the own colour (aloc >= 0) and live tabu colours without aspiration (their
 // g >= A = thr + gva, :336-339) -- from the 4 slots (cols / expiries tx) and,
 // when spl, the dense spilled row, each lane checking its own 4 colours.
+// A == INT_MIN: every slot colour excluded whatever its state (the row cache).
 // Padding colours are 0xFF already.  Warp-cooperative: lanes >= KW get ~0.
 __device__ __forceinline__ uint32_t cl_word(const uint8_t *gamma, const uint16_t *gstamp, int KH, int v, int aloc,
                                             uint32_t cols, uint2 tx, bool spl, int A, uint32_t it, int lane) {
@@ -101,7 +102,8 @@ __device__ __forceinline__ uint32_t cl_word(const uint8_t *gamma, const uint16_t
 #pragma unroll
         for (int q = 0; q < 4; q++) {
             const int t = (cols >> (8 * q)) & 0xFF;
-            if (t != 0xFF && (t >> 2) == lane && active<uint16_t>(e[q], it) && !((int)((x0 >> (8 * (t & 3))) & 0xFF) < A))
+            if (t != 0xFF && (t >> 2) == lane &&
+                (A == INT_MIN || (active<uint16_t>(e[q], it) && !((int)((x0 >> (8 * (t & 3))) & 0xFF) < A))))
                 x |= 0xFFu << (8 * (t & 3));
         }
     }
@@ -185,11 +187,13 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
     uint16_t *nbs = reinterpret_cast<uint16_t *>(smem + L.off[CS_NBS]);
     uint32_t *evm = reinterpret_cast<uint32_t *>(smem + L.off[CS_EVM]);
     // Row cache (this CTA's colours): minimum of gamma over the row's local
-    // colours except its own colour (low byte, 0xFF = none) and how many reach
-    // it (high byte; 0 = stale).  A move v*: a -> b changes two columns of the
-    // neighbours' rows, so the update loop keeps it in O(1) per neighbour; a
-    // row whose minimum group empties, and v*'s own row, go stale and are
-    // rescanned when next needed.  Tabu exclusions are applied on top of it.
+    // colours except its own colour and its tabu-slot colours (low byte, 0xFF
+    // = none) and how many reach it (high byte; 0 = stale).  A move v*: a -> b
+    // changes two columns of the neighbours' rows, so the update loop keeps it
+    // in O(1) per neighbour; a row whose minimum group empties, v*'s own row
+    // (own colour and slots change) and, at the expiry sweep, every row go
+    // stale and are rescanned when next needed.  Pass 1 merges in the slot
+    // colours that are admissible at the time (expired, or aspiration).
     uint16_t *hc = reinterpret_cast<uint16_t *>(smem + L.off[CS_HC]);
     uint16_t *gstamp = reinterpret_cast<uint16_t *>(P.ws_stamp + blockIdx.x * P.ws_s_stride);
     uint32_t *rown = rank ? rhi : rlo, *rpeer = rank ? rlo : rhi;
@@ -405,14 +409,14 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
                             tx[r] = reinterpret_cast<const uint2 *>(texp)[v[r]];
                             spl[r] = active<uint16_t>(tovf[v[r]], it32);
                         }
-                        // stale cache rows: rescanned by the whole warp (own colour excluded)
+                        // stale cache rows: rescanned by the whole warp (own and slot colours excluded)
 #pragma unroll
                         for (int r = 0; r < R; r++) {
                             for (unsigned sm = __ballot_sync(FULL, (h[r] >> 8) == 0); sm; sm &= sm - 1) {
                                 const int src = __ffs(sm) - 1;
                                 const uint32_t x = cl_word(gamma, gstamp, KH, __shfl_sync(FULL, v[r], src),
-                                                           __shfl_sync(FULL, aloc[r], src), 0xFFFFFFFFu,
-                                                           make_uint2(0, 0), false, 0, it32, lane);
+                                                           __shfl_sync(FULL, aloc[r], src), __shfl_sync(FULL, cols[r], src),
+                                                           make_uint2(0, 0), false, INT_MIN, it32, lane);
                                 int wm, wc;
                                 warp_min_count(x, wm, wc);
                                 if (lane == src) {
@@ -428,37 +432,41 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
                             m[r] = (int)(h[r] & 0xFFu);
                             c[r] = (int)(h[r] >> 8);
                             masked[r] = false;
-                            if (on[r] && m[r] != 0xFF) {
-                                // live tabu colours at the minimum without aspiration
-                                // (g < thr + gva admits them, :336-339) leave the group
-                                const bool adm = m[r] < thr + gv[r];
+                            if (on[r]) {
+                                // the cache holds the minimum over the colours that are
+                                // neither the own colour nor in a tabu slot; a slot colour
+                                // joins when its entry expired or aspiration admits it
+                                // (g < thr + gva, :336-339)
+                                const int A = thr + gv[r];
                                 const uint8_t *gr = gamma + (size_t)v[r] * KH;
-                                if (!adm && cols[r] != 0xFFFFFFFFu) {
+                                if (cols[r] != 0xFFFFFFFFu) {
                                     const uint16_t e[4] = {(uint16_t)tx[r].x, (uint16_t)(tx[r].x >> 16),
                                                            (uint16_t)tx[r].y, (uint16_t)(tx[r].y >> 16)};
 #pragma unroll
                                     for (int q = 0; q < 4; q++) {
                                         const int t = (cols[r] >> (8 * q)) & 0xFF;
-                                        if (t != 0xFF && t != aloc[r] && gr[t] == m[r] && active<uint16_t>(e[q], it32))
-                                            c[r]--;
+                                        if (t == 0xFF || t == aloc[r]) continue;
+                                        const int g = gr[t];
+                                        if (!active<uint16_t>(e[q], it32) || g < A) {
+                                            c[r] = g < m[r] ? 1 : c[r] + (g == m[r]);
+                                            m[r] = min(m[r], g);
+                                        }
                                     }
                                 }
                                 if (prof) n_spill += spl[r];
-                                if (!adm && spl[r]) {
-                                    const uint16_t *gs = gstamp + (size_t)v[r] * KH;
-                                    for (int t = 0; t < KH; t++)
-                                        if (t != aloc[r] && gr[t] == m[r] && active<uint16_t>(gs[t], it32)) c[r]--;
+                                masked[r] = spl[r];  // live spilled entries: full masked scan
+                                if (m[r] == 0xFF) {
+                                    m[r] = TC_BIG;
+                                    c[r] = 0;
+                                } else {
+                                    m[r] -= gv[r];
                                 }
-                                masked[r] = c[r] == 0;
-                                m[r] -= gv[r];
                             } else {
                                 m[r] = TC_BIG;
                                 c[r] = 0;
                             }
                         }
-                        // rows whose whole minimum group is tabu: masked scan by the warp
-                        // (per-lane scans of these rows measured slower: 19 dependent
-                        // word steps per lane against one word per lane and two REDUX)
+                        // rows with live spilled tabu entries: masked scan by the warp
 #pragma unroll
                         for (int r = 0; r < R; r++) {
                             for (unsigned mm = __ballot_sync(FULL, masked[r]); mm; mm &= mm - 1) {
@@ -745,12 +753,18 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
                                 nbs[j] = (uint16_t)u;
                                 uint8_t *gr = gamma + (size_t)u * KH;
                                 const int au = assign[u];
+                                const uint32_t cu = reinterpret_cast<const uint32_t *>(tcol)[u];
                                 uint32_t h = hc[u];
                                 int hm = (int)(h & 0xFFu), hn = (int)(h >> 8);
+                                // colours in u's tabu slots are outside its cache
+                                auto in_slots = [cu](int x) {
+                                    return ((cu & 0xFFu) == (uint32_t)x) | (((cu >> 8) & 0xFFu) == (uint32_t)x) |
+                                           (((cu >> 16) & 0xFFu) == (uint32_t)x) | ((cu >> 24) == (uint32_t)x);
+                                };
                                 if (al >= 0) {
                                     const int ga = gr[al] - 1;
                                     gr[al] = (uint8_t)ga;
-                                    if (au != ma && hn != 0) {
+                                    if (au != ma && hn != 0 && !in_slots(al)) {
                                         hn = ga < hm ? 1 : hn + (ga == hm);
                                         hm = min(hm, ga);
                                     }
@@ -759,7 +773,7 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
                                     const int gb = gr[bl];
                                     if (gb >= CL_GMAX) bad = true;
                                     else gr[bl] = (uint8_t)(gb + 1);
-                                    if (au != mb && hn != 0 && gb == hm) hn--;  // 0: stale
+                                    if (au != mb && hn != 0 && gb == hm && !in_slots(bl)) hn--;  // 0: stale
                                 }
                                 hc[u] = (uint16_t)(hm | hn << 8);
                                 if (au == ma) {
@@ -835,6 +849,7 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
                     for (int v = tid; v < n; v += NT) {
                         for (int s = 0; s < 4; s++)
                             if (!active<uint16_t>(texp[4 * v + s], itw)) tcol[4 * v + s] = 0xFF;
+                        hc[v] = 0;  // its slot set (outside the cache) may have changed
                         if (active<uint16_t>(tovf[v], itw)) {
                             uint16_t *gs = gstamp + (size_t)v * KH;
                             for (int c = 0; c < KH; c++)
