@@ -78,7 +78,7 @@ struct ClCtrl {
 
 // segment offsets of the dynamic shared memory, computed on the host
 enum ClSeg { CS_GAMMA, CS_TEXP, CS_TCOL, CS_TOVF, CS_ASSIGN, CS_GVA, CS_CLIST, CS_CPOS, CS_RLO, CS_RHI, CS_NBS,
-             CS_EVM, CS_HC, CS_NSEG };
+             CS_EVM, CS_HC, CS_IP, CS_NSEG };
 struct ClLayout {
     uint32_t off[CS_NSEG + 1];
     int kh;
@@ -195,6 +195,10 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
     // stale and are rescanned when next needed.  Pass 1 merges in the slot
     // colours that are admissible at the time (expired, or aspiration).
     uint16_t *hc = reinterpret_cast<uint16_t *>(smem + L.off[CS_HC]);
+    // CSR row offsets (2m < 2^32 for n <= 32767): the move needs indptr[v*]
+    // before barrier #3, and every cluster barrier invalidates L1
+    uint32_t *ip = reinterpret_cast<uint32_t *>(smem + L.off[CS_IP]);
+    for (int v = tid; v <= n; v += NT) ip[v] = (uint32_t)P.indptr[v];
     uint16_t *gstamp = reinterpret_cast<uint16_t *>(P.ws_stamp + blockIdx.x * P.ws_s_stride);
     uint32_t *rown = rank ? rhi : rlo, *rpeer = rank ? rlo : rhi;
     // the partner CTA's records and control block (distributed shared memory).
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
                 const int au = assign[u];
                 int gu = 0, nl = 0;
                 uint32_t *row32 = reinterpret_cast<uint32_t *>(gamma + (size_t)u * KH);
-                const int64_t s0 = P.indptr[u], s1 = P.indptr[u + 1];
+                const int64_t s0 = ip[u], s1 = ip[u + 1];
 #pragma unroll 4
                 for (int64_t idx = s0 + lane; idx < s1; idx += 32) {
                     const int c = assign[__ldg(P.indices + idx)];
@@ -648,8 +652,8 @@ __global__ void __launch_bounds__(NT, 1) tabucol_cluster_kernel(TabuParams P, Cl
                 int64_t g0 = 0, g1 = 0;
                 int nb[NBR];
                 if (mv_v >= 0) {
-                    g0 = P.indptr[mv_v];
-                    g1 = P.indptr[mv_v + 1];
+                    g0 = ip[mv_v];
+                    g1 = ip[mv_v + 1];
                 }
 #pragma unroll
                 for (int q = 0; q < NBR; q++) {
@@ -921,7 +925,7 @@ ClLayout cl_layout(int n, int k) {
     L.kh = (((k + 1) / 2) + 3) & ~3;
     const size_t N = (size_t)n;
     const size_t bytes[CS_NSEG] = {N * L.kh, N * 8, N * 4, N * 2, N,     N,
-                                   N * 2,    N * 2, N * 4, N * 4, N * 2, 4 * ((N + 31) / 32 + 32), N * 2};  // evm: + one word per warp
+                                   N * 2,    N * 2, N * 4, N * 4, N * 2, 4 * ((N + 31) / 32 + 32), N * 2, (N + 1) * 4};  // evm: + one word per warp
     size_t off = 0;
     for (int i = 0; i < CS_NSEG; i++) {
         L.off[i] = (uint32_t)off;
