@@ -419,6 +419,15 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                 for (int i = tid; i < 2 * ((n + 31) / 32); i += NT) nbits[i] = 0u;
                 if (tid == 0) ctl.inc = 0;
             }
+            // the objective's exact-integer mode depends on phi only: once per round
+            __shared__ GvMode s_gm;
+            __shared__ int s_fast32;
+            if (tid == 0) {
+                const GvMode g0 = gv_mode(ctl.phi, n);
+                s_gm = g0;
+                // 32-bit numerators when |t| n + maxw 2^s < 2^30 (|dc| <= n, |ds| <= maxw)
+                s_fast32 = g0.fast && (long long)(g0.t < 0 ? -g0.t : g0.t) * n + ((long long)s_maxw << g0.s) < (1ll << 30);
+            }
             __syncthreads();
             // phase counters live in shared memory (thread 0 only): no registers
             // held across the iteration when the flag is off
@@ -440,11 +449,8 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                 }
                 const long long it = ctl.it, score = ctl.score, conflicts = ctl.conflicts,
                                 best = ctl.best;
-                const double phi = ctl.phi;
-                const GvMode gm = gv_mode(phi, n);
-                // 32-bit numerators when |t| n + maxw 2^s < 2^30 (|dc| <= n, |ds| <= maxw)
-                const bool fast32 =
-                    gm.fast && (long long)(gm.t < 0 ? -gm.t : gm.t) * n + ((long long)s_maxw << gm.s) < (1ll << 30);
+                const GvMode gm = s_gm;
+                const bool fast32 = s_fast32 != 0;
                 // pass 1: (min g, count) per vertex row over admissible candidates
                 const int nch = (n + 31) >> 5;
                 if (fast32 && nch <= 32) {
@@ -524,13 +530,30 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                     const int need_dc = -(int)conflicts;
                                     const long long room = best - score;  // ds < room
                                     const int dsmax = room > INT_MAX ? INT_MAX : (room < INT_MIN ? INT_MIN : (int)room);
-                                    for (int c = 0; c < k; c++) {
-                                        const int dc = (int)row[c] - gva;
-                                        const int ds = max(0, wv - (int)max_val[c]) - rem;
-                                        const bool ok = c != a && dc == need_dc && ds < dsmax;
-                                        const int G = ok ? (ds << S) + Tt * dc : INT_MAX;
-                                        cnt = (G < m) ? 1 : cnt + (G == m && ok);
-                                        m = min(m, G);
+                                    auto cand = [&](int c) {
+                                        const int ds = max(0, wv - mx32[c]) - rem;
+                                        if (c != a && ds < dsmax) {
+                                            const int G = (ds << S) + Tt * need_dc;
+                                            cnt = (G < m) ? 1 : cnt + (G == m);
+                                            m = min(m, G);
+                                        }
+                                    };
+                                    if (NARROW && (k & 3) == 0) {
+                                        // only colours with gamma == gva - conflicts qualify:
+                                        // found 4 at a time by a byte-equality mask
+                                        const uint32_t *r32w = reinterpret_cast<const uint32_t *>(row);
+                                        const uint32_t t4 = (uint32_t)(gva + need_dc) * 0x01010101u;
+                                        for (int w = 0; w < (k >> 2); w++) {
+                                            const uint32_t z = r32w[w] ^ t4;
+                                            uint32_t eq = ~(((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & 0x80808080u;
+                                            while (eq) {
+                                                cand(4 * w + ((__ffs(eq) - 1) >> 3));
+                                                eq &= eq - 1u;
+                                            }
+                                        }
+                                    } else {
+                                        for (int c = 0; c < k; c++)
+                                            if ((int)row[c] - gva == need_dc) cand(c);
                                     }
                                 }
                             }
@@ -541,17 +564,25 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                             const int src = __ffs(rs) - 1;
                             const int au = __shfl_sync(FULL, a, src), wu = __shfl_sync(FULL, wv, src);
                             const GT *ru = gamma + (size_t)(v0 + src) * k;
-                            int lmin = INT_MAX;
-                            for (int cb = 0; cb < k; cb += 32) {
-                                const int c = cb + lane;
-                                if (c < k && c != au) lmin = min(lmin, (max(0, wu - mx32[c]) << S) + Tt * (int)ru[c]);
-                            }
-                            const int hm = __reduce_min_sync(FULL, lmin);
-                            int hcn = 0;
-                            for (int cb = 0; cb < k; cb += 32) {
-                                const int c = cb + lane;
-                                const bool eq = c < k && c != au && (max(0, wu - mx32[c]) << S) + Tt * (int)ru[c] == hm;
-                                hcn += __popc(__ballot_sync(FULL, eq));
+                            int hm, hcn = 0;
+                            if (k <= 64) {  // each lane's two colours evaluated once
+                                const int c0 = lane, c1 = lane + 32;
+                                const int h0 = (c0 < k && c0 != au) ? (max(0, wu - mx32[c0]) << S) + Tt * (int)ru[c0] : INT_MAX;
+                                const int h1 = (c1 < k && c1 != au) ? (max(0, wu - mx32[c1]) << S) + Tt * (int)ru[c1] : INT_MAX;
+                                hm = __reduce_min_sync(FULL, min(h0, h1));
+                                hcn = __popc(__ballot_sync(FULL, h0 == hm)) + __popc(__ballot_sync(FULL, h1 == hm));
+                            } else {
+                                int lmin = INT_MAX;
+                                for (int cb = 0; cb < k; cb += 32) {
+                                    const int c = cb + lane;
+                                    if (c < k && c != au) lmin = min(lmin, (max(0, wu - mx32[c]) << S) + Tt * (int)ru[c]);
+                                }
+                                hm = __reduce_min_sync(FULL, lmin);
+                                for (int cb = 0; cb < k; cb += 32) {
+                                    const int c = cb + lane;
+                                    const bool eq = c < k && c != au && (max(0, wu - mx32[c]) << S) + Tt * (int)ru[c] == hm;
+                                    hcn += __popc(__ballot_sync(FULL, eq));
+                                }
                             }
                             if (lane == src) {
                                 mh = hm;
@@ -777,7 +808,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                         if (dadd < 0) dadd = 0;
                         const long long ds = dadd - rem;
                         if (frozen && (conflicts + dc != 0 || score + ds >= best)) continue;
-                        const double gv = gval_of(ds, dc, phi);
+                        const double gv = gval_of(ds, dc, gm.phi);
                         if (gv < m) {
                             m = gv;
                             cnt = 1;
