@@ -37,6 +37,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cuda_pipeline.h>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -400,9 +402,14 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
 
         // warp 0, as soon as the moving vertex is known: its neighbour list into
         // shared memory (the L2 round trip overlaps the colour locate)
+        // N(v*) into nbuf by asynchronous global -> shared copies: the L2 round
+        // trip overlaps the colour locate and the move bookkeeping; warp 0 waits
+        // for them (__pipeline_wait_prior) just before the barrier that
+        // publishes the move
         auto fetch_nbrs = [&](int v) {
             const int e0 = ip32[v], d = ip32[v + 1] - e0;
-            for (int i = lane; i < d; i += 32) nbuf[i] = __ldg(P.indices + e0 + i);
+            for (int i = lane; i < d; i += 32) __pipeline_memcpy_async(nbuf + i, P.indices + e0 + i, 4);
+            __pipeline_commit();
             if (lane == 0) ctl.deg = d;
         };
 
@@ -764,6 +771,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                             if (lane == 0) wv_apply_move(v, a, b, bds, bdc, frozen, it, total, score, conflicts);
                         }
                         if (lane == 0) ctl.has_move = (mv_v >= 0);
+                        __pipeline_wait_prior(0);
                     }
                 } else {
                 // pass 1: (min g, count) per vertex row over admissible candidates
@@ -1040,6 +1048,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                         if (lane == 0) wv_apply_move(v, a, b, mv_ds, mv_dc, mv_tabu, it, total, score, conflicts);
                     }
                     if (lane == 0) ctl.has_move = (mv_v >= 0);
+                    __pipeline_wait_prior(0);
                 }
                 }
                 __syncthreads();
