@@ -707,6 +707,13 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                     __syncthreads();
                     WVPH(3);
                     if (warp == 0) {
+                        long long t_sp = (wst && lane == 0) ? clock64() : 0;
+#define WVSP(i)                                                             \
+    if (wst && lane == 0) {                                                 \
+        const long long _t = clock64();                                     \
+        atomicAdd(&g_wvstats[9 + (i)], (unsigned long long)(_t - t_sp));    \
+        t_sp = _t;                                                          \
+    }
                         const int total = __reduce_add_sync(FULL, lane < NW ? s_wts[lane] + s_wts2[lane] : 0);
                         int mv_v = -1;
                         if (D != INT_MAX) {
@@ -726,6 +733,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                     sstar = 1 + (int)philox_below(key, ctr, (uint32_t)T);
                                 }
                             }
+                            WVSP(0);
                             // the chunk, then the row holding the sstar-th D-candidate
                             const int ci = warp_incl_sum(cc, lane);
                             const int ch = __ffs(__ballot_sync(FULL, ci >= sstar)) - 1;
@@ -735,6 +743,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                             const int incl = warp_incl_sum(c1, lane);
                             const int src = __ffs(__ballot_sync(FULL, before + incl >= sstar)) - 1;
                             const int v = ch * 32 + src;
+                            WVSP(1);
                             fetch_nbrs(v);
                             const int need = sstar - before - __shfl_sync(FULL, incl - c1, src);
                             // within the row: the need-th colour with G == D
@@ -768,10 +777,14 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                 cum += hc;
                             }
                             mv_v = v;
+                            WVSP(2);
                             if (lane == 0) wv_apply_move(v, a, b, bds, bdc, frozen, it, total, score, conflicts);
+                            WVSP(3);
                         }
                         if (lane == 0) ctl.has_move = (mv_v >= 0);
                         __pipeline_wait_prior(0);
+                        WVSP(4);
+#undef WVSP
                     }
                 } else {
                 // pass 1: (min g, count) per vertex row over admissible candidates

@@ -53,4 +53,6 @@ N.check(N.lib().mcb_debug_wvcp_stats(ctypes.addressof(buf), 1))
 it = max(buf[0], 1)
 names = ["pass1", "chunk_min", "prefix_walks", "warp0", "gamma_update", "refresh", "best", "tail"]
 print(json.dumps({"iterations": buf[0], **{nm: round(buf[i + 1] / it, 1) for i, nm in enumerate(names)},
-                  "total": round(sum(buf[1:9]) / it, 1)}))
+                  "total": round(sum(buf[1:9]) / it, 1),
+                  "warp0_sub": {nm: round(buf[9 + i] / it, 1) for i, nm in
+                                enumerate(["draws", "chunk_row", "colour_locate", "apply_move", "nbr_wait"])}}))
