@@ -62,3 +62,4 @@ if a.cluster:
     print("   " + " ".join(f"{wbuf[w]/its:6.0f}" for w in range(32) if wbuf[w]))
     print("   " + " ".join(f"{wbuf[32+w]/its:6.0f}" for w in range(32) if wbuf[w]))
     print("   " + " ".join(f"{wbuf[64+w]/its:6.2f}" for w in range(32) if wbuf[w]))
+    print("  warp0 pass-1 stage cycles: " + " ".join(f"{wbuf[80+i]/its:7.0f}" for i in range(4)))
