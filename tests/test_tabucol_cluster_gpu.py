@@ -109,3 +109,26 @@ def test_cluster_is_the_config4_kernel():
     buf = ctypes.create_string_buffer(256)
     N.check(N.lib().mcb_tabucol_describe(2000, 150, 256, buf, 256))
     assert b"tabucol_cluster_kernel" in buf.value, buf.value
+
+
+def test_cluster_k255_vs_oracle(oracle_lib):
+    """k = 255, the ABI maximum: halves of 128 colours (32 words, every lane
+    of the warp-cooperative scans, walks and locate busy)"""
+    g = rand_graph(21, 420, 0.7)
+    A = random_col_assigns(420, 255, 6, 21)
+    keys = stream_keys(21, TAG_LS, 2, 6)
+    ref = oracle_lib.tabucol_batch(g, A.copy(), 255, keys, 1500, log_moves=True, counters=True)
+    got = LS._run_tabucol_batch(g, A.copy(), 255, keys, 1500, log_moves=True, counters=True,
+                                flags=N.FLAG_FORCE_CLUSTER)
+    _same(got, ref, "k255")
+
+
+@pytest.mark.parametrize("n,k,kind", [(2000, 150, b"tabucol_cluster_kernel"), (2200, 150, b"gamma in L2"),
+                                      (2600, 150, b"gamma in L2"), (2000, 200, b"gamma in L2"),
+                                      (1000, 200, b"gamma in shared memory"), (1100, 200, b"tabucol_cluster_kernel")])
+def test_cluster_dispatch_boundary(n, k, kind):
+    """the cluster kernel serves exactly the shapes one CTA's shared memory
+    cannot hold and the pair's can; beyond the pair, the L2 path"""
+    buf = ctypes.create_string_buffer(256)
+    N.check(N.lib().mcb_tabucol_describe(n, k, 64, buf, 256))
+    assert kind in buf.value, buf.value
