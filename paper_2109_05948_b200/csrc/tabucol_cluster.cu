@@ -18,17 +18,21 @@
 // colour b gain one, gva[v*] += D), the conflict list and every counter --
 // so list maintenance, the tenure draw and the reservoir draws need no
 // exchange.  Per iteration the CTAs meet at three cluster barriers:
-//   #1 after pass 1: each CTA has scanned its half of every conflicting row
-//      ((min delta, #candidates at it) per half) and stored the record in
-//      both CTAs' record arrays (DSMEM stores);
+//   #1 after pass 1: each CTA has evaluated its half of every conflicting
+//      row ((min delta, #candidates at it) per half, from its row cache plus
+//      the admissible tabu-slot colours) and the per-warp block minima; each
+//      warp then pulls its block of the partner's records (DSMEM loads);
 //   #2 after the prefix-min pass: rows equal to the running minimum carry
 //      their combined count of tie events, rows that lower it are walked --
 //      each CTA walks its own half, half 1 entered with min(R, half-0
 //      minimum) -- and the walk events are exchanged;
-//   #3 after the draw: both CTAs derive the same winner row and half; the
-//      owner of that half locates the column b and publishes it.
-// The prefix-min pass is spread over all warps (per-warp contiguous blocks
-// of rows: block minima, then each block scanned from its entering minimum).
+//   #3 after the draw (spread over all warps): every warp derives the same
+//      winner row and half, the owner of that half locates the column b and
+//      publishes it, all threads prefetch their slice of N(v*).
+// The prefix-min pass is spread over all warps (per-warp contiguous blocks of
+// rows, block minima from pass 1, each block scanned from its entering
+// minimum).  After #3 warp 0 does the tenure / tabu / log bookkeeping while
+// the other warps update gamma, gva and the row caches over N(v*).
 //
 // Overflow (a gamma count reaching 255, tenure >= 16384) stops the individual
 // in both CTAs at the same barrier; the host re-runs it on the wide CTA pass.
@@ -50,9 +54,10 @@ namespace {
 
 constexpr int CL_GMAX = 254;
 // MCB_FLAG_PROFILE: rank 0 thread 0's cycles per phase ([1] pass 1 + barrier
-// #1, [2] prefix/walk pass + #2, [3] draw/locate + #3, [4] move bookkeeping,
-// [5] gamma update, [6] list events / best, [7] tail), [10] iterations,
-// [11] pass-1 rows with spilled tabu expiries, [12] walked half-rows
+// #1, [2] prefix/walk pass + #2, [3] draw/locate + #3, [4] move + update,
+// [6] list events, [7] tail, [8] / [9] slowest warp's pass 1 in rank 0 / 1),
+// [10] iterations, [11] pass-1 rows with spilled tabu expiries, [12] walked
+// half-rows, [13] stale cache rescans, [14] masked scans, [15] init cycles
 __device__ unsigned long long g_cl_cycles[16];
 // MCB_FLAG_PROFILE, rank 0: per warp w, [w] summed pass-1 durations (clock
 // from the warp's own start), [32 + w] summed start delays after thread 0's
