@@ -61,7 +61,10 @@ WORKLOADS = {
 }
 # bounded depth of the extra workloads in a default run (iterations, or
 # iterations x rounds for WVCP); --workload cN runs any of them at full depth
-EXTRA_DEPTH = {"c3": (10000, 1), "c4": (5000, 2), "c5": (5000, 1)}
+EXTRA_DEPTH = {"c3": (10000, 1), "c4": (5000, 2), "c5": (5000, 1), "c2p": (10000, 1)}
+# "<config>p": the config in production mode (Philox4x32-10 tie-break and
+# tenure draws: statistically equivalent to the reference, not bit-identical;
+# tests/test_production_stats_gpu.py)
 METRIC = "TabuCol moves/sec (whole box) G(500,0.5) k=48 D=8192 at 1/2/4/8 GPU; x CPU ref"
 REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
@@ -296,13 +299,17 @@ def run_reference(args):
 
 
 def workload_config(wl, depth, world, rounds=None):
+    prod = wl.endswith("p")
+    if prod:
+        wl = wl[:-1]
     kind, seed, n, pe, wmax, k, D, dep, rnd = WORKLOADS[wl]
     rounds = rounds or rnd
     w = f"{wl}: G({n},{pe}) seed {seed}" + (f", weights 1..{wmax}" if wmax > 1 else "") + f", k={k}, D={D}, "
     w += (f"{rounds} rounds x {depth} iterations/individual/step (iterated WVCP tabu)" if kind == "wvcp"
           else f"{depth} iterations/individual/step")
     return {"workload": w,
-            "mode": "validation (SplitMix64, bit-exact)",
+            "mode": ("production (Philox4x32-10 draws, statistically equivalent, not bit-identical)" if prod
+                     else "validation (SplitMix64, bit-exact)"),
             "parallelism": f"population sharded {-(-D // world)}/GPU" + (
                 ", NCCL all_gather of elites per step" if world > 1 else ""),
             "l2": "flushed (256 MB write) between timed steps"}
@@ -579,10 +586,12 @@ def run_extra(wl, world, rank, dev, flush, reduce_max_sum):
     from paper_2109_05948_b200.localsearch import default_wvcp_phi0
     from paper_2109_05948_b200.rng import TAG_LS, stream_keys
 
-    kind, seed, n, pe, wmax, k, D, full_depth, full_rounds = WORKLOADS[wl]
     depth, rounds = EXTRA_DEPTH[wl]
+    prod = wl.endswith("p")
+    base = wl[:-1] if prod else wl
+    kind, seed, n, pe, wmax, k, D, full_depth, full_rounds = WORKLOADS[base]
     lo, hi, pad = shard(D, world, rank)
-    g, A = make_inputs(wl, lo, hi - lo)
+    g, A = make_inputs(base, lo, hi - lo)
     dg = Dv.DeviceGraph(g, dev)
     a0 = torch.from_numpy(A).to(dev)
     keys = Dv.keys_to_tensor(stream_keys(seed, TAG_LS, 0, hi - lo, start=lo), dev)
@@ -594,9 +603,11 @@ def run_extra(wl, world, rank, dev, flush, reduce_max_sum):
         if ev:
             ev[0].record(stream)
         if kind == "col":
-            out = Dv.tabucol_batch(dg, a, k, keys, d, flags=N.FLAG_DIAG, counters=True)
+            out = Dv.tabucol_batch(dg, a, k, keys, d, flags=N.FLAG_DIAG | (N.FLAG_PRODUCTION if prod else 0),
+                                   counters=True)
         else:
-            out = Dv.wvcp_batch(dg, a, k, keys, d, rounds, True, phi0)
+            out = Dv.wvcp_batch(dg, a, k, keys, d, rounds, True, phi0,
+                                flags=N.FLAG_DIAG | (N.FLAG_PRODUCTION if prod else 0))
         if ev:
             ev[1].record(stream)
         return out
@@ -648,7 +659,9 @@ def run_extra(wl, world, rank, dev, flush, reduce_max_sum):
                            "bytes_per_iter": per, "note": "deg(v*) taken as the mean degree 2m/n"}
     if world == 1:
         try:
-            res["cpu_baseline"] = cpu_baseline(wl, depth, rounds, full=False)
+            res["cpu_baseline"] = cpu_baseline(base, depth, rounds, full=False)
+            if prod:
+                res["cpu_baseline"]["note"] = "the reference's own (validation) mode on the same config"
         except Exception as e:  # noqa: BLE001
             res["cpu_baseline"] = {"error": str(e)[:200]}
     return res
@@ -714,7 +727,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--extra", default="c3,c4,c5", help="other configs measured after the headline")
+    ap.add_argument("--extra", default="c3,c4,c5,c2p",
+                    help="other configs measured after the headline (a trailing p: production mode)")
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--rng", default="splitmix", choices=["splitmix", "philox"])
     ap.add_argument("--pop", type=int, default=0, help="override D (testing)")
