@@ -13,22 +13,25 @@
 //   * early exit at zero conflicts (:322), `it` counts no-move iterations (:398),
 //     O(m) scratch check every 1024 iterations -> diag (:398-405).
 //
-// Iteration structure (NT threads, two block barriers):
+// Iteration structure (NT threads):
 //   pass 1 (all threads, one conflicting vertex per thread): the row's
 //     candidates are scanned 4 colours per 32-bit word (u8 gamma; native
 //     VIMNMX.U16x2 byte minima and LOP3/IADD zero-byte counts, branch-free --
 //     no emulated video-SIMD), tabu/aspiration exclusions applied as byte
 //     masks -> (row minimum, #candidates at the minimum).
-//   pass 2 (warp 0): exclusive prefix-min over the rows.  A tie event of the
-//     sequential reservoir is a candidate equal to the running minimum, so rows
-//     above the running minimum hold none, rows equal to it hold #min of them,
-//     and only the few rows that LOWER it need an in-row walk -- queued and
-//     walked one per lane in parallel.  That gives the minimum D, its
-//     multiplicity T and the counter offset of D's group; the T-1 reservoir
-//     draws are independent (rank s uses counter ctr + E + s - 2) and the
-//     winner is the last rank whose draw is zero.  Then locate (parallel over
-//     the row's words), tenure, gamma update over N(v) (adjacency prefetched
-//     speculatively), conflict-list events in neighbour order, best copy.
+//   pass 2a (all warps, per-warp contiguous blocks of rows): block minima,
+//     then each block's exclusive prefix-min from its entering running
+//     minimum.  A tie event of the sequential reservoir is a candidate equal to
+//     the running minimum, so rows above the running minimum hold none, rows
+//     equal to it hold #min of them, and only the few rows that LOWER it need
+//     an in-row walk (warp-cooperative, by the block's warp).  That gives the
+//     minimum D, its multiplicity T and the counter offset of D's group.
+//   pass 2b (warp 0): the T-1 reservoir draws are independent (rank s uses
+//     counter ctr + E + s - 2) and the winner is the last rank whose draw is
+//     zero; its block from the per-warp D-counts, its row in the block, then
+//     locate (parallel over the row's words), tenure, gamma update over N(v)
+//     (adjacency prefetched speculatively), conflict-list events in
+//     neighbour order, best copy.
 //
 // Tabu state: the reference's dense `tabu_pair[n][k]` int64 table is replaced
 // by 4 (colour, expiry) slots per vertex in shared memory; a vertex needing a
@@ -76,6 +79,7 @@ struct TabuCtrl {
     int C, work, ovf, mv_v, mv_a, mv_b, gvb;
     long long red[NW];
     int wcnt[NW];
+    int bmin[NW], bD[NW], bsum[NW], bfirst[NW];  // pass 2a per-warp block results
     long long ph[10];
 };
 
@@ -275,27 +279,6 @@ struct RowEval {
     }
 };
 
-// warp-cooperative walks of the queued (running min, row) pairs; returns the
-// tie events on lane 0 (0 elsewhere)
-template <typename G, typename S, int KQ, typename Rec>
-__device__ __forceinline__ int walk_queued(const Rec *lowl, int nlow, const G *gamma, const S *texp,
-                                           const uint8_t *tcol, const S *tovf, const S *gstamp,
-                                           const uint8_t *assign, const uint16_t *clist, int kp, int k,
-                                           uint32_t it32, int thr, const uint32_t *lut, int rs, int rm,
-                                           int lane) {
-    __syncwarp();
-    int t = 0;
-    for (int j = 0; j < nlow; j++) {
-        const int2 e = rec_unpack(lowl[j]);  // (running min, row)
-        RowEval<G, S, KQ> re;
-        re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[e.y], kp, k, it32, thr, lut, rs, rm);
-        const int tj = re.warp_walk_ties(e.x, lane);
-        if (lane == 0) t += tj;
-    }
-    __syncwarp();
-    return t;
-}
-
 template <typename G, typename S, bool GSM, int KQ, int NT>
 __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_kernel(TabuParams P) {
     constexpr int NW = NT / 32;
@@ -334,8 +317,6 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
     using Rec = typename RecT<NARROW>::T;
     Rec *rmc = reinterpret_cast<Rec *>(smem + off);  // per row: (min delta, count)
     off += (sizeof(Rec) * n + 15) & ~(size_t)15;
-    Rec *lowl = reinterpret_cast<Rec *>(smem + off);  // queued (row, running min) pairs
-    off += sizeof(Rec) * TC_LOWCAP;
     uint16_t *nbs = reinterpret_cast<uint16_t *>(smem + off);  // staged N(v)
     off += (2 * (size_t)n + 15) & ~(size_t)15;
     uint32_t *evm = reinterpret_cast<uint32_t *>(smem + off);  // event ballots per 32 neighbours
@@ -505,79 +486,76 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                 }
                 __syncthreads();
                 PH(1);
-                // pass 2a (warp 0): exclusive prefix-min over the rows (R rows per lane).
-                // Rows above the running minimum hold no tie event, rows equal to it
-                // hold #min of them, rows below it are queued and walked in parallel.
-                int carry = TC_BIG, lmin = TC_BIG, lT = 0, lfirst = INT_MAX, tsum = 0;
-                if (warp == 0) {
-                    constexpr int R = 4;
-                    int nlow = 0;
-                    for (int r0 = 0; r0 < C; r0 += 32 * R) {
-                        if (nlow > TC_LOWCAP - 32 * R) {
-                            tsum += walk_queued<G, S, KQ>(lowl, nlow, gamma, texp, tcol, tovf, gstamp, assign,
-                                                          clist, kp, k, it32, thr, s_nib, swz_rs, swz_rm, lane);
-                            nlow = 0;
-                        }
-                        int2 mc[R];
-                        int lmn = TC_BIG;
-#pragma unroll
-                        for (int r = 0; r < R; r++) {
-                            const int q = r0 + lane * R + r;
-                            mc[r] = q < C ? rec_unpack(rmc[q]) : make_int2(TC_BIG, 0);
-                            lmn = min(lmn, mc[r].x);
-                        }
-                        const int incl = warp_incl_min(lmn, lane);
+                // pass 2a (all warps): exclusive prefix-min over per-warp contiguous
+                // blocks of rows -- block minima first, then every block scanned
+                // from its entering running minimum.  Rows above it hold no tie
+                // event, rows equal to it hold #min of them, rows below it (few)
+                // are walked by the block's warp.
+                const int BS = (C + NW - 1) / NW;
+                const int b0 = min(C, warp * BS), b1 = min(C, b0 + BS);
+                {
+                    int bm = TC_BIG;
+                    for (int q = b0 + lane; q < b1; q += 32) bm = min(bm, rec_unpack(rmc[q]).x);
+                    bm = __reduce_min_sync(FULL, bm);
+                    if (lane == 0) ctl.bmin[warp] = bm;
+                }
+                __syncthreads();
+                {
+                    const int binc = warp_incl_min(lane < NW ? ctl.bmin[lane] : TC_BIG, lane);
+                    const int Dg = __shfl_sync(FULL, binc, 31);
+                    int carry = warp == 0 ? TC_BIG : __shfl_sync(FULL, binc, warp - 1);
+                    int tsum = 0, dc = 0, first = INT_MAX;
+                    for (int q0 = b0; q0 < b1; q0 += 32) {
+                        const int q = q0 + lane;
+                        const int2 mc = q < b1 ? rec_unpack(rmc[q]) : make_int2(TC_BIG, 0);
+                        const int x = mc.x;
+                        const int incl = warp_incl_min(x, lane);
                         int excl = __shfl_up_sync(FULL, incl, 1);
                         if (lane == 0) excl = TC_BIG;
-                        int RM = min(carry, excl);
-                        int lowR[R];
-                        unsigned lowbits = 0;
-#pragma unroll
-                        for (int r = 0; r < R; r++) {
-                            const int x = mc[r].x;
-                            const int q = r0 + lane * R + r;
-                            if (x < lmin) {
-                                lmin = x;
-                                lT = mc[r].y;
-                                lfirst = q;
-                            } else if (x == lmin && x != TC_BIG) {
-                                lT += mc[r].y;
-                            }
-                            lowR[r] = RM;
-                            if (!prod && x != TC_BIG) {
-                                if (x == RM) tsum += mc[r].y;
-                                else if (x < RM) lowbits |= 1u << r;
-                            }
-                            RM = min(RM, x);
+                        const int RM = min(carry, excl);
+                        bool low = false;
+                        if (!prod && x != TC_BIG) {
+                            if (x == RM) tsum += mc.y;
+                            else if (x < RM) low = true;
                         }
-                        if (!prod) {
-                            const int cl = __popc(lowbits);
-                            const int ci = warp_incl_sum(cl, lane);
-                            int pos = nlow + ci - cl;
-#pragma unroll
-                            for (int r = 0; r < R; r++)
-                                if ((lowbits >> r) & 1u) lowl[pos++] = rec_pack(lowR[r], r0 + lane * R + r, (Rec *)nullptr);
-                            nlow += __shfl_sync(FULL, ci, 31);
+                        if (x == Dg && x != TC_BIG) {
+                            dc += mc.y;
+                            first = min(first, q);
+                        }
+                        for (unsigned wm = __ballot_sync(FULL, low); wm; wm &= wm - 1) {
+                            const int src = __ffs(wm) - 1;
+                            const int Rs = __shfl_sync(FULL, RM, src);
+                            RE re;
+                            re.init(gamma, texp, tcol, tovf, gstamp, assign, clist[q0 + src], kp, k, it32, thr, s_nib,
+                                    swz_rs, swz_rm);
+                            const int t = re.warp_walk_ties(Rs, lane);
+                            if (lane == 0) tsum += t;
                         }
                         carry = min(carry, __shfl_sync(FULL, incl, 31));
                     }
-                    if (nlow)
-                        tsum += walk_queued<G, S, KQ>(lowl, nlow, gamma, texp, tcol, tovf, gstamp, assign,
-                                                      clist, kp, k, it32, thr, s_nib, swz_rs, swz_rm, lane);
+                    tsum = __reduce_add_sync(FULL, tsum);
+                    dc = __reduce_add_sync(FULL, dc);
+                    first = (int)__reduce_min_sync(FULL, (unsigned)first);
+                    if (lane == 0) {
+                        ctl.bsum[warp] = tsum;
+                        ctl.bD[warp] = dc;
+                        ctl.bfirst[warp] = first;
+                    }
                 }
+                __syncthreads();
                 PH(2);
 
                 // pass 2b (warp 0): reservoir, move, gamma update, conflict list
                 if (warp == 0) {
-                    const int D = carry;
+                    const int D = __reduce_min_sync(FULL, lane < NW ? ctl.bmin[lane] : TC_BIG);
                     int mv_v = -1, mv_a = 0, mv_b = 0, gvb = 0;
                     int64_t s0 = 0, s1 = 0;
                     constexpr int NB = 8;  // neighbour chunks of 32 held in registers
                     int uu[NB];
                     if (D != TC_BIG) {
-                        const int T = __reduce_add_sync(FULL, lmin == D ? lT : 0);
-                        const int L = (int)__reduce_min_sync(FULL, (unsigned)(lmin == D ? lfirst : INT_MAX));
-                        const int total = __reduce_add_sync(FULL, tsum);
+                        const int T = __reduce_add_sync(FULL, lane < NW ? ctl.bD[lane] : 0);
+                        const int L = (int)__reduce_min_sync(FULL, (unsigned)(lane < NW ? ctl.bfirst[lane] : INT_MAX));
+                        const int total = __reduce_add_sync(FULL, lane < NW ? ctl.bsum[lane] : 0);
                         const unsigned long long ctr = ctl.ctr;
                         int sstar = 1;
                         if (T > 1) {
@@ -594,25 +572,30 @@ __global__ void __launch_bounds__(NT, (GSM && sizeof(G) == 1) ? 6 : 1) tabucol_k
                         }
                         PH(3);
                         int row_li = L, need = 1;
-                        if (sstar > 1) {  // rank sstar among the D-candidates in scan order
-                            int cum = 0;
-                            for (int base = 0; base < C; base += 32) {
+                        if (sstar > 1) {  // rank sstar among the D-candidates in scan order:
+                            // its block from the per-warp counts, then the row in the block
+                            const int cj = lane < NW ? ctl.bD[lane] : 0;
+                            const int cin = warp_incl_sum(cj, lane);
+                            const int wb = __ffs(__ballot_sync(FULL, cin >= sstar)) - 1;
+                            int nd = sstar - __shfl_sync(FULL, cin - cj, wb);
+                            const int r0 = min(C, wb * BS), r1 = min(C, r0 + BS);
+                            for (int base = r0; base < r1; base += 32) {
                                 const int li = base + lane;
                                 int c = 0;
-                                if (li < C) {
+                                if (li < r1) {
                                     const int2 mc = rec_unpack(rmc[li]);
                                     c = (mc.x == D) ? mc.y : 0;
                                 }
                                 const int incl = warp_incl_sum(c, lane);
                                 const int tot = __shfl_sync(FULL, incl, 31);
-                                if (cum + tot >= sstar) {
-                                    const unsigned bm = __ballot_sync(FULL, cum + incl >= sstar);
+                                if (tot >= nd) {
+                                    const unsigned bm = __ballot_sync(FULL, incl >= nd);
                                     const int src = __ffs(bm) - 1;
                                     row_li = base + src;
-                                    need = sstar - cum - __shfl_sync(FULL, incl - c, src);
+                                    need = nd - __shfl_sync(FULL, incl - c, src);
                                     break;
                                 }
-                                cum += tot;
+                                nd -= tot;
                             }
                         }
                         // the winner's vertex is known: start its adjacency loads now so
@@ -899,7 +882,7 @@ static size_t misc_bytes(int n, int nt) {
     auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
     const size_t rec = sizeof(S) == 2 ? 4 : 8;
     return a16((size_t)n * 4 * sizeof(S)) + a16((size_t)n * 4) + a16((size_t)n * sizeof(S)) +
-           a16(n) + 2 * a16(2 * (size_t)n) + a16(rec * (size_t)n) + rec * TC_LOWCAP +
+           a16(n) + 2 * a16(2 * (size_t)n) + a16(rec * (size_t)n) +
            a16(2 * (size_t)n) + a16(4 * (size_t)((n + 31) / 32));
 }
 

@@ -10,7 +10,6 @@
 namespace mcb {
 
 constexpr int TC_BIG = 1 << 20;
-constexpr int TC_LOWCAP = 192;
 
 struct TabuParams {
     int32_t *assigns;
