@@ -75,6 +75,7 @@ TABUCOL_CASES = [
     ("k64", 11, 400, 0.85, 64, 4, 3000, 3000, True),
     ("k70", 12, 400, 0.9, 70, 4, 3000, 3000, True),       # k > 64
     ("k150", 13, 700, 0.95, 150, 2, 1500, 1500, True),    # config 5 palette
+    ("c5s", 1, 2000, 0.5, 150, 2, 2000, 2000, True),      # config 4 (C5) shape: the cluster kernel
     ("easy", 14, 80, 0.1, 6, 16, 5000, 5000, True),       # early exits
     ("k1", 15, 30, 0.3, 1, 4, 100, 100, True),            # k < 2: no iterations
     ("edgeless", 16, 40, 0.0, 4, 4, 100, 100, True),      # m = 0
