@@ -473,6 +473,9 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                                (size_t)((it - 1) & 1) * ((n + 31) / 32);
                     const int inc = ctl.inc, mvv = ctl.mv_v, mva = ctl.mv_a, mvb = ctl.mv_b;
                     const int mao = ctl.ma_old, mbo = ctl.mb_old;
+                    // class maxima moved by the last move (rows not adjacent to v* see
+                    // columns a* / b* change only through them)
+                    const bool a_moved = inc == 1 && mao != mx32[mva], b_moved = inc == 1 && mbo != mx32[mvb];
                     // pass 1, rows warp-uniform (chunk = warp + NW j): every row's
                     // (min G, #candidates at it), then the chunk's minimum and multiplicity
                     for (int v0 = warp * 32; v0 < n; v0 += NT) {
@@ -510,6 +513,9 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                         for (int side = 0; side < 2; side++) {
                                             const int x = side ? mvb : mva;
                                             if (x == a) continue;  // the own colour is not a candidate
+                                            // unchanged column: out and in again is a no-op (and
+                                            // would empty a unique minimum group for nothing)
+                                            if (!nb && !(side ? b_moved : a_moved)) continue;
                                             const int gnew = (int)row[x];
                                             const int gold = gnew + (side ? -nb : nb);  // a*: -1, b*: +1 on N(v*)
                                             const int hold = (max(0, wv - (side ? mbo : mao)) << S) + Tt * gold;
