@@ -132,3 +132,23 @@ def test_cluster_dispatch_boundary(n, k, kind):
     buf = ctypes.create_string_buffer(256)
     N.check(N.lib().mcb_tabucol_describe(n, k, 64, buf, 256))
     assert kind in buf.value, buf.value
+
+
+@pytest.mark.parametrize("hot", [0, 9], ids=["rank0-colour", "rank1-colour"])
+def test_cluster_overflow_in_either_half(hot, oracle_lib):
+    """a u8 count overflow seen by one CTA only (colour `hot` lives in rank 0's
+    or rank 1's half at k = 10) stops both CTAs at the same barrier; the
+    individual is re-run by the wide pass and the results match the oracle"""
+    from paper_2109_05948_b200.graph import WeightedGraph
+
+    n, k = 320, 10
+    edges = [(0, v) for v in range(1, n)] + [(v, v + 2) for v in range(1, n - 2, 5)]
+    g = WeightedGraph(n, edges, [1] * n)
+    A = random_col_assigns(n, k, 4, 5)
+    A[:, 1:] = np.where(np.arange(n - 1)[None, :] % 10 == 0, A[:, 1:], hot)  # ~287 leaves coloured `hot` (> 254)
+    A[:, 0] = (hot + 1) % k
+    keys = stream_keys(5, TAG_LS, 0, 4)
+    ref = oracle_lib.tabucol_batch(g, A.copy(), k, keys, 800, log_moves=True, counters=True)
+    got = LS._run_tabucol_batch(g, A.copy(), k, keys, 800, log_moves=True, counters=True,
+                                flags=N.FLAG_FORCE_CLUSTER)
+    _same(got, ref, f"overflow-{hot}")
