@@ -463,6 +463,12 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                 if (fast32 && nch <= 32) {
                     // ================= exact 32-bit path (all arrays int) =================
                     const int S = gm.s, Tt = (int)gm.t;
+                    // 32-bit forms of the iteration scalars (it < 2^32 as the u32 expiries
+                    // assume, conflicts <= m < 2^31; score + ds >= best <=> ds >= room,
+                    // clamping best - score keeps that exact): fewer live registers
+                    const uint32_t it32 = (uint32_t)it;
+                    const int conf32 = (int)min(conflicts, (long long)INT_MAX);
+                    const int room32 = (int)max(min(best - score, (long long)INT_MAX), (long long)INT_MIN);
                     int32_t *r32 = reinterpret_cast<int32_t *>(rmin);  // row minima (numerators)
                     int32_t *c_min = lowq;                           // [32] chunk minima
                     int32_t *c_cnt = lowq + 32;                      // [32] multiplicity at the chunk minimum
@@ -470,7 +476,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                     int32_t *hc_min = r32 + n;                       // row caches (rmin's second half)
                     uint16_t *hc_cnt = reinterpret_cast<uint16_t *>(lowR);
                     const uint32_t *nbr_bits = reinterpret_cast<const uint32_t *>(lowR) + ((size_t)n + 1) / 2 +
-                                               (size_t)((it - 1) & 1) * ((n + 31) / 32);
+                                               (size_t)((it32 - 1u) & 1u) * ((n + 31) / 32);
                     const int inc = ctl.inc, mvv = ctl.mv_v, mva = ctl.mv_a, mvb = ctl.mv_b;
                     const int mao = ctl.ma_old, mbo = ctl.mb_old;
                     // class maxima moved by the last move (rows not adjacent to v* see
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                             rem = (wrk[v] == max_rank[a]) ? (int)uniq_drop[a] : 0;
                             const GT *row = gamma + (size_t)v * k;
                             gva = row[a];
-                            const bool frozen = (uint64_t)it < tabu_until[v];
+                            const bool frozen = it32 < tabu_until[v];
                             wv = wgt[v];
                             if (!frozen) {
                                 // G = (ds << S) + t dc = H_c + K with the row constant
@@ -534,15 +540,14 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                 }
                             } else {
                                 hc_cnt[v] = 0xFFFFu;
-                                if (conflicts <= gva && rem + min(best - score, (long long)INT_MAX) > 0) {
+                                if (conf32 <= gva && (long long)rem + room32 > 0) {
                                     // (a frozen row needs ds = max(0, w - M_c) - rem < best - score:
                                     // impossible when rem + best - score <= 0, e.g. every row
                                     // whose move cannot lower a class maximum at a legal state)
                                     // frozen vertex: only legal moves (dc == -conflicts, reachable
                                     // only if conflicts <= gva) that beat the best legal score
-                                    const int need_dc = -(int)conflicts;
-                                    const long long room = best - score;  // ds < room
-                                    const int dsmax = room > INT_MAX ? INT_MAX : (room < INT_MIN ? INT_MIN : (int)room);
+                                    const int need_dc = -conf32;
+                                    const int dsmax = room32;  // ds < best - score
                                     auto cand = [&](int c) {
                                         const int ds = max(0, wv - mx32[c]) - rem;
                                         if (c != a && ds < dsmax) {
@@ -603,7 +608,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                             }
                         }
                         if (v < n) {
-                            if ((uint64_t)it >= tabu_until[v]) {  // not frozen: the cache and the row minimum
+                            if (it32 >= tabu_until[v]) {  // not frozen: the cache and the row minimum
                                 hc_min[v] = mh;
                                 hc_cnt[v] = (uint16_t)cnt;
                                 m = (mh == INT_MAX) ? INT_MAX : mh - (rem << S) - Tt * gva;
@@ -672,7 +677,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                     // events in colour order, :194-210), spread over the warps
                     {   // the neighbour flags pass 1 read are dead: clear them for the move after next
                         uint32_t *nb_clear = reinterpret_cast<uint32_t *>(lowR) + ((size_t)n + 1) / 2 +
-                                             (size_t)((it - 1) & 1) * ((n + 31) / 32);
+                                             (size_t)((it32 - 1u) & 1u) * ((n + 31) / 32);
                         for (int i = tid; i < (n + 31) / 32; i += NT) nb_clear[i] = 0u;
                     }
                     {
@@ -684,7 +689,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                             const int rem = (wrk[wvx] == max_rank[a]) ? (int)uniq_drop[a] : 0;
                             const GT *row = gamma + (size_t)wvx * k;
                             const int gva = row[a];
-                            const bool frozen = (uint64_t)it < tabu_until[wvx];
+                            const bool frozen = it32 < tabu_until[wvx];
                             const int wv = wgt[wvx];
                             int cr = R;
                             for (int c0 = 0; c0 < k; c0 += 32) {
@@ -693,7 +698,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                 if (c < k && c != a) {
                                     const int dc = (int)row[c] - gva;
                                     const int ds = max(0, wv - mx32[c]) - rem;
-                                    if (!(frozen && (conflicts + dc != 0 || score + ds >= best))) G = (ds << S) + Tt * dc;
+                                    if (!(frozen && (dc != -conf32 || ds >= room32))) G = (ds << S) + Tt * dc;
                                 }
                                 int inc2 = G;
 #pragma unroll
@@ -757,7 +762,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                             const int rem = (wrk[v] == max_rank[a]) ? (int)uniq_drop[a] : 0;
                             const GT *rw = gamma + (size_t)v * k;
                             const int gva = rw[a];
-                            const bool frozen = (uint64_t)it < tabu_until[v];
+                            const bool frozen = it32 < tabu_until[v];
                             const int wv = wgt[v];
                             int cum = 0, b = -1, bds = 0, bdc = 0;
                             for (int c0 = 0; c0 < k && b < 0; c0 += 32) {
@@ -767,7 +772,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                                 if (c < k && c != a) {
                                     dc = (int)rw[c] - gva;
                                     ds = max(0, wv - mx32[c]) - rem;
-                                    if (!(frozen && (conflicts + dc != 0 || score + ds >= best)))
+                                    if (!(frozen && (dc != -conf32 || ds >= room32)))
                                         hit = (ds << S) + Tt * dc == D;
                                 }
                                 const unsigned hm = __ballot_sync(FULL, hit);
@@ -784,7 +789,7 @@ __global__ void __launch_bounds__(WV_NT, 4) wvcp_kernel(WvParams P) {
                             }
                             mv_v = v;
                             WVSP(2);
-                            if (lane == 0) wv_apply_move(v, a, b, bds, bdc, frozen, it, total, score, conflicts);
+                            if (lane == 0) wv_apply_move(v, a, b, bds, bdc, frozen, ctl.it, total, ctl.score, ctl.conflicts);
                             WVSP(3);
                         }
                         if (lane == 0) ctl.has_move = (mv_v >= 0);
