@@ -16,8 +16,12 @@
 //   * every smaller value x = 31..1 is one "level": within a level the
 //     reference visits cells in flat order, i.e. rows ascending and, inside a
 //     row, columns ascending -- so a free row takes its lowest free column
-//     holding x.  The level's cells are scattered into row -> column bitmasks
-//     and one lane walks the free rows holding x with bit operations.
+//     holding x.  A level's cells are row -> column / column -> row bitmasks,
+//     resolved by parallel rounds (pd_level_rounds).  Level 1 -- most nonzero
+//     cells of unrelated colourings -- needs no list or bucket: only the
+//     cells reaching 2 (<= n / 2) are listed and bucketed into levels 2..31,
+//     and level 1, when the matching reaches it, takes its masks from one pass
+//     over the pair's vertices (the vertex of a cell holding exactly 1).
 // Zero cells add nothing to the total, so they are never visited.
 // The job space and the cross/within unranking are the reference's own
 // (:94-113), so ranks shard it by contiguous [job_begin, job_end) ranges.
@@ -29,28 +33,31 @@
 
 namespace mcb {
 
-constexpr int PD_WARPS = 4;
+constexpr int PD_WARPS = 8;
+#ifndef PD_FAST
+#define PD_FAST 1  // levels of <= 32 cells with distinct free rows / columns taken in one step
+#endif
 
 // Per-warp shared tile: the k x k overlap histogram (u8 counters, or u16 when
-// WIDE), the nonzero cells in first-touch order and bucketed by value, the
-// per-level row -> column and column -> row bitmasks, the explicit list of
-// entries >= 32 and the level counters.
+// WIDE); the cells reaching 2 in a compact list, later bucketed by value; the
+// row -> column / column -> row masks of one level at a time; the explicit
+// list of entries >= 32 and the level counters.
 struct PdLayout {
-    size_t hist_words, list_words, big, cmask, uni, per;
+    size_t hist_words, mlist_words, big, cmask, uni, per;
 };
 
 __host__ __device__ inline PdLayout pd_layout(int n, int k, bool wide) {
     PdLayout L;
     const size_t kk = (size_t)k * k;
-    L.hist_words = wide ? (kk + 1) / 2 : (kk + 3) / 4;
-    L.list_words = ((size_t)n + 1) / 2;        // u16 (r << 8 | c) per cell
-    L.big = (size_t)n / 32 + 2;
+    L.hist_words = ((wide ? (kk + 1) / 2 : (kk + 3) / 4) + 3) & ~(size_t)3;  // uint4-clearable
     L.cmask = (size_t)k * ((k + 31) / 32);
-    // the first-touch list is dead once the cells are bucketed; the level
-    // masks are live only after that: one region for both
-    L.uni = L.list_words > 2 * L.cmask ? L.list_words : 2 * L.cmask;
-    // hist + (list | cmask + rmask) + bucket + big + lvbeg[32] + lvcur[32] + rowused/colused[16] + bigcnt
-    L.per = (L.hist_words + L.uni + L.list_words + L.big + 32 + 32 + 16 + 4) * 4;
+    L.mlist_words = ((size_t)n / 2 + 2) / 2;  // u16 (r << 8 | c) per cell >= 2 (<= n / 2 cells)
+    L.big = (size_t)n / 32 + 2;
+    // the multi-cell list is dead once its cells are bucketed; the level masks
+    // are live only after that: one region for both
+    L.uni = L.mlist_words > 2 * L.cmask ? L.mlist_words : 2 * L.cmask;
+    // hist + (mlist | cmask + rmask) + bucket + big + lvbeg[32] + lvcur[32] + rowused/colused[16] + counters
+    L.per = (L.hist_words + L.uni + L.mlist_words + L.big + 32 + 32 + 16 + 4) * 4;
     L.per = (L.per + 15) & ~(size_t)15;
     return L;
 }
@@ -85,6 +92,72 @@ __global__ void pd_to_u8_kernel(const int32_t *__restrict__ src, int64_t rows, i
     if (bad) atomicOr(err, 1);
 }
 
+// One level of the greedy over its row -> column (cm) and column -> row (rm)
+// masks.  The reference visits a level's cells in flat order (rows ascending,
+// then columns ascending): a free row takes its lowest free column.  That
+// greedy equals repeated rounds in which every free row r whose lowest free
+// column c has r as its lowest free row takes (r, c): such a cell precedes
+// every other live cell in its row and column, so the ordered greedy takes it
+// too, and removing it leaves the rest unchanged.  Rows are lanes
+// (r = lane + 32 j).
+template <int KWD>
+__device__ __forceinline__ void pd_level_rounds(const uint32_t *cm, const uint32_t *rm, int k, int lane, int xval,
+                                                uint32_t (&rowused)[KWD], uint32_t (&colused)[KWD],
+                                                long long &total, int &matched, int &bad) {
+    // every round takes the smallest live cell at least, so <= k rounds; more
+    // means inconsistent masks (reported, never an endless loop)
+    for (int round = 0;; round++) {
+        if (round > k) {
+            bad |= 4;
+            break;
+        }
+        bool act = false;
+        int col[KWD];
+#pragma unroll
+        for (int j = 0; j < KWD; j++) {
+            col[j] = -1;
+            const int r = lane + 32 * j;
+            if (r < k && !((rowused[j] >> lane) & 1u)) {
+                int c = -1;
+#pragma unroll
+                for (int w = KWD - 1; w >= 0; w--) {
+                    const uint32_t av = cm[r * KWD + w] & ~colused[w];
+                    if (av) c = 32 * w + __ffs(av) - 1;
+                }
+                if (c >= 0) {
+                    act = true;
+                    int r2 = -1;
+#pragma unroll
+                    for (int w = KWD - 1; w >= 0; w--) {
+                        const uint32_t fr = rm[c * KWD + w] & ~rowused[w];
+                        if (fr) r2 = 32 * w + __ffs(fr) - 1;
+                    }
+                    if (r2 == r) col[j] = c;
+                }
+            }
+        }
+        if (!__any_sync(0xffffffffu, act)) break;
+        int took = 0;
+#pragma unroll
+        for (int j = 0; j < KWD; j++) {
+            const uint32_t tb = __ballot_sync(0xffffffffu, col[j] >= 0);
+            rowused[j] |= tb;
+            took += __popc(tb);
+        }
+#pragma unroll
+        for (int w = 0; w < KWD; w++) {
+            uint32_t mine = 0;
+#pragma unroll
+            for (int j = 0; j < KWD; j++)
+                if (col[j] >= 0 && (col[j] >> 5) == w) mine |= 1u << (col[j] & 31);
+            colused[w] |= __reduce_or_sync(0xffffffffu, mine);
+        }
+        total += (long long)xval * took;
+        matched += took;
+        if (matched >= k) break;
+    }
+}
+
 template <int KWD, bool WIDE>
 __global__ void __launch_bounds__(PD_WARPS * 32)
     pairwise_kernel(const uint8_t *__restrict__ pop, int64_t p, const uint8_t *__restrict__ off,
@@ -95,16 +168,19 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const PdLayout L = pd_layout(n, k, WIDE);
     uint32_t *hist = reinterpret_cast<uint32_t *>(smem + warp * L.per);
-    uint16_t *list = reinterpret_cast<uint16_t *>(hist + L.hist_words);  // shares with cmask / rmask
+    uint16_t *mlist = reinterpret_cast<uint16_t *>(hist + L.hist_words);  // shares with cmask / rmask
     uint32_t *cmask = hist + L.hist_words;  // [k][KWD]: row r -> columns holding the level
     uint32_t *rmask = cmask + L.cmask;      // [k][KWD]: column c -> rows holding the level
     uint16_t *bucket = reinterpret_cast<uint16_t *>(hist + L.hist_words + L.uni);
-    uint32_t *big = reinterpret_cast<uint32_t *>(bucket + 2 * L.list_words);
+    uint32_t *big = reinterpret_cast<uint32_t *>(bucket + 2 * L.mlist_words);
     uint32_t *lvbeg = big + L.big;
     uint32_t *lvcur = lvbeg + 32;
     uint32_t *s_used = lvcur + 32;   // rowused[8], colused[8] (entries >= 32 only)
     uint32_t *bigcnt = s_used + 16;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    // clearing the histogram: whole tile (uint4) when it is small, else the
+    // words the pair's vertices touched
+    const bool bulk_clear = L.hist_words <= 4 * (size_t)n;
 
     for (size_t i = lane; i < L.hist_words; i += 32) hist[i] = 0u;
     __syncwarp();
@@ -136,8 +212,8 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
         }
         lvbeg[lane] = 0u;
         if (lane == 0) *bigcnt = 0u;
-        // overlap histogram (4 vertices per 32-bit load); the first touch of
-        // a cell appends it to the list
+        // overlap histogram (4 vertices per 32-bit load): the second increment
+        // of a cell appends it to the multi-vertex list
         int bad = 0, m = 0;
         const int nw = (n + 3) >> 2;
         for (int w0 = 0; w0 < nw; w0 += 32) {
@@ -149,18 +225,18 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
             }
 #pragma unroll
             for (int b = 0; b < 4; b++) {
-                bool first = false;
+                bool second = false;
                 const uint32_t a = (xa >> (8 * b)) & 0xFFu, c = (yb >> (8 * b)) & 0xFFu;
                 if (4 * w + b < n) {
                     const int code = (int)a * k + (int)c;
                     const uint32_t sh = WIDE ? 16 * (code & 1) : 8 * (code & 3);
                     const uint32_t old = atomicAdd(&hist[WIDE ? code >> 1 : code >> 2], 1u << sh);
                     const uint32_t was = (old >> sh) & (WIDE ? 0xFFFFu : 0xFFu);
-                    first = was == 0u;
+                    second = was == 1u;
                     if (!WIDE && was == 0xFFu) bad |= 2;  // u8 counter overflow
                 }
-                const uint32_t bm = __ballot_sync(0xffffffffu, first);
-                if (first) list[m + __popc(bm & lt_mask)] = (uint16_t)((a << 8) | c);
+                const uint32_t bm = __ballot_sync(0xffffffffu, second);
+                if (second) mlist[m + __popc(bm & lt_mask)] = (uint16_t)((a << 8) | c);
                 m += __popc(bm);
             }
         }
@@ -173,10 +249,11 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
             continue;
         }
         __syncwarp();
-        // values: count each level; entries >= 32 go to the explicit list
+        // multi-vertex cells: count each level; entries >= 32 go to the
+        // explicit list
         uint32_t levels = 0;
         for (int i = lane; i < m; i += 32) {
-            const uint32_t e = list[i];
+            const uint32_t e = mlist[i];
             const int flat = (int)(e >> 8) * k + (int)(e & 0xFFu);
             const uint32_t val = hist_get<WIDE>(hist, flat);
             if (val >= 32) {
@@ -190,26 +267,28 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
         }
         levels = __reduce_or_sync(0xffffffffu, levels);
         __syncwarp();
-        {   // bucket offsets: exclusive prefix over the 32 level counts
-            const uint32_t c = lvbeg[lane];
-            uint32_t inc = c;
+        if (levels & ~3u) {
+            {   // bucket offsets: exclusive prefix over the 32 level counts
+                const uint32_t c = lvbeg[lane];
+                uint32_t inc = c;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += t;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += t;
+                }
+                lvbeg[lane] = inc - c;
+                lvcur[lane] = inc - c;
             }
-            lvbeg[lane] = inc - c;
-            lvcur[lane] = inc - c;
+            __syncwarp();
+            for (int i = lane; i < m; i += 32) {
+                const uint32_t e = mlist[i];
+                const uint32_t val = hist_get<WIDE>(hist, (int)(e >> 8) * k + (int)(e & 0xFFu));
+                if (val < 32) bucket[atomicAdd(&lvcur[val], 1u)] = (uint16_t)e;
+            }
+            // the multi list is dead: its region becomes the (zeroed) level masks
+            __syncwarp();
+            for (size_t i = lane; i < 2 * L.cmask; i += 32) cmask[i] = 0u;
         }
-        __syncwarp();
-        for (int i = lane; i < m; i += 32) {
-            const uint32_t e = list[i];
-            const uint32_t val = hist_get<WIDE>(hist, (int)(e >> 8) * k + (int)(e & 0xFFu));
-            if (val < 32) bucket[atomicAdd(&lvcur[val], 1u)] = (uint16_t)e;
-        }
-        // the list is dead: its region becomes the (zeroed) level masks
-        __syncwarp();
-        for (size_t i = lane; i < 2 * L.cmask; i += 32) cmask[i] = 0u;
         __syncwarp();
         uint32_t rowused[KWD], colused[KWD];
 #pragma unroll
@@ -221,8 +300,8 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
             if (lane < 16) s_used[lane] = 0u;
             __syncwarp();
             if (lane == 0) {
-                const int nb = (int)*bigcnt;
-                for (int a = 1; a < nb; a++) {
+                const int nbg = (int)*bigcnt;
+                for (int a = 1; a < nbg; a++) {
                     const uint32_t t = big[a];
                     int b = a - 1;
                     while (b >= 0 && big[b] < t) {
@@ -231,7 +310,7 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
                     }
                     big[b + 1] = t;
                 }
-                for (int a = 0; a < nb && matched < k; a++) {
+                for (int a = 0; a < nbg && matched < k; a++) {
                     const uint32_t t = big[a];
                     const int flat = 0xFFFF - (int)(t & 0xFFFFu);
                     const int r = flat / k, c = flat % k;
@@ -253,79 +332,97 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
             }
         }
         __syncwarp();
-        // levels 31..1.  Within a level the reference visits cells in flat
-        // order (rows ascending, then columns ascending).  That greedy equals
-        // repeated rounds in which every free row r whose lowest free column c
-        // (at this level) has r as its lowest free row takes (r, c): such a
-        // cell precedes every other live cell in its row and column, so the
-        // ordered greedy takes it too, and removing it leaves the rest of the
-        // greedy unchanged.  Rows are lanes (r = lane + 32 j).
-        uint32_t lv = levels & ~1u;
+        // levels 31..2 from their buckets (each level's masks cleared after
+        // it, so the region stays zero), then level 1
+        uint32_t lv = levels & ~3u;
         while (lv && matched < k) {
             const int xval = 31 - __clz(lv);
             lv &= ~(1u << xval);
             const int beg = (int)lvbeg[xval], end = (int)lvcur[xval];
-            for (int i = beg + lane; i < end; i += 32) {
-                const uint32_t e = bucket[i];
-                const int r = (int)(e >> 8), c = (int)(e & 0xFFu);
-                atomicOr(&cmask[r * KWD + (c >> 5)], 1u << (c & 31));
-                atomicOr(&rmask[c * KWD + (r >> 5)], 1u << (r & 31));
-            }
-            __syncwarp();
-            while (true) {
-                bool act = false;
-                int col[KWD];
+            bool fast = false;
+            if (PD_FAST && end - beg <= 32) {
+                // few cells (related colourings: the level's large cells):
+                // when its free cells have pairwise distinct rows and columns,
+                // the ordered greedy takes every one of them
+                int r = -1, c = -1;
+                if (beg + lane < end) {
+                    const uint32_t e = bucket[beg + lane];
+                    const int rr = (int)(e >> 8), cc = (int)(e & 0xFFu);
+                    bool fr = false, fc = false;
 #pragma unroll
-                for (int j = 0; j < KWD; j++) {
-                    col[j] = -1;
-                    const int r = lane + 32 * j;
-                    if (r < k && !((rowused[j] >> lane) & 1u)) {
-                        int c = -1;
-#pragma unroll
-                        for (int w = KWD - 1; w >= 0; w--) {
-                            const uint32_t av = cmask[r * KWD + w] & ~colused[w];
-                            if (av) c = 32 * w + __ffs(av) - 1;
-                        }
-                        if (c >= 0) {
-                            act = true;
-                            int r2 = -1;
-#pragma unroll
-                            for (int w = KWD - 1; w >= 0; w--) {
-                                const uint32_t fr = rmask[c * KWD + w] & ~rowused[w];
-                                if (fr) r2 = 32 * w + __ffs(fr) - 1;
-                            }
-                            if (r2 == r) col[j] = c;
-                        }
+                    for (int w = 0; w < KWD; w++) {
+                        if ((rr >> 5) == w) fr = !((rowused[w] >> (rr & 31)) & 1u);
+                        if ((cc >> 5) == w) fc = !((colused[w] >> (cc & 31)) & 1u);
+                    }
+                    if (fr && fc) {
+                        r = rr;
+                        c = cc;
                     }
                 }
-                if (!__any_sync(0xffffffffu, act)) break;
-                int took = 0;
-#pragma unroll
-                for (int j = 0; j < KWD; j++) {
-                    const uint32_t tb = __ballot_sync(0xffffffffu, col[j] >= 0);
-                    rowused[j] |= tb;
-                    took += __popc(tb);
-                }
+                const int nlive = __popc(__ballot_sync(0xffffffffu, r >= 0));
+                uint32_t rb[KWD], cb[KWD];
+                int nr = 0, nc = 0;
 #pragma unroll
                 for (int w = 0; w < KWD; w++) {
-                    uint32_t mine = 0;
-#pragma unroll
-                    for (int j = 0; j < KWD; j++)
-                        if (col[j] >= 0 && (col[j] >> 5) == w) mine |= 1u << (col[j] & 31);
-                    colused[w] |= __reduce_or_sync(0xffffffffu, mine);
+                    rb[w] = __reduce_or_sync(0xffffffffu, (r >= 0 && (r >> 5) == w) ? 1u << (r & 31) : 0u);
+                    cb[w] = __reduce_or_sync(0xffffffffu, (c >= 0 && (c >> 5) == w) ? 1u << (c & 31) : 0u);
+                    nr += __popc(rb[w]);
+                    nc += __popc(cb[w]);
                 }
-                total += (long long)xval * took;
-                matched += took;
-                if (matched >= k) break;
+                if (nr == nlive && nc == nlive) {
+#pragma unroll
+                    for (int w = 0; w < KWD; w++) {
+                        rowused[w] |= rb[w];
+                        colused[w] |= cb[w];
+                    }
+                    total += (long long)xval * nlive;
+                    matched += nlive;
+                    fast = true;
+                }
             }
-            for (int i = beg + lane; i < end; i += 32) {
-                const uint32_t e = bucket[i];
-                const int r = (int)(e >> 8), c = (int)(e & 0xFFu);
-                cmask[r * KWD + (c >> 5)] = 0u;
-                rmask[c * KWD + (r >> 5)] = 0u;
+            if (!fast) {
+                for (int i = beg + lane; i < end; i += 32) {
+                    const uint32_t e = bucket[i];
+                    const int r = (int)(e >> 8), c = (int)(e & 0xFFu);
+                    atomicOr(&cmask[r * KWD + (c >> 5)], 1u << (c & 31));
+                    atomicOr(&rmask[c * KWD + (r >> 5)], 1u << (r & 31));
+                }
+                __syncwarp();
+                pd_level_rounds<KWD>(cmask, rmask, k, lane, xval, rowused, colused, total, matched, bad);
+                for (int i = beg + lane; i < end; i += 32) {
+                    const uint32_t e = bucket[i];
+                    const int r = (int)(e >> 8), c = (int)(e & 0xFFu);
+                    cmask[r * KWD + (c >> 5)] = 0u;
+                    rmask[c * KWD + (r >> 5)] = 0u;
+                }
             }
             __syncwarp();
         }
+        if (matched < k) {
+            // level 1, only when reached (pairs of related colourings are
+            // matched by their large cells): a vertex whose cell holds exactly
+            // 1 is that cell's only vertex, so one pass over the pair's
+            // vertices sets the level's masks
+            if (!(levels & ~3u)) {
+                for (size_t i = lane; i < 2 * L.cmask; i += 32) cmask[i] = 0u;  // still holds the multi list
+                __syncwarp();
+            }
+            for (int w = lane; w < nw; w += 32) {
+                const uint32_t xa = __ldg(reinterpret_cast<const uint32_t *>(x) + w);
+                const uint32_t yb = __ldg(reinterpret_cast<const uint32_t *>(y) + w);
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const int r = (int)((xa >> (8 * b)) & 0xFFu), c = (int)((yb >> (8 * b)) & 0xFFu);
+                    if (4 * w + b < n && hist_get<WIDE>(hist, r * k + c) == 1u) {
+                        atomicOr(&cmask[r * KWD + (c >> 5)], 1u << (c & 31));
+                        atomicOr(&rmask[c * KWD + (r >> 5)], 1u << (r & 31));
+                    }
+                }
+            }
+            __syncwarp();
+            pd_level_rounds<KWD>(cmask, rmask, k, lane, 1, rowused, colused, total, matched, bad);
+        }
+        if (bad && lane == 0) atomicOr(err, bad);
         const int d = n - (int)total;
         if (lane == 0) {
             if (jobs16) {
@@ -337,17 +434,24 @@ __global__ void __launch_bounds__(PD_WARPS * 32)
                 within[oj * q + oi] = d;
             }
         }
-        // reset the warp's histogram for the next pair: only its nonzero cells,
-        // i.e. the level buckets and the entries >= 32
-        const int nbk = (int)lvcur[31], nbig = (int)*bigcnt;
-        for (int i = lane; i < nbk; i += 32) {
-            const uint32_t e = bucket[i];
-            const int flat = (int)(e >> 8) * k + (int)(e & 0xFFu);
-            hist[WIDE ? flat >> 1 : flat >> 2] = 0u;
-        }
-        for (int i = lane; i < nbig; i += 32) {
-            const int flat = 0xFFFF - (int)(big[i] & 0xFFFFu);
-            hist[WIDE ? flat >> 1 : flat >> 2] = 0u;
+        // reset the histogram for the next pair: whole, or through the pair's
+        // vertices (the mask region is zeroed before its next use)
+        __syncwarp();
+        if (bulk_clear) {
+            uint4 *h4 = reinterpret_cast<uint4 *>(hist);
+            for (size_t i = lane; i < L.hist_words / 4; i += 32) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+        } else {
+            for (int w = lane; w < nw; w += 32) {
+                const uint32_t xa = __ldg(reinterpret_cast<const uint32_t *>(x) + w);
+                const uint32_t yb = __ldg(reinterpret_cast<const uint32_t *>(y) + w);
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    if (4 * w + b < n) {
+                        const int code = (int)((xa >> (8 * b)) & 0xFFu) * k + (int)((yb >> (8 * b)) & 0xFFu);
+                        hist[WIDE ? code >> 1 : code >> 2] = 0u;
+                    }
+                }
+            }
         }
         __syncwarp();
     }
@@ -402,17 +506,34 @@ int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, i
     // (possible only when n >= 256) is re-run with u16 counters
     for (int wide = 0; wide < 2; wide++) {
         const PdLayout L = pd_layout((int)n, (int)k, wide);
-        // warps per block: as many of PD_WARPS as shared memory holds
-        int warps = PD_WARPS;
-        while (warps > 1 && (size_t)warps * L.per > (size_t)max_smem_optin()) warps >>= 1;
-        const size_t smem = warps * L.per;
-        if (smem > (size_t)max_smem_optin())
-            return set_error(MCB_ERR_UNSUPPORTED, "pairwise: k too large for shared memory");
         const PdKernel kern = wide ? pd_pick<true>((int)(k + 31) / 32) : pd_pick<false>((int)(k + 31) / 32);
+        // warps per block: the count (<= PD_WARPS) with the most warps resident
+        // per SM (the per-block shared-memory reservation makes the best count
+        // depend on the tile size)
+        int warps = 0, per_sm = 0, dev = 0;
+        cudaGetDevice(&dev);
+        static thread_local struct { PdKernel kern; size_t per; int dev, warps, per_sm; } memo = {nullptr, 0, -1, 0, 0};
+        if (memo.kern == kern && memo.per == L.per && memo.dev == dev) {
+            warps = memo.warps;
+            per_sm = memo.per_sm;
+        }
+        for (int w = warps ? PD_WARPS + 1 : 1; w <= PD_WARPS; w++) {
+            const size_t sm_w = w * L.per;
+            if (sm_w > (size_t)max_smem_optin()) break;
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w) != cudaSuccess)
+                return set_error(MCB_ERR_CUDA, "pairwise: smem attribute failed");
+            int b = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, w * 32, sm_w);
+            if (w * b >= warps * per_sm) {
+                warps = w;
+                per_sm = b;
+            }
+        }
+        if (warps == 0) return set_error(MCB_ERR_UNSUPPORTED, "pairwise: k too large for shared memory");
+        memo = {kern, L.per, dev, warps, per_sm};
+        const size_t smem = warps * L.per;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return set_error(MCB_ERR_CUDA, "pairwise: smem attribute failed");
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
         per_sm = std::max(per_sm, 1);
         const int64_t jobs = job_end - job_begin;
         const int grid = (int)std::min<int64_t>((jobs + warps - 1) / warps, (int64_t)per_sm * num_sms());
@@ -425,6 +546,7 @@ int pairwise_run(const int32_t *pop, int64_t p, const int32_t *off, int64_t q, i
             return set_error(MCB_ERR_CUDA, "pairwise kernel failed: %s",
                              cudaGetErrorString(cudaGetLastError()));
         if (herr & 1) return set_error(MCB_ERR_RANGE, "pairwise: color id out of range [0, k)");
+        if (herr & 4) return set_error(MCB_ERR_CUDA, "pairwise: internal error (greedy rounds did not converge)");
         if (!(herr & 2)) break;
         cudaMemsetAsync(err, 0, 4, st);
     }

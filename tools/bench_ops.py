@@ -89,6 +89,17 @@ def bench_distance(a):
     n, k, p = 1000, 83, a.dist_pop
     P = random_col_assigns(n, k, p, 1)
     Q = random_col_assigns(n, k, p, 2)
+    if a.dist_related:
+        # LS-like related pairs (a converged GA population): every colouring
+        # is one base colouring under its own colour permutation with a
+        # fraction of the vertices recoloured
+        rng = np.random.default_rng(5)
+        base = P[0].copy()
+        for M in (P, Q):
+            for i in range(p):
+                M[i] = rng.permutation(k).astype(P.dtype)[base]
+                flip = rng.random(n) < a.dist_related
+                M[i, flip] = rng.integers(0, k, int(flip.sum()))
     pd, qd = torch.from_numpy(P).cuda(), torch.from_numpy(Q).cuda()
     cross = torch.zeros((p, p), dtype=torch.int32, device="cuda")
     within = torch.zeros((p, p), dtype=torch.int32, device="cuda")
@@ -101,7 +112,7 @@ def bench_distance(a):
     tc = time.perf_counter() - t0
     return {"op": "distance", "unit": "pairs/s", "gpu": pairs / t,
             "cpu": (pc * pc + pc * (pc - 1) // 2) / tc, "cores": cores,
-            "config": f"n={n} k={k} p=q={p} (random colourings)", "cpu_sample": f"p=q={pc}",
+            "config": f"n={n} k={k} p=q={p} " + (f"(related pairs, {a.dist_related:.0%} recoloured)" if a.dist_related else "(random colourings)"), "cpu_sample": f"p=q={pc}",
             "gpu_ms": 1e3 * t, "alg_bytes_per_pair": 6 * n}
 
 
@@ -249,6 +260,7 @@ def main():
     ap.add_argument("--wvcp-depth", type=int, default=500)
     ap.add_argument("--gpx-pop", type=int, default=16384)
     ap.add_argument("--dist-pop", type=int, default=4096)
+    ap.add_argument("--dist-related", type=float, default=0.0, help="recoloured fraction of related pairs (0: random)")
     ap.add_argument("--pop-p", type=int, default=16384)
     a = ap.parse_args()
     N.lib()
