@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
             }
         }
         __syncwarp();
-        long long conflicts, best;
+        int conflicts, best;  // <= n (n - 1) / 2 < 2^19 (n <= 1024): 32-bit on the chain
         int C = 0;
         {
             long long c2 = 0;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                 C += __popc(bal);
             }
             c2 = warp_sum64(c2);
-            conflicts = c2 / 2;
+            conflicts = (int)(c2 / 2);
             best = conflicts;
         }
         if (__any_sync(FULLM, rangeerr) && lane == 0) atomicExch(P.err_flag, 1);
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                 if constexpr (stats) ph_t = clock64();
                 WST(WS_IT, 1);
                 const uint32_t it32 = (uint32_t)it;
-                const int thr = (int)max(best - conflicts, (long long)-TW_BIG);
+                const int thr = max(best - conflicts, -TW_BIG);
 
                 // ---- tabu expiry: it < tabu[v,c] fails from it == expiry on
                 if (nrows > 0 && (int)(next_exp - it32) <= 0) {
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                     const int tot = prod ? 0 : __reduce_add_sync(FULLM, total);
                     WPH(WS_CY_P2);
                     // tenure draw (:363-365), issued early so it overlaps the reservoir
-                    const long long nconf = conflicts + D;
+                    const int nconf = conflicts + D;
                     uint32_t ll;
                     if (!prod) ll = u64_below32(key, ctr + (unsigned long long)tot, 10u);
                     else ll = philox_below(key, ctr + 1, 10u);
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                     // ---- move, tenure, tabu entry (:352-366)
                     conflicts = nconf;
                     ctr += prod ? 2ull : (unsigned long long)tot + 1ull;
-                    const long long tt = (long long)ll + (6LL * conflicts) / 10LL;
+                    const int tt = (int)ll + (6 * conflicts) / 10;
                     if (tt >= 8190) {
                         bad = true;
                         break;
