@@ -54,7 +54,7 @@ def test_vertex_limits_raise():
     assert (a[:, :-1] != a[:, 1:]).all() and (used <= 3).all()
 
 
-def test_shared_state_limits_raise_cleanly():
+def test_shared_state_limits_raise_cleanly(oracle_lib):
     """WVCP and distances whose per-individual / per-pair shared-memory state
     cannot fit: a ValueError naming the limit, not a CUDA failure."""
     g = _path_graph(40000, wmax=3)
@@ -62,9 +62,18 @@ def test_shared_state_limits_raise_cleanly():
     A[0, 1::2] = 1
     with pytest.raises(ValueError, match="shared memory"):
         LS._run_wvcp_batch(g, A, 3, stream_keys(1, TAG_LS, 0, 1), 5, 1, True, 1.0)
-    P = random_col_assigns(60000, 200, 1, 2)
+    # distances list only the cells reaching 2 (<= n / 2): n = 60000, k = 200
+    # fits, u16 counters included (classes of ~300 vertices overflow u8)
+    P = random_col_assigns(60000, 200, 2, 2)
+    c, w = DI.pairwise_distances(P, P, k=200)
+    rc, rw = oracle_lib.pairwise(P, P, 200)
+    np.testing.assert_array_equal(c, rc)
+    np.testing.assert_array_equal(w, rw)
+    # u16 counters at n = 65535, k = 255 (~270 KB per pair) do not fit
+    P = random_col_assigns(65535, 255, 1, 3)
+    P[0, :600] = 0  # a class of >= 600 vertices: the u16 re-run is needed
     with pytest.raises(ValueError, match="shared memory"):
-        DI.pairwise_distances(P, P, k=200)
+        DI.pairwise_distances(P, P, k=255)
 
 
 @pytest.mark.parametrize("n,pe,k", [(1000, 0.9, 222), (1000, 0.5, 234)], ids=["dsjc1000.9-like", "r1000.5-like"])

@@ -128,3 +128,34 @@ def test_distance_structured_vs_oracle(n, k, oracle_lib):
     rc, rw = oracle_lib.pairwise(P, Q, k)
     np.testing.assert_array_equal(c, rc)
     np.testing.assert_array_equal(w, rw)
+
+
+@pytest.mark.parametrize("k,noise", [(48, 0.02), (83, 0.1), (83, 0.3), (150, 0.05)])
+def test_distance_converged_population_vs_oracle(k, noise, oracle_lib):
+    """A converged population (every member one base colouring under its own
+    colour permutation, a fraction recoloured): levels of a few large cells,
+    taken in one step when their free cells have distinct rows and columns.
+    Merged classes (two base colours onto one) and split classes (one base
+    colour over two) put several cells of a level in one row or column, so
+    the same pairs also take the round-based path."""
+    n = 1000
+    rs = np.random.default_rng(k + int(1000 * noise))
+    base = random_col_assigns(n, k, 1, k)[0]
+    M = np.empty((14, n), np.int32)
+    for i in range(14):
+        x = rs.permutation(k)[base]
+        if i % 3 == 1:  # merge two classes
+            a, b = rs.choice(k, 2, replace=False)
+            x[x == a] = b
+        if i % 3 == 2:  # split a class
+            a = int(rs.integers(k))
+            idx = np.flatnonzero(x == a)
+            x[idx[::2]] = (a + 1) % k
+        flip = rs.random(n) < noise
+        x[flip] = rs.integers(0, k, int(flip.sum()))
+        M[i] = x
+    P, Q = M[:6], M[6:]
+    c, w = DI.pairwise_distances(P, Q, k=k)
+    rc, rw = oracle_lib.pairwise(P, Q, k)
+    np.testing.assert_array_equal(c, rc)
+    np.testing.assert_array_equal(w, rw)
