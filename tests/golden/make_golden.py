@@ -20,6 +20,8 @@ inputs, the outputs of the reference's own hot-path kernels:
 * surrogate.npz SurrogateNet init / gradients / online training / predictions (`surrogate.py`)
 * engine.npz    k-colouring generations without the surrogate, chained from the
                 reference's own operators as `engine.py:_generation_loop` does
+* improve.npz   improve_population LsResults, COL and WVCP, generations > 0 and
+                the default depths (`localsearch.py:615-682`)
 
 Inputs are regenerated in the tests from the recorded parameters with the
 package's own generators (which are themselves pinned by graphs.npz and the
@@ -538,6 +540,45 @@ def gen_surrogate(out):
     out["cases"] = np.array([c[0] for c in SURROGATE_CASES])
 
 
+# name, mode, seed, n, edge p, wmax, k, pop, generation, depth (0: default), max_rounds
+IMPROVE_CASES = [
+    ("col_g0", "col", 21, 120, 0.5, 1, 14, 6, 0, 3000, 0),
+    ("col_g3", "col", 22, 200, 0.3, 1, 10, 5, 3, 5000, 0),
+    ("col_default_depth", "col", 24, 60, 0.5, 1, 9, 4, 1, 0, 0),
+    ("wvcp_g2", "wvcp", 23, 80, 0.4, 20, 12, 4, 2, 300, 3),
+    ("wvcp_default", "wvcp", 25, 50, 0.5, 10, 10, 3, 0, 0, 2),
+]
+
+
+def gen_improve(out):
+    """improve_population (`localsearch.py:615-682`): keys from the master
+    seed and the generation, LsResult fields per individual."""
+    meta = []
+    for name, mode, seed, n, pe, wmax, k, pop, gen, depth, rounds in IMPROVE_CASES:
+        g = ref_rand_graph(seed, n, pe, wmax=wmax)
+        assert np.array_equal(g.edges, rand_graph(seed, n, pe, wmax=wmax).edges), name
+        A = random_col_assigns(n, k, pop, seed)
+        cols = [RColoring(A[i].copy(), k) for i in range(pop)]
+        kw = {"depth": depth or None}
+        if mode == "wvcp":
+            kw["max_rounds"] = rounds
+        res = RLS.improve_population(g, cols, RLS.WVCP if mode == "wvcp" else RLS.COL, seed, gen, **kw)
+        pre = f"{name}__"
+        out[pre + "params"] = np.array([seed, n, int(pe * 1000), wmax, k, pop, gen, depth, rounds], np.int64)
+        out[pre + "mode"] = np.array([mode])
+        out[pre + "init_digest"] = np.array([digest(A)])
+        out[pre + "best"] = np.stack([r.best.assign for r in res]).astype(np.uint8)
+        out[pre + "end"] = np.stack([r.end.assign for r in res]).astype(np.uint8)
+        out[pre + "best_score"] = np.array([r.best_score for r in res], np.int64)
+        out[pre + "iterations_used"] = np.array([r.iterations_used for r in res], np.int64)
+        out[pre + "legal_found"] = np.array([r.legal_found for r in res], bool)
+        if mode == "wvcp":
+            out[pre + "phi"] = np.array([list(r.phi_trajectory) for r in res], np.float64)
+        meta.append(name)
+        print("improve", name, [r.best_score for r in res], [r.iterations_used for r in res])
+    out["cases"] = np.array(meta)
+
+
 def main():
     """python make_golden.py [name ...]  (default: every fixture)"""
     os.makedirs(HERE, exist_ok=True)
@@ -545,7 +586,7 @@ def main():
     for fn, name in [(gen_rng, "rng"), (gen_graphs, "graphs"), (gen_tabucol, "tabucol"),
                      (gen_wvcp, "wvcp"), (gen_gpx, "gpx"), (gen_distance, "distance"),
                      (gen_population, "population"), (gen_engine, "engine"), (gen_init, "init"),
-                     (gen_surrogate, "surrogate")]:
+                     (gen_surrogate, "surrogate"), (gen_improve, "improve")]:
         if only and name not in only:
             continue
         out = {}
