@@ -105,7 +105,18 @@ __device__ __forceinline__ void pd_level_rounds(const uint32_t *cm, const uint32
                                                 uint32_t (&rowused)[KWD], uint32_t (&colused)[KWD],
                                                 long long &total, int &matched, int &bad) {
     // every round takes the smallest live cell at least, so <= k rounds; more
-    // means inconsistent masks (reported, never an endless loop)
+    // means inconsistent masks (reported, never an endless loop).  A row's
+    // column words do not change during the level: in registers for k <= 128
+    constexpr bool CACHE = KWD <= 4;
+    uint32_t cmr[CACHE ? KWD : 1][CACHE ? KWD : 1];
+    if constexpr (CACHE) {
+#pragma unroll
+        for (int j = 0; j < KWD; j++) {
+            const int r = lane + 32 * j;
+#pragma unroll
+            for (int w = 0; w < KWD; w++) cmr[j][w] = r < k ? cm[r * KWD + w] : 0u;
+        }
+    }
     for (int round = 0;; round++) {
         if (round > k) {
             bad |= 4;
@@ -121,7 +132,7 @@ __device__ __forceinline__ void pd_level_rounds(const uint32_t *cm, const uint32
                 int c = -1;
 #pragma unroll
                 for (int w = KWD - 1; w >= 0; w--) {
-                    const uint32_t av = cm[r * KWD + w] & ~colused[w];
+                    const uint32_t av = (CACHE ? cmr[CACHE ? j : 0][CACHE ? w : 0] : cm[r * KWD + w]) & ~colused[w];
                     if (av) c = 32 * w + __ffs(av) - 1;
                 }
                 if (c >= 0) {
