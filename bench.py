@@ -549,7 +549,8 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "int32",
         "data": "synthetic",
-        "config": workload_config(wl, depth, world) | {"D": D},
+        # the same config object as the reference arm's (D only when --pop overrides it)
+        "config": workload_config(wl, depth, world) | ({"D": D} if D != WORKLOADS[wl][6] else {}),
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                      "frac": achieved / smem_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": desc.value.decode(),
