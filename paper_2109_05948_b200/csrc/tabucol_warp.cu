@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                 // ---- tabu expiry: it < tabu[v,c] fails from it == expiry on
                 if (nrows > 0 && (int)(next_exp - it32) <= 0) {
                     // some entry may expire now (next_exp is a lower bound)
-                    int last = -1;
+                    int last = -1;  // this lane's last live row; one reduction after the rows
                     uint32_t dmin = 0x4000u;
 #pragma unroll
                     for (int j = 0; j < KE; j++) {
@@ -359,11 +359,13 @@ __global__ void __launch_bounds__(32 * TW_MAX_WARPS, 1) tabucol_warp_kernel(Warp
                         }
                         ring[j] = hit ? 0u : e;
                         const bool live = (ring[j] >> 31) != 0u;
-                        if (live) dmin = min(dmin, dist);
-                        if (__any_sync(FULLM, live)) last = j;
+                        if (live) {
+                            dmin = min(dmin, dist);
+                            last = j;
+                        }
                     }
                     WST(WS_EXPIRE_ROWS, nrows);
-                    nrows = last + 1;
+                    nrows = __reduce_max_sync(FULLM, last) + 1;
                     next_exp = it32 + __reduce_min_sync(FULLM, dmin);
                     __syncwarp();
                 }
